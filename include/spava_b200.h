@@ -1,0 +1,195 @@
+/* spava_b200.h -- C ABI of the B200-native Spava sequence-parallel prefill path.
+ *
+ * Drop-in boundary for the reference's C++ operator API (namespace seqpar,
+ * /root/reference/proj/core/include/seqpar/{partition,approx,attention}.hpp).
+ * Every entry point below names the reference interface it replaces.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Tensors are token-major row-major
+ *    [rows x heads*dh]; "ld" arguments are row strides in ELEMENTS.
+ *    Q/K/V/passing blocks are bf16 in device memory (dh = 128); scores are f32.
+ *  - Heads: q-head h reads kv-head h / (hq/hkv) (GQA).  The reference has no
+ *    GQA; hq == hkv reproduces it exactly.
+ *  - Every function returns a spava_status; on failure spava_last_error()
+ *    (thread-local) describes it.  No C++ exception crosses this ABI.  The
+ *    reference's std::invalid_argument maps to SPAVA_EINVAL, std::out_of_range
+ *    to SPAVA_ERANGE, std::runtime_error to SPAVA_ERUNTIME.
+ *  - Device work is asynchronous on the caller's stream (cudaStream_t passed as
+ *    void*; NULL = legacy default stream).  Caller owns all buffers.
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point fails with SPAVA_ECUDA.
+ */
+#ifndef SPAVA_B200_H
+#define SPAVA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SPAVA_OK = 0,
+  SPAVA_EINVAL = 1,   /* std::invalid_argument in the reference */
+  SPAVA_ERANGE = 2,   /* std::out_of_range                       */
+  SPAVA_ERUNTIME = 3, /* std::runtime_error                      */
+  SPAVA_ECUDA = 4,    /* CUDA failure / no sm_100 device          */
+  SPAVA_ENCCL = 5     /* NCCL failure                             */
+} spava_status;
+
+const char* spava_last_error(void);
+const char* spava_version(void);
+/* 1 if a CUDA device of compute capability 10.x is visible. */
+int spava_device_ok(void);
+
+/* ------------------------------------------------------------------ plan
+ * BlockPlan / HostTopology (partition.hpp:13-45).                          */
+typedef struct {
+  int n_v;           /* video context length                      */
+  int n_t;           /* query length                              */
+  int hosts;         /* physical hosts H                          */
+  int l_a;           /* anchor length                             */
+  int l_b;           /* per-virtual-block length incl. pad        */
+  int l_p;           /* essential KVs passed per block            */
+  int pad;           /* zero rows appended to the context         */
+  int virtual_hosts; /* 2H                                        */
+  int zigzag;        /* 1: pairs (h, 2H-1-h); 0: naive (2h, 2h+1) */
+} spava_plan;
+
+/* split_context geometry (partition.cpp:40-85); zigzag_map/naive_map (:21-29). */
+int spava_make_plan(int n_v, int n_t, int hosts, int l_a, int l_p, int zigzag, spava_plan* out);
+/* default_plan (partition.cpp:96-113): l_a = n/64, l_p = min(n/128, l_b). */
+int spava_default_plan(int n, int hosts, spava_plan* out);
+/* HostTopology::virtual_pair (partition.cpp:9-13) */
+int spava_virtual_pair(const spava_plan* plan, int h, int* lo, int* hi);
+/* HostTopology::physical_of (partition.cpp:15-19) */
+int spava_physical_of(const spava_plan* plan, int v, int* h);
+/* slice_anchor (partition.cpp:87-94) */
+int spava_slice_anchor(int l_a, int hosts, int h, int* begin, int* end);
+/* BlockPlan::block_offset / query_offset (partition.hpp:35-36) */
+int spava_block_offset(const spava_plan* plan, int v);
+int spava_query_offset(const spava_plan* plan);
+/* ContextSplit::pad_mask[v] (partition.cpp:71-79) -> l_b bytes, 1 = pad row */
+int spava_pad_mask(const spava_plan* plan, int v, uint8_t* mask_out);
+/* number of non-pad rows of virtual block v */
+int spava_block_valid_rows(const spava_plan* plan, int v);
+/* assemble_passing (approx.cpp:104-132) in exchange-slot terms: the sources < v
+ * arrive in round 0 (lo blocks, pass1) slots [r0_begin, r0_end) and round 1
+ * (hi blocks, pass2) slots [r1_begin, r1_end) of the host-ordered allgather.   */
+int spava_passing_ranges(const spava_plan* plan, int v, int* r0_begin, int* r0_end,
+                         int* r1_begin, int* r1_end);
+
+/* --------------------------------------------------------------- scoring
+ * score_block (simhost.cpp:209-224) -> score_context (approx.cpp:15-69),
+ * softmax or raw-logit aggregation, "exact" arithmetic.
+ * q: [n_t x ldq] bf16, k: [l_b x ldk] bf16, pad: device u8[l_b] or NULL,
+ * keys j >= n_valid are pads too.  scores: device f32[l_b] (pads -> -inf).  */
+size_t spava_score_workspace(int n_t, int l_b, int hq);
+int spava_score_block(const void* q, int64_t ldq, int n_t, const void* k, int64_t ldk, int l_b,
+                      const uint8_t* pad, int n_valid, int hq, int hkv, int dh, int softmax,
+                      float* scores, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------- select + pack
+ * select_essential (approx.cpp:71-102): top-l_p by score, ties -> lower index,
+ * non-finite never selected, indices ascending (+global_offset) in idx_out;
+ * K/V rows gathered into k_out/v_out (ld_out; rows >= count zero-filled).
+ * count_out, status_out: device int32 (status 1 = NaN score rejected).       */
+int spava_select_pack(const float* scores, int l_b, int l_p, int global_offset, const void* k,
+                      const void* v, int64_t ld, int width, int32_t* idx_out, void* k_out,
+                      void* v_out, int64_t ld_out, int32_t* count_out, int32_t* status_out,
+                      void* stream);
+
+/* ----------------------------------------------------------- attention
+ * attention_lse / mha_lse (attention.cpp:18-86, 158-178) over a segment table
+ * (KeySegment, attention.hpp:16-23).  Key j of a segment is visible to query
+ * row i iff j < rows and (!causal || j <= i) -- pads are a shorter `rows`.
+ * Used for anchor_attention (approx.cpp:134-138), block_attention (:140-154)
+ * and query_attention (:156-188).  out: [nq x ldo] bf16 (out_f32=0) or f32;
+ * lse (nullable): [nq x hq] f32, natural log, -inf for rows with no key.
+ * splits > 1 computes split-KV partials internally and merges them (needs
+ * workspace of spava_attention_workspace bytes).                            */
+typedef struct {
+  const void* k; /* bf16 [rows x ld], kv head h at columns [h*dh, (h+1)*dh) */
+  const void* v;
+  int64_t ld;
+  int rows;
+  int causal; /* MaskKind::CausalWithin (requires rows <= nq) */
+} spava_segment;
+
+size_t spava_attention_workspace(int nq, int hq, int dh, int splits);
+int spava_attention(const void* q, int64_t ldq, int nq, const spava_segment* segs, int nseg,
+                    int hq, int hkv, int dh, void* out, int64_t ldo, int out_f32, float* lse,
+                    int splits, void* workspace, size_t workspace_bytes, void* stream);
+
+/* --------------------------------------------------------------- merge
+ * mha_merge (attention.cpp:180-197) over nparts partials in host order.
+ * outs[p]: device f32 [rows x ld_part], lses[p]: device f32 [rows x hq]
+ * (host arrays of device pointers).  dst: bf16 or f32 [rows x ld_dst];
+ * dst_lse (nullable) receives the merged lse.  status: device int32, set to 1
+ * if a row is invalid in every part (the reference throws).                  */
+int spava_mha_merge(int nparts, const float* const* outs, const float* const* lses, int rows,
+                    int64_t ld_part, int hq, int dh, void* dst, int64_t ld_dst, int dst_f32,
+                    float* dst_lse, int32_t* status, void* stream);
+
+/* ---------------------------------------------------------- the layer
+ * One Spava attention layer of physical host h: the body of run_host's
+ * per-layer loop (simhost.cpp:321-426) minus projections/FFN.
+ *
+ * Host-local device buffers, token-major rows
+ *   [ anchor (l_a) | block lo (l_b) | block hi (l_b) | query (n_t) ]
+ * q: hq*dh columns, k/v: hkv*dh columns (bf16).  out: same rows, hq*dh bf16
+ * (anchor_attention, block_attention lo/hi, merged query attention).
+ * sel: int32 [2 x l_p] global indices of the lo/hi passing blocks (may be NULL).
+ *
+ * The exchange (GatherFabric, simhost.cpp:61-166) is a spava_fabric:
+ *  - local: H simulated hosts on ONE device, exchange buffers shared in place
+ *    (the reference's in-process mailbox); drive with spava_sim_layer.
+ *  - nccl: one process per GPU; pass1/pass2/qpartial are in-place
+ *    ncclAllGather on a dedicated comm stream, overlapped per Algorithm 1.  */
+typedef struct {
+  int n_v, n_t, hosts, l_a, l_p;
+  int zigzag;         /* HostTopology pairing                                 */
+  int designated;     /* host carrying query self keys; -1 = last (simhost.cpp:276) */
+  int query_self_all; /* SimOptions::query_self_all_hosts                     */
+  int softmax_scores; /* SimOptions::softmax_scores                           */
+  int hq, hkv, dh;
+  int query_splits;   /* split-KV factor of query attention; 0 = auto         */
+} spava_layer_cfg;
+
+typedef struct spava_fabric spava_fabric;
+typedef struct spava_host spava_host;
+
+int spava_fabric_create_local(const spava_layer_cfg* cfg, int device, spava_fabric** out);
+/* unique_id: 128-byte ncclUniqueId from spava_nccl_unique_id on rank 0. */
+int spava_nccl_unique_id(void* unique_id_128);
+int spava_fabric_create_nccl(const spava_layer_cfg* cfg, int device, const void* unique_id_128,
+                             int world, int rank, spava_fabric** out);
+int spava_fabric_destroy(spava_fabric* fab);
+
+int spava_host_create(spava_fabric* fab, int h, spava_host** out);
+int spava_host_destroy(spava_host* host);
+int spava_host_plan(const spava_host* host, spava_plan* out);
+/* rows of the host-local buffers: l_a + 2*l_b + n_t */
+int spava_host_rows(const spava_host* host);
+
+/* NCCL fabric: the whole layer of this rank, exchange overlapped.            */
+int spava_host_layer(spava_host* host, const void* q, const void* k, const void* v, void* out,
+                     int32_t* sel, void* stream);
+/* Local fabric: every host of the fabric, phase by phase, on one stream.
+ * q/k/v/out/sel are arrays of H per-host pointers (host arrays).            */
+int spava_sim_layer(spava_fabric* fab, spava_host* const* hosts, const void* const* q,
+                    const void* const* k, const void* const* v, void* const* out,
+                    int32_t* const* sel, void* stream);
+/* Device-side status word of the last layer (0 ok; non-zero: NaN score or a
+ * merge row invalid everywhere).  Synchronises the given stream.            */
+int spava_host_status(spava_host* host, void* stream, int32_t* status_out);
+
+/* Number of kernels the library launched since process start (for bench's
+ * gpu_launches claim). */
+uint64_t spava_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPAVA_B200_H */

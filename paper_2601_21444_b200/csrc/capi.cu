@@ -1,0 +1,847 @@
+// capi.cu -- the C ABI (include/spava_b200.h) and the per-layer runtime.
+//
+// The runtime is the B200 form of the reference's per-host layer schedule
+// (run_host, simhost.cpp:317-437; Algorithm 1):
+//   score(lo), score(hi) -> select+pack(lo) -> pass1 -------------------------.
+//                        -> select+pack(hi) -> pass2 ---------------------.   |
+//   query_attn(anchor slice | lo | hi | [self]) -> qpartial ---> merge     |   |
+//   stage1 = anchor_self + block(lo)   (waits pass1; pass2 too if naive) <-+---'
+//   stage2 = block(hi)                 (waits pass1 + pass2)
+// The GatherFabric (simhost.cpp:61-166) becomes a spava_fabric:
+//   local -> H simulated hosts on one device; the select+pack kernel of host h writes its
+//            slot of a shared exchange buffer, so the allgather is free (in place);
+//   nccl  -> one process per GPU; in-place ncclAllGather of the packed slots on a
+//            dedicated comm stream, cudaEvent edges implementing the DAG above.
+// The attention stages never copy the passing KV: the kernel's segment table points
+// straight into the exchange buffers (assemble_passing, approx.cpp:104-132, is free).
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/spava_b200.h"
+#include "spava_internal.h"
+
+using namespace spava;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU_TRY(expr)                                                                  \
+  do {                                                                                \
+    cudaError_t _e = (expr);                                                          \
+    if (_e != cudaSuccess)                                                            \
+      return fail(SPAVA_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));   \
+  } while (0)
+
+#define NCCL_TRY(expr)                                                                \
+  do {                                                                                \
+    ncclResult_t _r = (expr);                                                         \
+    if (_r != ncclSuccess)                                                            \
+      return fail(SPAVA_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));   \
+  } while (0)
+
+#define ST_TRY(expr)              \
+  do {                            \
+    int _s = (expr);              \
+    if (_s != SPAVA_OK) return _s; \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+bool device_ok_impl() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) return false;
+  int dev = 0, major = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess)
+    return false;
+  return major == 10;
+}
+
+int require_device() {
+  if (!device_ok_impl())
+    return fail(SPAVA_ECUDA, "no sm_100 (B200) CUDA device visible: the Spava path has no CPU fallback");
+  return SPAVA_OK;
+}
+
+// -------------------------------------------------------------------- plan
+int plan_impl(int n_v, int n_t, int hosts, int l_a, int l_p, int zigzag, spava_plan* out) {
+  if (!out) return fail(SPAVA_EINVAL, "plan: null output");
+  if (hosts < 1) return fail(SPAVA_EINVAL, "split_context: need at least one host");
+  if (l_a < 0 || l_a >= n_v)
+    return fail(SPAVA_EINVAL, "split_context: anchor length must satisfy 0 <= l_a < n_v");
+  if (n_t < 0) return fail(SPAVA_EINVAL, "split_context: negative query length");
+  const int vh = 2 * hosts;
+  const int rem = n_v - l_a;
+  const int pad = (vh - rem % vh) % vh;
+  const int l_b = (rem + pad) / vh;
+  if (l_p < 0 || l_p > l_b) return fail(SPAVA_EINVAL, "split_context: l_p must lie in [0, l_b]");
+  *out = spava_plan{n_v, n_t, hosts, l_a, l_b, l_p, pad, vh, zigzag ? 1 : 0};
+  return SPAVA_OK;
+}
+
+int valid_rows(const spava_plan& p, int v) {
+  const int start = p.l_a + v * p.l_b;
+  return std::max(0, std::min(p.l_b, p.n_v - start));
+}
+
+// slots of exchange round r (0 = lo blocks, 1 = hi blocks) whose virtual source < v
+void passing_range(const spava_plan& p, int round, int v, int* s0, int* s1) {
+  const int H = p.hosts;
+  if (p.zigzag) {
+    if (round == 0) {
+      *s0 = 0;
+      *s1 = std::min(v, H);
+    } else {
+      *s0 = std::max(0, 2 * H - v);
+      *s1 = H;
+    }
+  } else {
+    *s0 = 0;
+    *s1 = round == 0 ? (v + 1) / 2 : v / 2;
+  }
+  if (*s1 < *s0) *s1 = *s0;
+}
+
+}  // namespace
+
+// ============================================================ exchange + host
+struct Exchange {
+  void* passK[2] = {nullptr, nullptr};  // [H*l_p x hkv*dh] bf16
+  void* passV[2] = {nullptr, nullptr};
+  int32_t* passIdx[2] = {nullptr, nullptr};  // [H*l_p]
+  int32_t* passCnt[2] = {nullptr, nullptr};  // [H]
+  float* qOut = nullptr;                     // [H x n_t x hq*dh]
+  float* qLse = nullptr;                     // [H x n_t x hq]
+  void* base = nullptr;
+
+  int alloc(const spava_layer_cfg& c, const spava_plan& p) {
+    const size_t H = p.hosts, dk = static_cast<size_t>(c.hkv) * c.dh, dq = static_cast<size_t>(c.hq) * c.dh;
+    const size_t lp = std::max(p.l_p, 1);
+    const size_t kv = H * lp * dk * 2;
+    const size_t idx = H * lp * 4;
+    const size_t cnt = 256;
+    const size_t qo = H * std::max(p.n_t, 1) * dq * 4;
+    const size_t ql = H * std::max(p.n_t, 1) * c.hq * 4;
+    auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+    const size_t total = 2 * (2 * al(kv) + al(idx) + al(cnt)) + al(qo) + al(ql);
+    CU_TRY(cudaMalloc(&base, total));
+    CU_TRY(cudaMemset(base, 0, total));
+    uint8_t* b = static_cast<uint8_t*>(base);
+    for (int r = 0; r < 2; ++r) {
+      passK[r] = b; b += al(kv);
+      passV[r] = b; b += al(kv);
+      passIdx[r] = reinterpret_cast<int32_t*>(b); b += al(idx);
+      passCnt[r] = reinterpret_cast<int32_t*>(b); b += al(cnt);
+    }
+    qOut = reinterpret_cast<float*>(b); b += al(qo);
+    qLse = reinterpret_cast<float*>(b);
+    return SPAVA_OK;
+  }
+  void release() {
+    if (base) cudaFree(base);
+    base = nullptr;
+  }
+};
+
+struct spava_fabric {
+  spava_layer_cfg cfg{};
+  spava_plan plan{};
+  int device = 0;
+  bool nccl = false;
+  int world = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  Exchange shared;  // local mode
+};
+
+struct spava_host {
+  spava_fabric* fab = nullptr;
+  int h = 0, v_lo = 0, v_hi = 0, a0 = 0, a1 = 0;
+  bool self_keys = false;
+  int splits = 1;
+  Exchange own;       // nccl mode (per rank)
+  Exchange* ex = nullptr;
+  float* scores[2] = {nullptr, nullptr};
+  void* score_ws = nullptr;
+  size_t score_ws_bytes = 0;
+  float* qsplit_out = nullptr;
+  float* qsplit_lse = nullptr;
+  int32_t* status = nullptr;
+  void* base = nullptr;
+  cudaEvent_t ev[6] = {};  // pass1_ready, pass2_ready, q_ready, pass1_done, pass2_done, q_done
+};
+
+namespace {
+
+int cfg_check(const spava_layer_cfg* c, spava_plan* plan) {
+  if (!c) return fail(SPAVA_EINVAL, "layer: null cfg");
+  ST_TRY(plan_impl(c->n_v, c->n_t, c->hosts, c->l_a, c->l_p, c->zigzag, plan));
+  if (c->dh != kHeadDim) return fail(SPAVA_EINVAL, "layer: only dh == 128 is implemented");
+  if (c->hq < 1 || c->hkv < 1 || c->hq % c->hkv || c->hq > 32)
+    return fail(SPAVA_EINVAL, "layer: need hkv | hq and hq <= 32");
+  if (c->n_t < 1) return fail(SPAVA_EINVAL, "layer: empty query (score_context rejects it)");
+  if (plan->pad > plan->l_b)
+    return fail(SPAVA_EINVAL,
+                "layer: degenerate plan (pad > l_b puts pad rows in a passing source block)");
+  if (c->hosts > kMaxMergeParts) return fail(SPAVA_EINVAL, "layer: too many hosts");
+  return SPAVA_OK;
+}
+
+// -------------------------------------------------------- op wrappers
+int attention_impl(const ProbView* pv, int np, int hq, int hkv, int dh, cudaStream_t st) {
+  std::string err;
+  cudaError_t e = launch_attention(pv, np, hq, hkv, dh, st, &err);
+  if (e != cudaSuccess)
+    return fail(e == cudaErrorInvalidValue ? SPAVA_EINVAL : SPAVA_ECUDA,
+                err.empty() ? std::string("attention: ") + cudaGetErrorString(e) : err);
+  g_launches += 1;
+  return SPAVA_OK;
+}
+
+int merge_impl(const MergeParams& mp, cudaStream_t st) {
+  cudaError_t e = launch_merge(mp, st);
+  if (e != cudaSuccess) return fail(SPAVA_ECUDA, std::string("merge: ") + cudaGetErrorString(e));
+  g_launches += 1;
+  return SPAVA_OK;
+}
+
+int auto_splits(int nq, int hq, int total_keys) {
+  const int units = (nq + 255) / 256;
+  const int tiles = std::max(1, (total_keys + kBlockN - 1) / kBlockN);
+  int s = (2 * 148 + hq * units - 1) / (hq * units);
+  s = std::min(s, tiles);
+  s = std::min(s, 32);
+  return std::max(1, s);
+}
+
+// ---------------------------------------------------------- layer phases
+struct HostBufs {
+  const uint8_t* q;
+  const uint8_t* k;
+  const uint8_t* v;
+  uint8_t* out;
+  int32_t* sel;
+};
+
+inline const void* row_ptr(const uint8_t* base, long long row, long long ld) {
+  return base + row * ld * 2;
+}
+
+// score + select + pack (lo then hi) into this host's exchange slots
+int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record) {
+  const spava_fabric& F = *H->fab;
+  const spava_layer_cfg& c = F.cfg;
+  const spava_plan& p = F.plan;
+  const long long dq = static_cast<long long>(c.hq) * c.dh, dk = static_cast<long long>(c.hkv) * c.dh;
+  const long long qrow = p.l_a + 2LL * p.l_b;
+  const int vs[2] = {H->v_lo, H->v_hi};
+  for (int r = 0; r < 2; ++r) {
+    const long long krow = p.l_a + static_cast<long long>(r) * p.l_b;
+    const int nvalid = valid_rows(p, vs[r]);
+    cudaError_t e = launch_score_exact(row_ptr(b.q, qrow, dq), dq, p.n_t, row_ptr(b.k, krow, dk), dk,
+                                       p.l_b, nullptr, nvalid, c.hq, c.hkv, c.dh, c.softmax_scores,
+                                       H->scores[r], H->score_ws, H->score_ws_bytes, st);
+    if (e != cudaSuccess) return fail(SPAVA_ECUDA, std::string("score: ") + cudaGetErrorString(e));
+    g_launches += c.softmax_scores ? 3 : 2;
+    const long long slot = static_cast<long long>(H->h) * p.l_p;
+    int32_t* idx_out = H->ex->passIdx[r] + slot;
+    e = launch_select_pack(H->scores[r], p.l_b, p.l_p, p.l_a + vs[r] * p.l_b, row_ptr(b.k, krow, dk),
+                           row_ptr(b.v, krow, dk), dk, static_cast<int>(dk), idx_out,
+                           static_cast<uint8_t*>(H->ex->passK[r]) + slot * dk * 2,
+                           static_cast<uint8_t*>(H->ex->passV[r]) + slot * dk * 2, dk,
+                           H->ex->passCnt[r] + H->h, H->status, st);
+    if (e != cudaSuccess) return fail(SPAVA_ECUDA, std::string("select: ") + cudaGetErrorString(e));
+    g_launches += p.l_p > 0 ? 2 : 1;
+    if (b.sel && p.l_p > 0)
+      CU_TRY(cudaMemcpyAsync(b.sel + r * p.l_p, idx_out, sizeof(int32_t) * p.l_p,
+                             cudaMemcpyDeviceToDevice, st));
+    if (record) CU_TRY(cudaEventRecord(H->ev[r], st));
+  }
+  return SPAVA_OK;
+}
+
+// per-host partial query attention (split-KV, merged over splits) into its qpartial slot
+int phase_query(spava_host* H, const HostBufs& b, cudaStream_t st, bool record) {
+  const spava_fabric& F = *H->fab;
+  const spava_layer_cfg& c = F.cfg;
+  const spava_plan& p = F.plan;
+  const long long dq = static_cast<long long>(c.hq) * c.dh, dk = static_cast<long long>(c.hkv) * c.dh;
+  const long long qrow = p.l_a + 2LL * p.l_b;
+  ProbView pv{};
+  pv.q = row_ptr(b.q, qrow, dq);
+  pv.ldq = dq;
+  pv.nq = p.n_t;
+  int n = 0;
+  if (H->a1 > H->a0)
+    pv.seg[n++] = SegView{row_ptr(b.k, H->a0, dk), row_ptr(b.v, H->a0, dk), dk, H->a1 - H->a0, 0};
+  for (int r = 0; r < 2; ++r) {
+    const int nv = valid_rows(p, r == 0 ? H->v_lo : H->v_hi);
+    const long long krow = p.l_a + static_cast<long long>(r) * p.l_b;
+    if (nv > 0) pv.seg[n++] = SegView{row_ptr(b.k, krow, dk), row_ptr(b.v, krow, dk), dk, nv, 0};
+  }
+  if (H->self_keys)
+    pv.seg[n++] = SegView{row_ptr(b.k, qrow, dk), row_ptr(b.v, qrow, dk), dk, p.n_t, 1};
+  pv.nseg = n;
+  float* dst_out = H->ex->qOut + static_cast<long long>(H->h) * p.n_t * dq;
+  float* dst_lse = H->ex->qLse + static_cast<long long>(H->h) * p.n_t * c.hq;
+  if (H->splits <= 1) {
+    pv.out = dst_out;
+    pv.ldo = dq;
+    pv.out_f32 = 1;
+    pv.lse = dst_lse;
+    pv.ld_lse = c.hq;
+    pv.splits = 1;
+    ST_TRY(attention_impl(&pv, 1, c.hq, c.hkv, c.dh, st));
+  } else {
+    pv.out = H->qsplit_out;
+    pv.ldo = dq;
+    pv.out_f32 = 1;
+    pv.lse = H->qsplit_lse;
+    pv.ld_lse = c.hq;
+    pv.splits = H->splits;
+    pv.split_stride_out = static_cast<long long>(p.n_t) * dq;
+    pv.split_stride_lse = static_cast<long long>(p.n_t) * c.hq;
+    ST_TRY(attention_impl(&pv, 1, c.hq, c.hkv, c.dh, st));
+    MergeParams mp{};
+    mp.nparts = H->splits;
+    for (int s = 0; s < H->splits; ++s) {
+      mp.out[s] = H->qsplit_out + s * pv.split_stride_out;
+      mp.lse[s] = H->qsplit_lse + s * pv.split_stride_lse;
+    }
+    mp.rows = p.n_t;
+    mp.hq = c.hq;
+    mp.dh = c.dh;
+    mp.ld_part = dq;
+    mp.ld_lse = c.hq;
+    mp.dst = dst_out;
+    mp.ld_dst = dq;
+    mp.dst_f32 = 1;
+    mp.dst_lse = dst_lse;
+    mp.status = nullptr;  // query partials may legitimately be empty rows
+    ST_TRY(merge_impl(mp, st));
+  }
+  if (record) CU_TRY(cudaEventRecord(H->ev[2], st));
+  return SPAVA_OK;
+}
+
+ProbView block_problem(spava_host* H, const HostBufs& b, int which) {
+  const spava_fabric& F = *H->fab;
+  const spava_layer_cfg& c = F.cfg;
+  const spava_plan& p = F.plan;
+  const long long dq = static_cast<long long>(c.hq) * c.dh, dk = static_cast<long long>(c.hkv) * c.dh;
+  const int v = which == 0 ? H->v_lo : H->v_hi;
+  const long long row = p.l_a + static_cast<long long>(which) * p.l_b;
+  ProbView pv{};
+  pv.q = row_ptr(b.q, row, dq);
+  pv.ldq = dq;
+  pv.nq = p.l_b;
+  int n = 0;
+  if (p.l_a > 0) pv.seg[n++] = SegView{b.k, b.v, dk, p.l_a, 0};
+  for (int r = 0; r < 2; ++r) {
+    int s0, s1;
+    passing_range(p, r, v, &s0, &s1);
+    if (s1 > s0 && p.l_p > 0)
+      pv.seg[n++] = SegView{static_cast<uint8_t*>(H->ex->passK[r]) + static_cast<long long>(s0) * p.l_p * dk * 2,
+                            static_cast<uint8_t*>(H->ex->passV[r]) + static_cast<long long>(s0) * p.l_p * dk * 2,
+                            dk, (s1 - s0) * p.l_p, 0};
+  }
+  const int nv = valid_rows(p, v);
+  pv.seg[n++] = SegView{row_ptr(b.k, row, dk), row_ptr(b.v, row, dk), dk, nv, 1};
+  pv.nseg = n;
+  pv.out = b.out + row * dq * 2;
+  pv.ldo = dq;
+  pv.out_f32 = 0;
+  pv.splits = 1;
+  return pv;
+}
+
+ProbView anchor_problem(spava_host* H, const HostBufs& b) {
+  const spava_layer_cfg& c = H->fab->cfg;
+  const spava_plan& p = H->fab->plan;
+  const long long dq = static_cast<long long>(c.hq) * c.dh, dk = static_cast<long long>(c.hkv) * c.dh;
+  ProbView pv{};
+  pv.q = b.q;
+  pv.ldq = dq;
+  pv.nq = p.l_a;
+  pv.nseg = 1;
+  pv.seg[0] = SegView{b.k, b.v, dk, p.l_a, 1};
+  pv.out = b.out;
+  pv.ldo = dq;
+  pv.splits = 1;
+  return pv;
+}
+
+// needs pass1 (and pass2 under naive pairing)
+int phase_stage1(spava_host* H, const HostBufs& b, cudaStream_t st) {
+  const spava_layer_cfg& c = H->fab->cfg;
+  ProbView pv[2] = {block_problem(H, b, 0), anchor_problem(H, b)};  // heavier first
+  return attention_impl(pv, H->fab->plan.l_a > 0 ? 2 : 1, c.hq, c.hkv, c.dh, st);
+}
+
+int phase_stage2(spava_host* H, const HostBufs& b, cudaStream_t st) {
+  const spava_layer_cfg& c = H->fab->cfg;
+  ProbView pv = block_problem(H, b, 1);
+  return attention_impl(&pv, 1, c.hq, c.hkv, c.dh, st);
+}
+
+int phase_merge(spava_host* H, const HostBufs& b, cudaStream_t st) {
+  const spava_layer_cfg& c = H->fab->cfg;
+  const spava_plan& p = H->fab->plan;
+  const long long dq = static_cast<long long>(c.hq) * c.dh;
+  MergeParams mp{};
+  mp.nparts = p.hosts;
+  for (int g = 0; g < p.hosts; ++g) {
+    mp.out[g] = H->ex->qOut + static_cast<long long>(g) * p.n_t * dq;
+    mp.lse[g] = H->ex->qLse + static_cast<long long>(g) * p.n_t * c.hq;
+  }
+  mp.rows = p.n_t;
+  mp.hq = c.hq;
+  mp.dh = c.dh;
+  mp.ld_part = dq;
+  mp.ld_lse = c.hq;
+  mp.dst = b.out + (p.l_a + 2LL * p.l_b) * dq * 2;
+  mp.ld_dst = dq;
+  mp.dst_f32 = 0;
+  mp.status = H->status;
+  return merge_impl(mp, st);
+}
+
+int nccl_round(spava_fabric* F, Exchange* ex, int r) {
+  const spava_plan& p = F->plan;
+  const size_t dk = static_cast<size_t>(F->cfg.hkv) * F->cfg.dh;
+  const size_t n_kv = static_cast<size_t>(p.l_p) * dk * 2;  // bytes per slot
+  uint8_t* K = static_cast<uint8_t*>(ex->passK[r]);
+  uint8_t* V = static_cast<uint8_t*>(ex->passV[r]);
+  uint8_t* I = reinterpret_cast<uint8_t*>(ex->passIdx[r]);
+  uint8_t* C = reinterpret_cast<uint8_t*>(ex->passCnt[r]);
+  NCCL_TRY(ncclGroupStart());
+  NCCL_TRY(ncclAllGather(K + F->rank * n_kv, K, n_kv, ncclUint8, F->comm, F->comm_stream));
+  NCCL_TRY(ncclAllGather(V + F->rank * n_kv, V, n_kv, ncclUint8, F->comm, F->comm_stream));
+  NCCL_TRY(ncclAllGather(I + F->rank * p.l_p * 4, I, static_cast<size_t>(p.l_p) * 4, ncclUint8, F->comm,
+                         F->comm_stream));
+  NCCL_TRY(ncclAllGather(C + F->rank * 4, C, 4, ncclUint8, F->comm, F->comm_stream));
+  NCCL_TRY(ncclGroupEnd());
+  return SPAVA_OK;
+}
+
+int nccl_qround(spava_fabric* F, Exchange* ex) {
+  const spava_plan& p = F->plan;
+  const size_t dq = static_cast<size_t>(F->cfg.hq) * F->cfg.dh;
+  const size_t no = static_cast<size_t>(p.n_t) * dq * 4, nl = static_cast<size_t>(p.n_t) * F->cfg.hq * 4;
+  uint8_t* O = reinterpret_cast<uint8_t*>(ex->qOut);
+  uint8_t* L = reinterpret_cast<uint8_t*>(ex->qLse);
+  NCCL_TRY(ncclGroupStart());
+  NCCL_TRY(ncclAllGather(O + F->rank * no, O, no, ncclUint8, F->comm, F->comm_stream));
+  NCCL_TRY(ncclAllGather(L + F->rank * nl, L, nl, ncclUint8, F->comm, F->comm_stream));
+  NCCL_TRY(ncclGroupEnd());
+  return SPAVA_OK;
+}
+
+}  // namespace
+
+// ================================================================= C ABI
+extern "C" {
+
+const char* spava_last_error(void) { return g_err.c_str(); }
+const char* spava_version(void) { return "spava-b200 0.1 (sm_100a)"; }
+int spava_device_ok(void) { return device_ok_impl() ? 1 : 0; }
+uint64_t spava_kernel_launches(void) { return g_launches.load(); }
+
+int spava_make_plan(int n_v, int n_t, int hosts, int l_a, int l_p, int zigzag, spava_plan* out) {
+  return plan_impl(n_v, n_t, hosts, l_a, l_p, zigzag, out);
+}
+
+int spava_default_plan(int n, int hosts, spava_plan* out) {
+  if (n < 128) return fail(SPAVA_EINVAL, "default_plan: n must be at least 128");
+  if (hosts < 1) return fail(SPAVA_EINVAL, "default_plan: need at least one host");
+  const int l_a = n / 64, vh = 2 * hosts, rem = n - l_a;
+  const int pad = (vh - rem % vh) % vh;
+  const int l_b = (rem + pad) / vh;
+  if (l_b == 0) return fail(SPAVA_EINVAL, "default_plan: n too small for nonempty blocks");
+  *out = spava_plan{n, 0, hosts, l_a, l_b, std::min(n / 128, l_b), pad, vh, 1};
+  return SPAVA_OK;
+}
+
+int spava_virtual_pair(const spava_plan* p, int h, int* lo, int* hi) {
+  if (!p || h < 0 || h >= p->hosts) return fail(SPAVA_ERANGE, "virtual_pair: host index");
+  if (p->zigzag) {
+    *lo = h;
+    *hi = 2 * p->hosts - 1 - h;
+  } else {
+    *lo = 2 * h;
+    *hi = 2 * h + 1;
+  }
+  return SPAVA_OK;
+}
+
+int spava_physical_of(const spava_plan* p, int v, int* h) {
+  if (!p || v < 0 || v >= 2 * p->hosts) return fail(SPAVA_ERANGE, "physical_of: virtual index");
+  *h = p->zigzag ? (v < p->hosts ? v : 2 * p->hosts - 1 - v) : v / 2;
+  return SPAVA_OK;
+}
+
+int spava_slice_anchor(int l_a, int hosts, int h, int* begin, int* end) {
+  if (h < 0 || h >= hosts) return fail(SPAVA_ERANGE, "slice_anchor: host index");
+  const int base = l_a / hosts, extra = l_a % hosts;
+  *begin = h * base + std::min(h, extra);
+  *end = *begin + base + (h < extra ? 1 : 0);
+  return SPAVA_OK;
+}
+
+int spava_block_offset(const spava_plan* p, int v) { return p->l_a + v * p->l_b; }
+int spava_query_offset(const spava_plan* p) { return p->l_a + p->virtual_hosts * p->l_b; }
+int spava_block_valid_rows(const spava_plan* p, int v) { return valid_rows(*p, v); }
+
+int spava_passing_ranges(const spava_plan* p, int v, int* r0b, int* r0e, int* r1b, int* r1e) {
+  if (!p || v < 0 || v >= p->virtual_hosts) return fail(SPAVA_ERANGE, "passing_ranges: virtual index");
+  passing_range(*p, 0, v, r0b, r0e);
+  passing_range(*p, 1, v, r1b, r1e);
+  return SPAVA_OK;
+}
+
+int spava_pad_mask(const spava_plan* p, int v, uint8_t* mask) {
+  if (!p || v < 0 || v >= p->virtual_hosts) return fail(SPAVA_ERANGE, "pad_mask: virtual index");
+  for (int r = 0; r < p->l_b; ++r) mask[r] = (p->l_a + v * p->l_b + r) >= p->n_v ? 1 : 0;
+  return SPAVA_OK;
+}
+
+size_t spava_score_workspace(int n_t, int l_b, int hq) { return score_workspace_bytes(n_t, l_b, hq); }
+
+int spava_score_block(const void* q, int64_t ldq, int n_t, const void* k, int64_t ldk, int l_b,
+                      const uint8_t* pad, int n_valid, int hq, int hkv, int dh, int softmax,
+                      float* scores, void* ws, size_t ws_bytes, void* stream) {
+  if (n_t < 1) return fail(SPAVA_EINVAL, "score_context: empty query");
+  if (dh != kHeadDim || hq < 1 || hkv < 1 || hq % hkv || hq > 32)
+    return fail(SPAVA_EINVAL, "score_block: need dh == 128, hkv | hq, hq <= 32");
+  if (ldq % 8 || ldk % 8) return fail(SPAVA_EINVAL, "score_block: row strides must be multiples of 8");
+  if (ws_bytes < score_workspace_bytes(n_t, l_b, hq))
+    return fail(SPAVA_EINVAL, "score_block: workspace too small");
+  ST_TRY(require_device());
+  cudaError_t e = launch_score_exact(q, ldq, n_t, k, ldk, l_b, pad, n_valid, hq, hkv, dh, softmax,
+                                     scores, ws, ws_bytes, as_stream(stream));
+  if (e != cudaSuccess) return fail(SPAVA_ECUDA, std::string("score_block: ") + cudaGetErrorString(e));
+  g_launches += softmax ? 3 : 2;
+  return SPAVA_OK;
+}
+
+int spava_select_pack(const float* scores, int l_b, int l_p, int global_offset, const void* k,
+                      const void* v, int64_t ld, int width, int32_t* idx_out, void* k_out,
+                      void* v_out, int64_t ld_out, int32_t* count_out, int32_t* status_out,
+                      void* stream) {
+  if (l_p < 0 || l_p > l_b) return fail(SPAVA_EINVAL, "select_essential: l_p out of range");
+  if (width % 8 || ld % 8 || ld_out % 8)
+    return fail(SPAVA_EINVAL, "select_essential: widths/strides must be multiples of 8");
+  ST_TRY(require_device());
+  cudaError_t e = launch_select_pack(scores, l_b, l_p, global_offset, k, v, ld, width, idx_out, k_out,
+                                     v_out, ld_out, count_out, status_out, as_stream(stream));
+  if (e != cudaSuccess) return fail(SPAVA_ECUDA, std::string("select_pack: ") + cudaGetErrorString(e));
+  g_launches += (l_p > 0 && k_out && v_out) ? 2 : 1;
+  return SPAVA_OK;
+}
+
+size_t spava_attention_workspace(int nq, int hq, int dh, int splits) {
+  if (splits <= 1) return 0;
+  return static_cast<size_t>(splits) * nq * hq * (dh + 1) * sizeof(float) + 512;
+}
+
+int spava_attention(const void* q, int64_t ldq, int nq, const spava_segment* segs, int nseg,
+                    int hq, int hkv, int dh, void* out, int64_t ldo, int out_f32, float* lse,
+                    int splits, void* ws, size_t ws_bytes, void* stream) {
+  if (nseg < 0 || nseg > kMaxSegs) return fail(SPAVA_EINVAL, "attention: at most 4 key segments");
+  if (splits < 1) splits = 1;
+  if (splits > kMaxMergeParts) return fail(SPAVA_EINVAL, "attention: too many splits");
+  for (int s = 0; s < nseg; ++s)
+    if (segs[s].causal && segs[s].rows > nq)
+      return fail(SPAVA_EINVAL, "attention_lse: causal segment must match query rows");
+  ST_TRY(require_device());
+  ProbView pv{};
+  pv.q = q;
+  pv.ldq = ldq;
+  pv.nq = nq;
+  pv.nseg = nseg;
+  for (int s = 0; s < nseg; ++s)
+    pv.seg[s] = SegView{segs[s].k, segs[s].v, segs[s].ld, segs[s].rows, segs[s].causal};
+  cudaStream_t st = as_stream(stream);
+  const long long dq = static_cast<long long>(hq) * dh;
+  if (splits == 1) {
+    pv.out = out;
+    pv.ldo = ldo;
+    pv.out_f32 = out_f32;
+    pv.lse = lse;
+    pv.ld_lse = hq;
+    pv.splits = 1;
+    return attention_impl(&pv, 1, hq, hkv, dh, st);
+  }
+  if (ws_bytes < spava_attention_workspace(nq, hq, dh, splits))
+    return fail(SPAVA_EINVAL, "attention: workspace too small for splits");
+  float* po = static_cast<float*>(ws);
+  float* pl = po + static_cast<size_t>(splits) * nq * dq;
+  pv.out = po;
+  pv.ldo = dq;
+  pv.out_f32 = 1;
+  pv.lse = pl;
+  pv.ld_lse = hq;
+  pv.splits = splits;
+  pv.split_stride_out = static_cast<long long>(nq) * dq;
+  pv.split_stride_lse = static_cast<long long>(nq) * hq;
+  ST_TRY(attention_impl(&pv, 1, hq, hkv, dh, st));
+  MergeParams mp{};
+  mp.nparts = splits;
+  for (int s = 0; s < splits; ++s) {
+    mp.out[s] = po + s * pv.split_stride_out;
+    mp.lse[s] = pl + s * pv.split_stride_lse;
+  }
+  mp.rows = nq;
+  mp.hq = hq;
+  mp.dh = dh;
+  mp.ld_part = dq;
+  mp.ld_lse = hq;
+  mp.dst = out;
+  mp.ld_dst = ldo;
+  mp.dst_f32 = out_f32;
+  mp.dst_lse = lse;
+  return merge_impl(mp, st);
+}
+
+int spava_mha_merge(int nparts, const float* const* outs, const float* const* lses, int rows,
+                    int64_t ld_part, int hq, int dh, void* dst, int64_t ld_dst, int dst_f32,
+                    float* dst_lse, int32_t* status, void* stream) {
+  if (nparts < 1) return fail(SPAVA_EINVAL, "mha_merge: empty part list");
+  if (nparts > kMaxMergeParts) return fail(SPAVA_EINVAL, "mha_merge: too many parts");
+  ST_TRY(require_device());
+  MergeParams mp{};
+  mp.nparts = nparts;
+  for (int i = 0; i < nparts; ++i) {
+    mp.out[i] = outs[i];
+    mp.lse[i] = lses[i];
+  }
+  mp.rows = rows;
+  mp.hq = hq;
+  mp.dh = dh;
+  mp.ld_part = ld_part;
+  mp.ld_lse = hq;
+  mp.dst = dst;
+  mp.ld_dst = ld_dst;
+  mp.dst_f32 = dst_f32;
+  mp.dst_lse = dst_lse;
+  mp.status = status;
+  return merge_impl(mp, as_stream(stream));
+}
+
+// ------------------------------------------------------------- fabric/host
+int spava_fabric_create_local(const spava_layer_cfg* cfg, int device, spava_fabric** out) {
+  spava_plan plan;
+  ST_TRY(cfg_check(cfg, &plan));
+  CU_TRY(cudaSetDevice(device));
+  ST_TRY(require_device());
+  auto* F = new spava_fabric();
+  F->cfg = *cfg;
+  F->plan = plan;
+  F->device = device;
+  int s = F->shared.alloc(*cfg, plan);
+  if (s != SPAVA_OK) {
+    delete F;
+    return s;
+  }
+  *out = F;
+  return SPAVA_OK;
+}
+
+int spava_nccl_unique_id(void* uid) {
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  std::memcpy(uid, &id, sizeof(id));
+  return SPAVA_OK;
+}
+
+int spava_fabric_create_nccl(const spava_layer_cfg* cfg, int device, const void* uid, int world,
+                             int rank, spava_fabric** out) {
+  spava_plan plan;
+  ST_TRY(cfg_check(cfg, &plan));
+  if (world != cfg->hosts) return fail(SPAVA_EINVAL, "nccl fabric: world size must equal hosts");
+  if (rank < 0 || rank >= world) return fail(SPAVA_ERANGE, "nccl fabric: rank");
+  CU_TRY(cudaSetDevice(device));
+  ST_TRY(require_device());
+  auto* F = new spava_fabric();
+  F->cfg = *cfg;
+  F->plan = plan;
+  F->device = device;
+  F->nccl = true;
+  F->world = world;
+  F->rank = rank;
+  ncclUniqueId id;
+  std::memcpy(&id, uid, sizeof(id));
+  ncclResult_t r = ncclCommInitRank(&F->comm, world, id, rank);
+  if (r != ncclSuccess) {
+    delete F;
+    return fail(SPAVA_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  }
+  CU_TRY(cudaStreamCreateWithFlags(&F->comm_stream, cudaStreamNonBlocking));
+  *out = F;
+  return SPAVA_OK;
+}
+
+int spava_fabric_destroy(spava_fabric* F) {
+  if (!F) return SPAVA_OK;
+  if (F->comm) ncclCommDestroy(F->comm);
+  if (F->comm_stream) cudaStreamDestroy(F->comm_stream);
+  F->shared.release();
+  delete F;
+  return SPAVA_OK;
+}
+
+int spava_host_create(spava_fabric* F, int h, spava_host** out) {
+  if (!F) return fail(SPAVA_EINVAL, "host_create: null fabric");
+  const spava_plan& p = F->plan;
+  const spava_layer_cfg& c = F->cfg;
+  if (h < 0 || h >= p.hosts) return fail(SPAVA_ERANGE, "host_create: host index");
+  if (F->nccl && h != F->rank) return fail(SPAVA_EINVAL, "host_create: nccl host must equal rank");
+  CU_TRY(cudaSetDevice(F->device));
+  auto* H = new spava_host();
+  H->fab = F;
+  H->h = h;
+  spava_virtual_pair(&p, h, &H->v_lo, &H->v_hi);
+  spava_slice_anchor(p.l_a, p.hosts, h, &H->a0, &H->a1);
+  const int designated = c.designated < 0 ? p.hosts - 1 : c.designated;
+  H->self_keys = c.query_self_all || h == designated;
+  const int keys = (H->a1 - H->a0) + 2 * p.l_b + (H->self_keys ? p.n_t : 0);
+  H->splits = c.query_splits > 0 ? std::min(c.query_splits, kMaxMergeParts) : auto_splits(p.n_t, c.hq, keys);
+  if (F->nccl) {
+    int s = H->own.alloc(c, p);
+    if (s != SPAVA_OK) {
+      delete H;
+      return s;
+    }
+    H->ex = &H->own;
+  } else {
+    H->ex = &F->shared;
+  }
+  const size_t dq = static_cast<size_t>(c.hq) * c.dh;
+  H->score_ws_bytes = score_workspace_bytes(p.n_t, p.l_b, c.hq);
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  const size_t sc = al(static_cast<size_t>(p.l_b) * 4);
+  const size_t qo = al(static_cast<size_t>(H->splits) * p.n_t * dq * 4);
+  const size_t ql = al(static_cast<size_t>(H->splits) * p.n_t * c.hq * 4);
+  const size_t total = 2 * sc + al(H->score_ws_bytes) + qo + ql + 256;
+  if (cudaMalloc(&H->base, total) != cudaSuccess) {
+    delete H;
+    return fail(SPAVA_ECUDA, "host_create: out of device memory");
+  }
+  cudaMemset(H->base, 0, total);
+  uint8_t* b = static_cast<uint8_t*>(H->base);
+  H->scores[0] = reinterpret_cast<float*>(b); b += sc;
+  H->scores[1] = reinterpret_cast<float*>(b); b += sc;
+  H->score_ws = b; b += al(H->score_ws_bytes);
+  H->qsplit_out = reinterpret_cast<float*>(b); b += qo;
+  H->qsplit_lse = reinterpret_cast<float*>(b); b += ql;
+  H->status = reinterpret_cast<int32_t*>(b);
+  for (auto& e : H->ev) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  *out = H;
+  return SPAVA_OK;
+}
+
+int spava_host_destroy(spava_host* H) {
+  if (!H) return SPAVA_OK;
+  for (auto& e : H->ev)
+    if (e) cudaEventDestroy(e);
+  H->own.release();
+  if (H->base) cudaFree(H->base);
+  delete H;
+  return SPAVA_OK;
+}
+
+int spava_host_plan(const spava_host* H, spava_plan* out) {
+  *out = H->fab->plan;
+  return SPAVA_OK;
+}
+
+int spava_host_rows(const spava_host* H) {
+  const spava_plan& p = H->fab->plan;
+  return p.l_a + 2 * p.l_b + p.n_t;
+}
+
+int spava_host_layer(spava_host* H, const void* q, const void* k, const void* v, void* out,
+                     int32_t* sel, void* stream) {
+  spava_fabric* F = H->fab;
+  if (!F->nccl && F->plan.hosts != 1)
+    return fail(SPAVA_EINVAL, "host_layer: local fabric with H > 1 must be driven by spava_sim_layer");
+  CU_TRY(cudaSetDevice(F->device));
+  cudaStream_t st = as_stream(stream);
+  HostBufs b{static_cast<const uint8_t*>(q), static_cast<const uint8_t*>(k),
+             static_cast<const uint8_t*>(v), static_cast<uint8_t*>(out), sel};
+  if (!F->nccl) {
+    ST_TRY(phase_select(H, b, st, false));
+    ST_TRY(phase_query(H, b, st, false));
+    ST_TRY(phase_stage1(H, b, st));
+    ST_TRY(phase_stage2(H, b, st));
+    return phase_merge(H, b, st);
+  }
+  cudaStream_t cs = F->comm_stream;
+  ST_TRY(phase_select(H, b, st, true));  // records pass1_ready, pass2_ready
+  CU_TRY(cudaStreamWaitEvent(cs, H->ev[0], 0));
+  ST_TRY(nccl_round(F, H->ex, 0));
+  CU_TRY(cudaEventRecord(H->ev[3], cs));
+  CU_TRY(cudaStreamWaitEvent(cs, H->ev[1], 0));
+  ST_TRY(nccl_round(F, H->ex, 1));
+  CU_TRY(cudaEventRecord(H->ev[4], cs));
+  ST_TRY(phase_query(H, b, st, true));  // overlaps the pass rounds
+  CU_TRY(cudaStreamWaitEvent(cs, H->ev[2], 0));
+  ST_TRY(nccl_qround(F, H->ex));
+  CU_TRY(cudaEventRecord(H->ev[5], cs));
+  CU_TRY(cudaStreamWaitEvent(st, H->ev[3], 0));
+  if (!F->plan.zigzag) CU_TRY(cudaStreamWaitEvent(st, H->ev[4], 0));  // simhost.cpp:392-402
+  ST_TRY(phase_stage1(H, b, st));
+  CU_TRY(cudaStreamWaitEvent(st, H->ev[4], 0));
+  ST_TRY(phase_stage2(H, b, st));
+  CU_TRY(cudaStreamWaitEvent(st, H->ev[5], 0));
+  return phase_merge(H, b, st);
+}
+
+int spava_sim_layer(spava_fabric* F, spava_host* const* hosts, const void* const* q,
+                    const void* const* k, const void* const* v, void* const* out,
+                    int32_t* const* sel, void* stream) {
+  if (!F || F->nccl) return fail(SPAVA_EINVAL, "sim_layer: needs a local fabric");
+  CU_TRY(cudaSetDevice(F->device));
+  cudaStream_t st = as_stream(stream);
+  const int H = F->plan.hosts;
+  std::vector<HostBufs> b(H);
+  for (int h = 0; h < H; ++h) {
+    if (!hosts[h] || hosts[h]->fab != F || hosts[h]->h != h)
+      return fail(SPAVA_EINVAL, "sim_layer: hosts[h] must be host h of this fabric");
+    b[h] = HostBufs{static_cast<const uint8_t*>(q[h]), static_cast<const uint8_t*>(k[h]),
+                    static_cast<const uint8_t*>(v[h]), static_cast<uint8_t*>(out[h]),
+                    sel ? sel[h] : nullptr};
+  }
+  // phase 1 on every host fills the shared exchange (the GatherFabric rounds)
+  for (int h = 0; h < H; ++h) {
+    ST_TRY(phase_select(hosts[h], b[h], st, false));
+    ST_TRY(phase_query(hosts[h], b[h], st, false));
+  }
+  for (int h = 0; h < H; ++h) {
+    ST_TRY(phase_stage1(hosts[h], b[h], st));
+    ST_TRY(phase_stage2(hosts[h], b[h], st));
+    ST_TRY(phase_merge(hosts[h], b[h], st));
+  }
+  return SPAVA_OK;
+}
+
+int spava_host_status(spava_host* H, void* stream, int32_t* status_out) {
+  CU_TRY(cudaMemcpyAsync(status_out, H->status, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                         as_stream(stream)));
+  CU_TRY(cudaStreamSynchronize(as_stream(stream)));
+  return SPAVA_OK;
+}
+
+}  // extern "C"

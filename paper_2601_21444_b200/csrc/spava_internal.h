@@ -1,0 +1,107 @@
+// spava_internal.h -- device-side descriptors shared by the Spava kernels and the
+// host runtime (never part of the public C ABI, see include/spava_b200.h).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+namespace spava {
+
+// ---------------------------------------------------------------- attention
+constexpr int kHeadDim = 128;       // dh (Qwen2.5-VL 3B/7B)
+constexpr int kBlockM = 128;        // query rows per Q tile (TMEM lanes)
+constexpr int kBlockN = 128;        // keys per KV tile
+constexpr int kTilesPerCta = 2;     // two Q tiles share every K/V tile (ping-pong softmax)
+constexpr int kMaxSegs = 4;         // [anchor | passing lo-round | passing hi-round | own]
+constexpr int kMaxProbs = 3;        // attention problems fused into one launch
+
+struct AttnSeg {
+  int len;     // keys in the segment; key j of row i is visible iff j < len (&& j <= i if causal)
+  int causal;  // MaskKind::CausalWithin (attention.hpp:14)
+};
+
+struct AttnProb {
+  int nq;                    // query rows
+  int nseg;
+  AttnSeg seg[kMaxSegs];
+  int units;                 // ceil(nq / 256)
+  int splits;                // split-KV factor; >1 writes per-split partials
+  int work_begin;            // first work index of this problem
+  int out_f32;               // 0: bf16 output, 1: f32 output
+  void* out;                 // [splits][nq][ldo]
+  long long ldo;             // row stride (elements)
+  long long split_stride_out;
+  float* lse;                // nullable; [splits][nq][ld_lse] natural-log lse per head
+  int ld_lse;
+  long long split_stride_lse;
+};
+
+struct __align__(64) AttnParams {
+  // per problem: [0] = Q, [1+2s] = K of segment s, [2+2s] = V of segment s
+  CUtensorMap tmap[kMaxProbs][1 + 2 * kMaxSegs];
+  AttnProb prob[kMaxProbs];
+  int nprob;
+  int hq, hkv;
+  int total_work;
+  float scale_log2;  // (1/sqrt(dh)) * log2(e)
+};
+
+// Host launch helpers (attention.cu)
+struct SegView {
+  const void* k;
+  const void* v;
+  long long ld;  // row stride in elements (bf16)
+  int len;
+  int causal;
+};
+struct ProbView {
+  const void* q;
+  long long ldq;
+  int nq;
+  int nseg;
+  SegView seg[kMaxSegs];
+  void* out;
+  long long ldo;
+  int out_f32;
+  float* lse;
+  int ld_lse;
+  int splits;
+  long long split_stride_out;
+  long long split_stride_lse;
+};
+cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, int dh,
+                             cudaStream_t stream, std::string* err);
+
+// ---------------------------------------------------------------- scoring
+size_t score_workspace_bytes(int n_t, int l_b, int hq);
+cudaError_t launch_score_exact(const void* q, long long ldq, int n_t, const void* k,
+                               long long ldk, int l_b, const uint8_t* pad, int n_valid, int hq,
+                               int hkv, int dh, int softmax, float* scores, void* ws,
+                               size_t ws_bytes, cudaStream_t stream);
+
+// ---------------------------------------------------------------- selection
+cudaError_t launch_select_pack(const float* scores, int l_b, int l_p, int global_offset,
+                               const void* k, const void* v, long long ld, int width, int32_t* idx,
+                               void* k_out, void* v_out, long long ld_out, int32_t* count,
+                               int32_t* status, cudaStream_t stream);
+
+// ---------------------------------------------------------------- merge
+constexpr int kMaxMergeParts = 64;
+struct MergeParams {
+  const float* out[kMaxMergeParts];  // [rows][ld_part]
+  const float* lse[kMaxMergeParts];  // [rows][ld_lse]
+  int nparts;
+  int rows, hq, dh;
+  long long ld_part;
+  int ld_lse;
+  void* dst;
+  long long ld_dst;
+  int dst_f32;
+  float* dst_lse;  // nullable [rows][hq]
+  int32_t* status; // nullable; set to 1 if a row is invalid in every part
+};
+cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream);
+
+}  // namespace spava

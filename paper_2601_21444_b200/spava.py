@@ -1,0 +1,434 @@
+"""ctypes binding of include/spava_b200.h + a Python mirror of the reference API.
+
+Names and argument meanings follow the reference ``seqpar`` operators
+(/root/reference/proj/core/include/seqpar/{partition,approx,attention}.hpp) so the
+parity tests read like the reference's own doctest suites.  Tensors are torch CUDA
+tensors: Q/K/V bf16 token-major [rows, heads*dh]; scores/partials f32.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libspava_b200.so")
+
+__all__ = [
+    "SpavaError", "lib", "Plan", "LayerConfig", "Fabric", "Host", "make_plan", "default_plan",
+    "virtual_pair", "physical_of", "slice_anchor", "block_offset", "query_offset", "pad_mask",
+    "block_valid_rows", "passing_ranges", "score_block", "select_pack", "select_essential", "attention",
+    "mha_merge", "anchor_attention", "block_attention", "query_attention", "nccl_unique_id",
+    "kernel_launches", "device_ok", "EXPORTED_SYMBOLS",
+]
+
+EINVAL, ERANGE, ERUNTIME, ECUDA, ENCCL = 1, 2, 3, 4, 5
+
+EXPORTED_SYMBOLS = [
+    "spava_last_error", "spava_version", "spava_device_ok", "spava_make_plan",
+    "spava_default_plan", "spava_virtual_pair", "spava_physical_of", "spava_slice_anchor",
+    "spava_block_offset", "spava_query_offset", "spava_pad_mask", "spava_block_valid_rows",
+    "spava_passing_ranges",
+    "spava_score_workspace", "spava_score_block", "spava_select_pack",
+    "spava_attention_workspace", "spava_attention", "spava_mha_merge",
+    "spava_fabric_create_local", "spava_nccl_unique_id", "spava_fabric_create_nccl",
+    "spava_fabric_destroy", "spava_host_create", "spava_host_destroy", "spava_host_plan",
+    "spava_host_rows", "spava_host_layer", "spava_sim_layer", "spava_host_status",
+    "spava_kernel_launches",
+]
+
+
+class SpavaError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[spava status {code}] {msg}")
+        self.code = code
+
+
+class Plan(C.Structure):
+    _fields_ = [(n, C.c_int) for n in (
+        "n_v", "n_t", "hosts", "l_a", "l_b", "l_p", "pad", "virtual_hosts", "zigzag")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class _Segment(C.Structure):
+    _fields_ = [("k", C.c_void_p), ("v", C.c_void_p), ("ld", C.c_int64), ("rows", C.c_int),
+                ("causal", C.c_int)]
+
+
+class LayerConfig(C.Structure):
+    _fields_ = [(n, C.c_int) for n in (
+        "n_v", "n_t", "hosts", "l_a", "l_p", "zigzag", "designated", "query_self_all",
+        "softmax_scores", "hq", "hkv", "dh", "query_splits")]
+
+    @classmethod
+    def make(cls, n_v, n_t, hosts, l_a, l_p, hq, hkv, dh=128, zigzag=True, designated=-1,
+             query_self_all=False, softmax_scores=True, query_splits=0):
+        return cls(n_v, n_t, hosts, l_a, l_p, int(zigzag), designated, int(query_self_all),
+                   int(softmax_scores), hq, hkv, dh, query_splits)
+
+
+_lib = None
+
+
+def lib():
+    """Load libspava_b200.so; raises (no fallback) if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise SpavaError(ECUDA, f"{LIB_PATH} missing: build it with __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        L.spava_last_error.restype = C.c_char_p
+        L.spava_version.restype = C.c_char_p
+        L.spava_score_workspace.restype = C.c_size_t
+        L.spava_score_workspace.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.spava_attention_workspace.restype = C.c_size_t
+        L.spava_attention_workspace.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+        L.spava_kernel_launches.restype = C.c_uint64
+        L.spava_score_block.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64,
+                                        C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                        C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+        L.spava_select_pack.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                        C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.spava_attention.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int,
+                                      C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int,
+                                      C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p]
+        L.spava_mha_merge.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int64,
+                                      C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int,
+                                      C.c_void_p, C.c_void_p, C.c_void_p]
+        L.spava_host_layer.argtypes = [C.c_void_p] * 7
+        L.spava_sim_layer.argtypes = [C.c_void_p] * 8
+        L.spava_host_create.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.spava_host_destroy.argtypes = [C.c_void_p]
+        L.spava_host_rows.argtypes = [C.c_void_p]
+        L.spava_host_plan.argtypes = [C.c_void_p, C.c_void_p]
+        L.spava_host_status.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.spava_fabric_destroy.argtypes = [C.c_void_p]
+        L.spava_fabric_create_local.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.spava_fabric_create_nccl.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int,
+                                               C.c_void_p]
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise SpavaError(rc, lib().spava_last_error().decode())
+
+
+def device_ok() -> bool:
+    return bool(lib().spava_device_ok())
+
+
+def kernel_launches() -> int:
+    return int(lib().spava_kernel_launches())
+
+
+def _stream(stream=None):
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _require(t, dtype, name):
+    import torch
+
+    if t.device.type != "cuda":
+        raise SpavaError(EINVAL, f"{name}: expected a CUDA tensor (there is no CPU path)")
+    if t.dtype != dtype:
+        raise SpavaError(EINVAL, f"{name}: expected {dtype}, got {t.dtype}")
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise SpavaError(EINVAL, f"{name}: expected a row-major 2-D tensor")
+    _ = torch
+
+
+# ------------------------------------------------------------------ partition
+def make_plan(n_v, n_t, hosts, l_a, l_p, zigzag=True) -> Plan:
+    """split_context geometry (partition.cpp:40-85)."""
+    p = Plan()
+    _check(lib().spava_make_plan(n_v, n_t, hosts, l_a, l_p, int(zigzag), C.byref(p)))
+    return p
+
+
+def default_plan(n, hosts) -> Plan:
+    """default_plan (partition.cpp:96-113)."""
+    p = Plan()
+    _check(lib().spava_default_plan(n, hosts, C.byref(p)))
+    return p
+
+
+def virtual_pair(plan: Plan, h):
+    lo, hi = C.c_int(), C.c_int()
+    _check(lib().spava_virtual_pair(C.byref(plan), h, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
+def physical_of(plan: Plan, v):
+    h = C.c_int()
+    _check(lib().spava_physical_of(C.byref(plan), v, C.byref(h)))
+    return h.value
+
+
+def slice_anchor(l_a, hosts, h):
+    b, e = C.c_int(), C.c_int()
+    _check(lib().spava_slice_anchor(l_a, hosts, h, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+def block_offset(plan: Plan, v):
+    return lib().spava_block_offset(C.byref(plan), v)
+
+
+def query_offset(plan: Plan):
+    return lib().spava_query_offset(C.byref(plan))
+
+
+def block_valid_rows(plan: Plan, v):
+    return lib().spava_block_valid_rows(C.byref(plan), v)
+
+
+def passing_ranges(plan: Plan, v):
+    """Exchange slots holding the sources < v: ((r0_begin, r0_end), (r1_begin, r1_end))."""
+    a, b, c, d = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    _check(lib().spava_passing_ranges(C.byref(plan), v, C.byref(a), C.byref(b), C.byref(c),
+                                      C.byref(d)))
+    return (a.value, b.value), (c.value, d.value)
+
+
+def pad_mask(plan: Plan, v):
+    m = np.zeros(max(plan.l_b, 1), np.uint8)
+    _check(lib().spava_pad_mask(C.byref(plan), v, m.ctypes.data_as(C.c_void_p)))
+    return m[:plan.l_b]
+
+
+# -------------------------------------------------------------------- device ops
+def score_block(q, k, hq, hkv, dh=128, pad=None, n_valid=None, softmax=True, stream=None):
+    """score_block (simhost.cpp:209-224): per-key importance, pads -> -inf."""
+    import torch
+
+    _require(q, torch.bfloat16, "q")
+    _require(k, torch.bfloat16, "k")
+    n_t, l_b = q.shape[0], k.shape[0]
+    ws_bytes = lib().spava_score_workspace(n_t, l_b, hq)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
+    out = torch.empty(l_b, dtype=torch.float32, device=q.device)
+    padt = None
+    if pad is not None:
+        padt = torch.as_tensor(np.asarray(pad, np.uint8)).to(q.device)
+    _check(lib().spava_score_block(_ptr(q), q.stride(0), n_t, _ptr(k), k.stride(0), l_b, _ptr(padt),
+                                   l_b if n_valid is None else n_valid, hq, hkv, dh, int(softmax),
+                                   _ptr(out), _ptr(ws), ws_bytes, _stream(stream)))
+    return out
+
+
+def select_pack(scores, l_p, global_offset=0, k=None, v=None, stream=None):
+    """select_essential (approx.cpp:71-102) on device; returns device tensors
+    (idx[l_p], count[1], k_c, v_c, status[1]); rows >= count are zero."""
+    import torch
+
+    dev = scores.device
+    l_b = scores.shape[0]
+    idx = torch.full((max(l_p, 1),), -1, dtype=torch.int32, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    kc = vc = None
+    width, ld = 8, 8
+    if k is not None:
+        width, ld = k.shape[1], k.stride(0)
+        kc = torch.zeros((max(l_p, 1), width), dtype=k.dtype, device=dev)
+        vc = torch.zeros((max(l_p, 1), width), dtype=k.dtype, device=dev)
+    _check(lib().spava_select_pack(_ptr(scores), l_b, l_p, global_offset, _ptr(k), _ptr(v), ld,
+                                   width, _ptr(idx), _ptr(kc), _ptr(vc), width, _ptr(cnt), _ptr(st),
+                                   _stream(stream)))
+    return idx, cnt, kc, vc, st
+
+
+def select_essential(scores, l_p, global_offset=0, k=None, v=None):
+    """Host-facing select_essential: trims to the selected count (synchronises)."""
+    idx, cnt, kc, vc, st = select_pack(scores, l_p, global_offset, k, v)
+    if int(st.item()):
+        raise SpavaError(EINVAL, "select_essential: NaN score")
+    n = int(cnt.item())
+    return idx[:n], (kc[:n] if kc is not None else None), (vc[:n] if vc is not None else None)
+
+
+def attention(q, segments, hq, hkv, dh=128, out_f32=False, want_lse=False, splits=1, stream=None):
+    """mha_lse (attention.cpp:158-178) over a segment table.
+
+    segments: list of dict(k=, v=, rows=None, causal=False); rows < k.shape[0] masks
+    the tail (pads).  Returns (out [nq, hq*dh], lse [nq, hq] or None)."""
+    import torch
+
+    _require(q, torch.bfloat16, "q")
+    nq = q.shape[0]
+    arr = (_Segment * max(len(segments), 1))()
+    for i, s in enumerate(segments):
+        _require(s["k"], torch.bfloat16, "k")
+        _require(s["v"], torch.bfloat16, "v")
+        if s["k"].stride(0) != s["v"].stride(0):
+            raise SpavaError(EINVAL, "segment k/v must share a row stride")
+        arr[i].k = s["k"].data_ptr()
+        arr[i].v = s["v"].data_ptr()
+        arr[i].ld = s["k"].stride(0)
+        arr[i].rows = s["k"].shape[0] if s.get("rows") is None else int(s["rows"])
+        arr[i].causal = int(bool(s.get("causal", False)))
+    out = torch.empty((nq, hq * dh), dtype=torch.float32 if out_f32 else torch.bfloat16,
+                      device=q.device)
+    lse = torch.empty((nq, hq), dtype=torch.float32, device=q.device) if want_lse else None
+    ws_bytes = lib().spava_attention_workspace(nq, hq, dh, splits)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=q.device)
+    _check(lib().spava_attention(_ptr(q), q.stride(0), nq, arr, len(segments), hq, hkv, dh,
+                                 _ptr(out), out.stride(0), int(out_f32), _ptr(lse), splits,
+                                 _ptr(ws), ws_bytes, _stream(stream)))
+    return out, lse
+
+
+def mha_merge(outs, lses, hq, dh=128, out_f32=True, want_lse=False, stream=None):
+    """mha_merge (attention.cpp:180-197) in part order."""
+    import torch
+
+    n = len(outs)
+    rows = outs[0].shape[0]
+    po = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
+    pl = (C.c_void_p * n)(*[l.data_ptr() for l in lses])
+    dst = torch.empty((rows, hq * dh), dtype=torch.float32 if out_f32 else torch.bfloat16,
+                      device=outs[0].device)
+    dl = torch.empty((rows, hq), dtype=torch.float32, device=outs[0].device) if want_lse else None
+    st = torch.zeros(1, dtype=torch.int32, device=outs[0].device)
+    _check(lib().spava_mha_merge(n, po, pl, rows, outs[0].stride(0), hq, dh, _ptr(dst),
+                                 dst.stride(0), int(out_f32), _ptr(dl), _ptr(st), _stream(stream)))
+    return dst, dl, st
+
+
+def anchor_attention(q_a, k_a, v_a, hq, hkv, dh=128, out_f32=False):
+    """anchor_attention (approx.cpp:134-138)."""
+    return attention(q_a, [dict(k=k_a, v=v_a, causal=True)], hq, hkv, dh, out_f32)[0]
+
+
+def block_attention(q, k, v, n_valid, k_a, v_a, k_p, v_p, hq, hkv, dh=128, out_f32=False):
+    """block_attention (approx.cpp:140-154): [anchor | passing | own causal+pad]."""
+    segs = []
+    if k_a is not None and k_a.shape[0] > 0:
+        segs.append(dict(k=k_a, v=v_a))
+    if k_p is not None and k_p.shape[0] > 0:
+        segs.append(dict(k=k_p, v=v_p))
+    segs.append(dict(k=k, v=v, rows=n_valid, causal=True))
+    return attention(q, segs, hq, hkv, dh, out_f32)[0]
+
+
+def query_attention(q, k_a, v_a, a0, a1, k_lo, v_lo, nv_lo, k_hi, v_hi, nv_hi, k_q, v_q,
+                    include_self, hq, hkv, dh=128, splits=1):
+    """query_attention (approx.cpp:156-188) -> (out f32, lse)."""
+    segs = []
+    if a1 > a0:
+        segs.append(dict(k=k_a[a0:a1], v=v_a[a0:a1]))
+    if nv_lo > 0:
+        segs.append(dict(k=k_lo, v=v_lo, rows=nv_lo))
+    if nv_hi > 0:
+        segs.append(dict(k=k_hi, v=v_hi, rows=nv_hi))
+    if include_self:
+        segs.append(dict(k=k_q, v=v_q, causal=True))
+    return attention(q, segs, hq, hkv, dh, out_f32=True, want_lse=True, splits=splits)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().spava_nccl_unique_id(buf))
+    return buf.raw
+
+
+# ------------------------------------------------------------------ layer runtime
+class Host:
+    def __init__(self, fabric, h):
+        self.fabric = fabric
+        self.h = h
+        self._p = C.c_void_p()
+        _check(lib().spava_host_create(fabric._p, h, C.byref(self._p)))
+        self.rows = lib().spava_host_rows(self._p)
+        self.plan = Plan()
+        lib().spava_host_plan(self._p, C.byref(self.plan))
+
+    def layer(self, q, k, v, out, sel=None, stream=None):
+        """One layer of this host (NCCL fabric, or a local fabric with H == 1)."""
+        _check(lib().spava_host_layer(self._p, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(sel),
+                                      _stream(stream)))
+
+    def status(self, stream=None):
+        s = C.c_int32()
+        _check(lib().spava_host_status(self._p, _stream(stream), C.byref(s)))
+        return s.value
+
+    def close(self):
+        if self._p:
+            lib().spava_host_destroy(self._p)
+            self._p = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Fabric:
+    """GatherFabric (simhost.cpp:61-166) equivalent: local (one device) or NCCL."""
+
+    def __init__(self, cfg: LayerConfig, device=0, unique_id=None, world=1, rank=0):
+        self.cfg = cfg
+        self._p = C.c_void_p()
+        if unique_id is None:
+            _check(lib().spava_fabric_create_local(C.byref(cfg), device, C.byref(self._p)))
+            self.nccl = False
+        else:
+            buf = C.create_string_buffer(unique_id, 128)
+            _check(lib().spava_fabric_create_nccl(C.byref(cfg), device, buf, world, rank,
+                                                  C.byref(self._p)))
+            self.nccl = True
+
+    def host(self, h) -> Host:
+        return Host(self, h)
+
+    def sim_layer(self, hosts, qs, ks, vs, outs, sels=None, stream=None):
+        n = len(hosts)
+        arr = lambda ts: (C.c_void_p * n)(*[t.data_ptr() if t is not None else None for t in ts])
+        _check(lib().spava_sim_layer(self._p, (C.c_void_p * n)(*[h._p.value for h in hosts]),
+                                     arr(qs), arr(ks), arr(vs), arr(outs),
+                                     arr(sels) if sels is not None else None, _stream(stream)))
+
+    def close(self):
+        if self._p:
+            lib().spava_fabric_destroy(self._p)
+            self._p = C.c_void_p()
+
+
+@dataclass
+class HostLayout:
+    """Row ranges of the host-local buffers [anchor | lo | hi | query]."""
+    l_a: int
+    l_b: int
+    n_t: int
+
+    @property
+    def lo(self):
+        return slice(self.l_a, self.l_a + self.l_b)
+
+    @property
+    def hi(self):
+        return slice(self.l_a + self.l_b, self.l_a + 2 * self.l_b)
+
+    @property
+    def query(self):
+        return slice(self.l_a + 2 * self.l_b, self.l_a + 2 * self.l_b + self.n_t)
+
+    @property
+    def anchor(self):
+        return slice(0, self.l_a)

@@ -1,0 +1,234 @@
+"""GPU parity of the individual Spava kernels against the CPU oracle (C restatement of
+the reference, pinned bit-exact to the reference itself in test_oracle.py).
+
+Selection indices are checked bit-exact; scores to a few fp32 ulp; attention outputs
+within the bf16 tolerances stated in tests/util.py and DESIGN.md.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.util import (ATOL_BF16_OUT, ATOL_F32_OUT, ATOL_LSE, RTOL_L2_BF16, RTOL_L2_F32, bf16,
+                        load_golden, max_abs, randn, rel_l2, ulp_diff)
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(x, device):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(device).to(torch.bfloat16)
+
+
+def host(t):
+    import torch
+
+    return t.float().cpu().numpy() if t.dtype == torch.bfloat16 else t.cpu().numpy()
+
+
+# ------------------------------------------------------------------ scoring
+@pytest.mark.parametrize("n_t,l_b,hq,hkv,n_valid,softmax", [
+    (16, 300, 4, 2, 300, True),
+    (16, 300, 4, 2, 287, True),     # padded tail
+    (128, 1000, 16, 2, 1000, True),  # C0 geometry (n_t=64 there; 128 = C1..C4)
+    (64, 1000, 16, 2, 1000, False),  # raw-logit aggregation
+    (5, 77, 2, 1, 77, True),
+    (130, 200, 4, 4, 190, True),     # n_t > 128 row chunks, MHA
+])
+def test_score_block_matches_oracle(cuda, n_t, l_b, hq, hkv, n_valid, softmax):
+    from paper_2601_21444_b200 import spava
+
+    rng = np.random.default_rng(n_t * 7 + l_b)
+    q = randn(rng, n_t, hq * 128)
+    k = randn(rng, l_b, hkv * 128)
+    pad = (np.arange(l_b) >= n_valid).astype(np.uint8)
+    ref = O.score_block(q, k, hq, hkv, 128, pad, softmax)
+    got = host(spava.score_block(dev(q, cuda), dev(k, cuda), hq, hkv, 128, n_valid=n_valid,
+                                 softmax=softmax))
+    assert np.array_equal(np.isinf(got), np.isinf(ref))
+    fin = np.isfinite(ref)
+    assert ulp_diff(got[fin], ref[fin]) <= 4, "scores drift beyond 4 fp32 ulp"
+    frac_exact = float(np.mean(got[fin] == ref[fin]))
+    assert frac_exact > 0.95
+    # the contract: identical selection
+    for l_p in (0, 1, max(1, n_valid // 8), n_valid // 2, n_valid):
+        want = O.select_essential(ref, l_p, 40)
+        idx, _, _ = spava.select_essential(spava_t(got, cuda), l_p, 40)
+        assert np.array_equal(idx.cpu().numpy(), want)
+
+
+def spava_t(x, device):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(device)
+
+
+def test_score_closed_form(cuda):
+    """test_approx.cpp:26-44 restated for dh=128: logits [0, ln 3] -> scores [1/4, 3/4]."""
+    from paper_2601_21444_b200 import spava
+
+    q = np.zeros((1, 128), np.float32)
+    q[0, 0] = 1.0
+    k = np.zeros((2, 128), np.float32)
+    k[1, 0] = np.float32(np.log(3.0) * np.sqrt(128.0))  # scale = 1/sqrt(128)
+    kb = bf16(k)
+    s = host(spava.score_block(dev(q, cuda), dev(kb, cuda), 1, 1, 128))
+    ref = O.score_block(q, kb, 1, 1, 128)
+    assert abs(s[0] - 0.25) < 2e-3 and abs(s[1] - 0.75) < 2e-3
+    assert np.array_equal(s, ref)
+    q2 = np.concatenate([q, q])
+    s2 = host(spava.score_block(dev(q2, cuda), dev(kb, cuda), 1, 1, 128))
+    assert np.allclose(s2, 2 * s, rtol=1e-6)
+
+
+# ---------------------------------------------------------------- selection
+def test_select_examples(cuda):
+    """test_approx.cpp:90-105."""
+    from paper_2601_21444_b200 import spava
+
+    sv = spava_t(np.array([0.1, 0.9, 0.5, 0.9], np.float32), cuda)
+    assert spava.select_essential(sv, 2, 0)[0].cpu().tolist() == [1, 3]
+    ties = spava_t(np.array([0.5] * 4, np.float32), cuda)
+    assert spava.select_essential(ties, 2, 0)[0].cpu().tolist() == [0, 1]
+    assert spava.select_essential(sv, 4, 10)[0].cpu().tolist() == [10, 11, 12, 13]
+
+
+def test_select_ties_golden(cuda):
+    """acceptance.cpp:271-294 style tie-heavy vectors, against the reference's outputs."""
+    from paper_2601_21444_b200 import spava
+
+    g = load_golden("select_ties")
+    for c in range(len(g["n"])):
+        n, lp = int(g["n"][c]), int(g["l_p"][c])
+        want = g["sel"][c][g["sel"][c] >= 0]
+        got = spava.select_essential(spava_t(g["scores"][c, :n], cuda), lp, 0)[0].cpu().numpy()
+        assert np.array_equal(got, want), f"case {c}"
+
+
+def test_select_large_and_pack(cuda):
+    """Radix select at C4 block length with many exact ties + K/V gather."""
+    import torch
+
+    from paper_2601_21444_b200 import spava
+
+    rng = np.random.default_rng(3)
+    l_b, l_p = 128960, 2048
+    s = (rng.integers(0, 5000, l_b) / 7.0).astype(np.float32)
+    s[-100:] = -np.inf
+    k = torch.randn(l_b, 512, device=cuda).to(torch.bfloat16)
+    v = torch.randn(l_b, 512, device=cuda).to(torch.bfloat16)
+    idx, kc, vc = spava.select_essential(spava_t(s, cuda), l_p, 1000, k, v)
+    want = O.select_essential(s, l_p, 1000)
+    assert np.array_equal(idx.cpu().numpy(), want)
+    loc = torch.from_numpy(want - 1000).long().to(cuda)
+    assert torch.equal(kc, k[loc]) and torch.equal(vc, v[loc])
+
+
+def test_select_nonfinite_rules(cuda):
+    from paper_2601_21444_b200 import spava
+
+    s = np.array([1.0, -np.inf, 2.0, -np.inf], np.float32)
+    assert spava.select_essential(spava_t(s, cuda), 4, 0)[0].cpu().tolist() == [0, 2]
+    s2 = np.array([1.0, np.inf, 2.0], np.float32)
+    assert spava.select_essential(spava_t(s2, cuda), 2, 0)[0].cpu().tolist() == \
+        O.select_essential(s2, 2, 0).tolist()
+    with pytest.raises(spava.SpavaError):
+        spava.select_essential(spava_t(np.array([1.0, np.nan], np.float32), cuda), 1, 0)
+
+
+# ---------------------------------------------------------------- attention
+def _segs_np(segs):
+    return [dict(k=s["k"][:s.get("rows", len(s["k"]))], v=s["v"][:s.get("rows", len(s["v"]))],
+                 causal=s.get("causal", False)) for s in segs]
+
+
+@pytest.mark.parametrize("case", [
+    # (nq, [(rows, causal, valid_rows)], hq, hkv, splits)
+    (128, [(128, True, 128)], 2, 2, 1),               # anchor self-attention, one tile
+    (300, [(300, True, 300)], 4, 2, 1),               # 2 units, ragged tail
+    (517, [(64, False, 64), (96, False, 96), (517, True, 509)], 4, 1, 1),  # block: anchor|passing|own+pad
+    (256, [(1000, False, 1000), (256, True, 256)], 2, 1, 1),
+    (128, [(33, False, 33), (700, False, 690), (700, False, 700), (128, True, 128)], 8, 2, 1),  # query attn
+    (128, [(33, False, 33), (700, False, 690), (700, False, 700), (128, True, 128)], 8, 2, 5),  # split-KV
+    (64, [(5, False, 5)], 2, 2, 1),                     # tiny
+])
+def test_attention_matches_oracle(cuda, case):
+    from paper_2601_21444_b200 import spava
+
+    nq, seginfo, hq, hkv, splits = case
+    rng = np.random.default_rng(nq + len(seginfo) * 13 + splits)
+    q = randn(rng, nq, hq * 128)
+    segs_np, segs_dev = [], []
+    for rows, causal, valid in seginfo:
+        k = randn(rng, rows, hkv * 128)
+        v = randn(rng, rows, hkv * 128)
+        segs_np.append(dict(k=k[:valid], v=v[:valid], causal=causal) if not causal else
+                       dict(k=k, v=v, causal=True, pad=(np.arange(rows) >= valid).astype(np.uint8)))
+        segs_dev.append(dict(k=dev(k, cuda), v=dev(v, cuda), rows=valid, causal=causal))
+    ref_out, ref_lse = O.mha_lse(q, segs_np, hq, hkv, 128, allow_invalid=True)
+    out, lse = spava.attention(dev(q, cuda), segs_dev, hq, hkv, 128, out_f32=True, want_lse=True,
+                               splits=splits)
+    out, lse = host(out), host(lse)
+    fin = np.isfinite(ref_lse)
+    assert np.array_equal(np.isfinite(lse), fin)
+    assert max_abs(lse[fin], ref_lse[fin]) <= ATOL_LSE
+    assert max_abs(out, ref_out) <= ATOL_F32_OUT, max_abs(out, ref_out)
+    assert rel_l2(out, ref_out) <= RTOL_L2_F32, rel_l2(out, ref_out)
+    # bf16 output path
+    outb, _ = spava.attention(dev(q, cuda), segs_dev, hq, hkv, 128, out_f32=False, splits=splits)
+    outb = host(outb)
+    assert max_abs(outb, ref_out) <= ATOL_BF16_OUT
+    assert rel_l2(outb, ref_out) <= RTOL_L2_BF16
+
+
+def test_attention_single_key_and_empty_rows(cuda):
+    """test_tensor.cpp:116-128 (one visible key -> V row, lse = scaled logit) and
+    :163-174 (rows with no visible key -> zero row, lse = -inf)."""
+    from paper_2601_21444_b200 import spava
+
+    rng = np.random.default_rng(9)
+    q = randn(rng, 3, 128)
+    k = randn(rng, 4, 128)
+    v = randn(rng, 4, 128)
+    out, lse = spava.attention(dev(q, cuda), [dict(k=dev(k, cuda), v=dev(v, cuda), rows=1)], 1, 1,
+                               out_f32=True, want_lse=True)
+    out, lse = host(out), host(lse)
+    assert max_abs(out, np.repeat(v[:1], 3, 0)) < 4e-3
+    logit = (q.astype(np.float64) @ k[0].astype(np.float64)) / np.sqrt(128.0)
+    assert max_abs(lse[:, 0], logit) < 1e-3
+    out, lse = spava.attention(dev(q, cuda), [dict(k=dev(k, cuda), v=dev(v, cuda), rows=0)], 1, 1,
+                               out_f32=True, want_lse=True)
+    assert np.all(host(out) == 0) and np.all(np.isneginf(host(lse)))
+
+
+def test_attention_deterministic(cuda):
+    """test_tensor.cpp:254-264: identical inputs -> bit-identical outputs."""
+    from paper_2601_21444_b200 import spava
+
+    rng = np.random.default_rng(4)
+    q = dev(randn(rng, 300, 512), cuda)
+    k = dev(randn(rng, 900, 256), cuda)
+    v = dev(randn(rng, 900, 256), cuda)
+    segs = [dict(k=k, v=v), dict(k=k[:300], v=v[:300], causal=True)]
+    a = spava.attention(q, segs, 4, 2)[0]
+    b = spava.attention(q, segs, 4, 2)[0]
+    import torch
+
+    assert torch.equal(a, b)
+
+
+# --------------------------------------------------------------------- merge
+def test_merge_matches_oracle(cuda):
+    """mha_merge in host order; with an all-invalid part row (lse=-inf) skipped."""
+    from paper_2601_21444_b200 import spava
+
+    rng = np.random.default_rng(5)
+    hq, rows = 4, 37
+    outs = [rng.standard_normal((rows, hq * 128)).astype(np.float32) for _ in range(3)]
+    lses = [rng.standard_normal((rows, hq)).astype(np.float32) * 3 for _ in range(3)]
+    lses[1][5, :] = -np.inf
+    ref = O.mha_merge(outs, lses, hq, 128)
+    got, glse, st = spava.mha_merge([spava_t(o, cuda) for o in outs], [spava_t(l, cuda) for l in lses],
+                                    hq, 128, out_f32=True, want_lse=True)
+    assert int(st.item()) == 0
+    assert max_abs(host(got), ref) <= 2e-6 * max(1.0, float(np.abs(ref).max()))

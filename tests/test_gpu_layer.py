@@ -1,0 +1,101 @@
+"""GPU parity of a whole Spava layer (run_host order, simhost.cpp:321-426) through the
+C ABI's layer runtime, against the reference's golden fixtures and the C oracle.
+
+Checked per layer: passing-block indices of every virtual block bit-exact; anchor,
+block (non-pad rows) and merged query outputs within the bf16 tolerances.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.util import (ATOL_BF16_OUT, RTOL_L2_BF16, host_local, load_golden, max_abs, randn,
+                        rel_l2)
+
+pytestmark = pytest.mark.gpu
+
+
+def run_layer(cuda, Q, K, V, n_v, n_t, hosts, l_a, l_p, hq, hkv, zigzag=True, softmax=True,
+              query_splits=0):
+    """Drive the local fabric (H simulated hosts on one GPU) over the global padded inputs."""
+    import torch
+
+    from paper_2601_21444_b200 import spava
+
+    cfg = spava.LayerConfig.make(n_v, n_t, hosts, l_a, l_p, hq, hkv, 128, zigzag=zigzag,
+                                 softmax_scores=softmax, query_splits=query_splits)
+    fab = spava.Fabric(cfg, 0)
+    plan = spava.make_plan(n_v, n_t, hosts, l_a, l_p, zigzag)
+    l_b, qoff = plan.l_b, spava.query_offset(plan)
+    hs, qs, ks, vs, outs, sels = [], [], [], [], [], []
+    for h in range(hosts):
+        lo, hi = spava.virtual_pair(plan, h)
+        H = fab.host(h)
+        hs.append(H)
+        for X, lst in ((Q, qs), (K, ks), (V, vs)):
+            lst.append(torch.from_numpy(host_local(X, l_a, l_b, lo, hi, qoff, n_t)).to(cuda)
+                       .to(torch.bfloat16).contiguous())
+        outs.append(torch.zeros((H.rows, hq * 128), dtype=torch.bfloat16, device=cuda))
+        sels.append(torch.full((2, max(l_p, 1)), -1, dtype=torch.int32, device=cuda))
+    fab.sim_layer(hs, qs, ks, vs, outs, sels)
+    torch.cuda.synchronize()
+    status = [H.status() for H in hs]
+    res = dict(plan=plan, status=status, out=[o.float().cpu().numpy() for o in outs],
+               sel=[s.cpu().numpy() for s in sels])
+    for H in hs:
+        H.close()
+    fab.close()
+    return res
+
+
+def check_layer(res, want, n_t, hosts, l_a, zigzag=True):
+    from paper_2601_21444_b200 import spava
+
+    plan = res["plan"]
+    l_b, l_p = plan.l_b, plan.l_p
+    assert res["status"] == [0] * hosts
+    for h in range(hosts):
+        lo, hi = spava.virtual_pair(plan, h)
+        out = res["out"][h]
+        for r, v in enumerate((lo, hi)):
+            cnt = int(want["sel_count"][v])
+            # the contract: passing-block indices bit-exact (ties -> lowest index)
+            assert np.array_equal(res["sel"][h][r, :cnt], want["sel"][v, :cnt]), (h, v)
+            nv = spava.block_valid_rows(plan, v)
+            got = out[l_a + r * l_b: l_a + r * l_b + nv]
+            ref = want["blocks"][v][:nv]
+            assert max_abs(got, ref) <= ATOL_BF16_OUT, (h, v, max_abs(got, ref))
+            assert rel_l2(got, ref) <= RTOL_L2_BF16, (h, v, rel_l2(got, ref))
+        if l_a:
+            assert max_abs(out[:l_a], want["anchor"]) <= ATOL_BF16_OUT
+            assert rel_l2(out[:l_a], want["anchor"]) <= RTOL_L2_BF16
+        q = out[l_a + 2 * l_b: l_a + 2 * l_b + n_t]
+        assert max_abs(q, want["query"]) <= ATOL_BF16_OUT, max_abs(q, want["query"])
+        assert rel_l2(q, want["query"]) <= RTOL_L2_BF16
+
+
+@pytest.mark.parametrize("name", ["layer_h2_gqa", "layer_h4_pad", "layer_h2_naive",
+                                  "layer_h1_full", "layer_h2_raw"])
+def test_layer_golden(cuda, name):
+    """Golden fixtures generated from the UNMODIFIED reference operators."""
+    g = load_golden(name)
+    n_v, n_t, hosts, l_a, l_p, hq, hkv, dh, zz, sm = [int(x) for x in g["cfg"]]
+    res = run_layer(cuda, g["Q"], g["K"], g["V"], n_v, n_t, hosts, l_a, l_p, hq, hkv, bool(zz),
+                    bool(sm))
+    check_layer(res, g, n_t, hosts, l_a, bool(zz))
+
+
+@pytest.mark.parametrize("hosts,zigzag,splits", [(4, True, 0), (2, False, 3), (1, True, 1)])
+def test_layer_c0_shape(cuda, hosts, zigzag, splits):
+    """C0 geometry (8K tokens, 16 q / 2 kv heads, d=128) against the C oracle layer."""
+    from paper_2601_21444_b200 import spava
+
+    n, n_t, hq, hkv = 8192, 64, 16, 2
+    n_v = n - n_t
+    l_a, l_p = n // 64, n // 128
+    plan = spava.make_plan(n_v, n_t, hosts, l_a, l_p, zigzag)
+    n_pad = l_a + 2 * hosts * plan.l_b + n_t
+    rng = np.random.default_rng(100 + hosts)
+    Q, K, V = randn(rng, n_pad, hq * 128), randn(rng, n_pad, hkv * 128), randn(rng, n_pad, hkv * 128)
+    want = O.spava_layer(Q, K, V, n_v, n_t, hosts, l_a, l_p, hq, hkv, 128, zigzag=zigzag)
+    res = run_layer(cuda, Q, K, V, n_v, n_t, hosts, l_a, l_p, hq, hkv, zigzag, True, splits)
+    check_layer(res, want, n_t, hosts, l_a, zigzag)
