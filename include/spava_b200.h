@@ -185,6 +185,16 @@ int spava_sim_layer(spava_fabric* fab, spava_host* const* hosts, const void* con
  * merge row invalid everywhere).  Synchronises the given stream.            */
 int spava_host_status(spava_host* host, void* stream, int32_t* status_out);
 
+/* Device timing of this host's launches, by kernel class (0 attention, 1 score,
+ * 2 select+pack, 3 merge): CUDA events on the launching stream around every
+ * launch while enabled.  spava_host_set_timing resets the counters;
+ * spava_host_timing synchronises on the recorded events and returns the summed
+ * milliseconds per class, the algorithmic attention FLOPs launched (reference
+ * convention, attention.cpp:33-36) and the attention launch count.           */
+int spava_host_set_timing(spava_host* host, int enable);
+int spava_host_timing(spava_host* host, double* ms_by_class4, double* attn_flops,
+                      uint64_t* attn_launches);
+
 /* Number of kernels the library launched since process start (for bench's
  * gpu_launches claim). */
 uint64_t spava_kernel_launches(void);

@@ -181,7 +181,51 @@ struct spava_host {
   int32_t* status = nullptr;
   void* base = nullptr;
   cudaEvent_t ev[6] = {};  // pass1_ready, pass2_ready, q_ready, pass1_done, pass2_done, q_done
+  // optional per-kernel-class device timing (bench roofline): CUDA events recorded on the
+  // launching stream around every launch; classes 0 attention, 1 score, 2 select, 3 merge
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<std::pair<size_t, size_t>> spans[4];
+  double attn_flops = 0.0;
+  uint64_t attn_launches = 0;
 };
+
+namespace {
+
+cudaEvent_t pool_event(spava_host* H) {
+  if (H->ev_used == H->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    H->ev_pool.push_back(e);
+  }
+  return H->ev_pool[H->ev_used++];
+}
+
+// records an event on st if timing is on; returns its pool index (or SIZE_MAX)
+size_t mark(spava_host* H, cudaStream_t st) {
+  if (!H || !H->timing) return SIZE_MAX;
+  const size_t i = H->ev_used;
+  cudaEventRecord(pool_event(H), st);
+  return i;
+}
+
+void span(spava_host* H, int cls, size_t a, cudaStream_t st) {
+  if (!H || !H->timing || a == SIZE_MAX) return;
+  const size_t b = mark(H, st);
+  H->spans[cls].push_back({a, b});
+}
+
+// reference FLOP convention (attention.cpp:33-36): 4*nq*nk*dh visible, 2*nq*nk*dh causal
+double problem_flops(const ProbView* pv, int np, int hq, int dh) {
+  double f = 0.0;
+  for (int i = 0; i < np; ++i)
+    for (int s = 0; s < pv[i].nseg; ++s)
+      f += (pv[i].seg[s].causal ? 2.0 : 4.0) * pv[i].nq * static_cast<double>(pv[i].seg[s].len) * dh * hq;
+  return f;
+}
+
+}  // namespace
 
 namespace {
 
@@ -200,19 +244,28 @@ int cfg_check(const spava_layer_cfg* c, spava_plan* plan) {
 }
 
 // -------------------------------------------------------- op wrappers
-int attention_impl(const ProbView* pv, int np, int hq, int hkv, int dh, cudaStream_t st) {
+int attention_impl(const ProbView* pv, int np, int hq, int hkv, int dh, cudaStream_t st,
+                   spava_host* H = nullptr) {
   std::string err;
+  const size_t t0 = mark(H, st);
   cudaError_t e = launch_attention(pv, np, hq, hkv, dh, st, &err);
   if (e != cudaSuccess)
     return fail(e == cudaErrorInvalidValue ? SPAVA_EINVAL : SPAVA_ECUDA,
                 err.empty() ? std::string("attention: ") + cudaGetErrorString(e) : err);
+  span(H, 0, t0, st);
+  if (H && H->timing) {
+    H->attn_flops += problem_flops(pv, np, hq, dh);
+    ++H->attn_launches;
+  }
   g_launches += 1;
   return SPAVA_OK;
 }
 
-int merge_impl(const MergeParams& mp, cudaStream_t st) {
+int merge_impl(const MergeParams& mp, cudaStream_t st, spava_host* H = nullptr) {
+  const size_t t0 = mark(H, st);
   cudaError_t e = launch_merge(mp, st);
   if (e != cudaSuccess) return fail(SPAVA_ECUDA, std::string("merge: ") + cudaGetErrorString(e));
+  span(H, 3, t0, st);
   g_launches += 1;
   return SPAVA_OK;
 }
@@ -250,13 +303,16 @@ int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record)
   for (int r = 0; r < 2; ++r) {
     const long long krow = p.l_a + static_cast<long long>(r) * p.l_b;
     const int nvalid = valid_rows(p, vs[r]);
+    size_t t0 = mark(H, st);
     cudaError_t e = launch_score_exact(row_ptr(b.q, qrow, dq), dq, p.n_t, row_ptr(b.k, krow, dk), dk,
                                        p.l_b, nullptr, nvalid, c.hq, c.hkv, c.dh, c.softmax_scores,
                                        H->scores[r], H->score_ws, H->score_ws_bytes, st);
     if (e != cudaSuccess) return fail(SPAVA_ECUDA, std::string("score: ") + cudaGetErrorString(e));
     g_launches += c.softmax_scores ? 3 : 2;
+    span(H, 1, t0, st);
     const long long slot = static_cast<long long>(H->h) * p.l_p;
     int32_t* idx_out = H->ex->passIdx[r] + slot;
+    t0 = mark(H, st);
     e = launch_select_pack(H->scores[r], p.l_b, p.l_p, p.l_a + vs[r] * p.l_b, row_ptr(b.k, krow, dk),
                            row_ptr(b.v, krow, dk), dk, static_cast<int>(dk), idx_out,
                            static_cast<uint8_t*>(H->ex->passK[r]) + slot * dk * 2,
@@ -264,6 +320,7 @@ int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record)
                            H->ex->passCnt[r] + H->h, H->status, st);
     if (e != cudaSuccess) return fail(SPAVA_ECUDA, std::string("select: ") + cudaGetErrorString(e));
     g_launches += p.l_p > 0 ? 2 : 1;
+    span(H, 2, t0, st);
     if (b.sel && p.l_p > 0)
       CU_TRY(cudaMemcpyAsync(b.sel + r * p.l_p, idx_out, sizeof(int32_t) * p.l_p,
                              cudaMemcpyDeviceToDevice, st));
@@ -303,7 +360,7 @@ int phase_query(spava_host* H, const HostBufs& b, cudaStream_t st, bool record) 
     pv.lse = dst_lse;
     pv.ld_lse = c.hq;
     pv.splits = 1;
-    ST_TRY(attention_impl(&pv, 1, c.hq, c.hkv, c.dh, st));
+    ST_TRY(attention_impl(&pv, 1, c.hq, c.hkv, c.dh, st, H));
   } else {
     pv.out = H->qsplit_out;
     pv.ldo = dq;
@@ -313,7 +370,7 @@ int phase_query(spava_host* H, const HostBufs& b, cudaStream_t st, bool record) 
     pv.splits = H->splits;
     pv.split_stride_out = static_cast<long long>(p.n_t) * dq;
     pv.split_stride_lse = static_cast<long long>(p.n_t) * c.hq;
-    ST_TRY(attention_impl(&pv, 1, c.hq, c.hkv, c.dh, st));
+    ST_TRY(attention_impl(&pv, 1, c.hq, c.hkv, c.dh, st, H));
     MergeParams mp{};
     mp.nparts = H->splits;
     for (int s = 0; s < H->splits; ++s) {
@@ -330,7 +387,7 @@ int phase_query(spava_host* H, const HostBufs& b, cudaStream_t st, bool record) 
     mp.dst_f32 = 1;
     mp.dst_lse = dst_lse;
     mp.status = nullptr;  // query partials may legitimately be empty rows
-    ST_TRY(merge_impl(mp, st));
+    ST_TRY(merge_impl(mp, st, H));
   }
   if (record) CU_TRY(cudaEventRecord(H->ev[2], st));
   return SPAVA_OK;
@@ -387,13 +444,13 @@ ProbView anchor_problem(spava_host* H, const HostBufs& b) {
 int phase_stage1(spava_host* H, const HostBufs& b, cudaStream_t st) {
   const spava_layer_cfg& c = H->fab->cfg;
   ProbView pv[2] = {block_problem(H, b, 0), anchor_problem(H, b)};  // heavier first
-  return attention_impl(pv, H->fab->plan.l_a > 0 ? 2 : 1, c.hq, c.hkv, c.dh, st);
+  return attention_impl(pv, H->fab->plan.l_a > 0 ? 2 : 1, c.hq, c.hkv, c.dh, st, H);
 }
 
 int phase_stage2(spava_host* H, const HostBufs& b, cudaStream_t st) {
   const spava_layer_cfg& c = H->fab->cfg;
   ProbView pv = block_problem(H, b, 1);
-  return attention_impl(&pv, 1, c.hq, c.hkv, c.dh, st);
+  return attention_impl(&pv, 1, c.hq, c.hkv, c.dh, st, H);
 }
 
 int phase_merge(spava_host* H, const HostBufs& b, cudaStream_t st) {
@@ -415,7 +472,7 @@ int phase_merge(spava_host* H, const HostBufs& b, cudaStream_t st) {
   mp.ld_dst = dq;
   mp.dst_f32 = 0;
   mp.status = H->status;
-  return merge_impl(mp, st);
+  return merge_impl(mp, st, H);
 }
 
 int nccl_round(spava_fabric* F, Exchange* ex, int r) {
@@ -756,6 +813,7 @@ int spava_host_destroy(spava_host* H) {
   if (!H) return SPAVA_OK;
   for (auto& e : H->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : H->ev_pool) cudaEventDestroy(e);
   H->own.release();
   if (H->base) cudaFree(H->base);
   delete H;
@@ -834,6 +892,32 @@ int spava_sim_layer(spava_fabric* F, spava_host* const* hosts, const void* const
     ST_TRY(phase_stage2(hosts[h], b[h], st));
     ST_TRY(phase_merge(hosts[h], b[h], st));
   }
+  return SPAVA_OK;
+}
+
+int spava_host_set_timing(spava_host* H, int enable) {
+  H->timing = enable != 0;
+  H->ev_used = 0;
+  for (auto& s : H->spans) s.clear();
+  H->attn_flops = 0.0;
+  H->attn_launches = 0;
+  return SPAVA_OK;
+}
+
+int spava_host_timing(spava_host* H, double* ms_by_class, double* attn_flops,
+                      uint64_t* attn_launches) {
+  for (int c = 0; c < 4; ++c) {
+    double ms = 0.0;
+    for (auto& pr : H->spans[c]) {
+      CU_TRY(cudaEventSynchronize(H->ev_pool[pr.second]));
+      float t = 0.f;
+      CU_TRY(cudaEventElapsedTime(&t, H->ev_pool[pr.first], H->ev_pool[pr.second]));
+      ms += t;
+    }
+    if (ms_by_class) ms_by_class[c] = ms;
+  }
+  if (attn_flops) *attn_flops = H->attn_flops;
+  if (attn_launches) *attn_launches = H->attn_launches;
   return SPAVA_OK;
 }
 

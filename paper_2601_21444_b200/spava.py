@@ -36,7 +36,7 @@ EXPORTED_SYMBOLS = [
     "spava_fabric_create_local", "spava_nccl_unique_id", "spava_fabric_create_nccl",
     "spava_fabric_destroy", "spava_host_create", "spava_host_destroy", "spava_host_plan",
     "spava_host_rows", "spava_host_layer", "spava_sim_layer", "spava_host_status",
-    "spava_kernel_launches",
+    "spava_host_set_timing", "spava_host_timing", "spava_kernel_launches",
 ]
 
 
@@ -107,6 +107,8 @@ def lib():
         L.spava_host_rows.argtypes = [C.c_void_p]
         L.spava_host_plan.argtypes = [C.c_void_p, C.c_void_p]
         L.spava_host_status.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.spava_host_set_timing.argtypes = [C.c_void_p, C.c_int]
+        L.spava_host_timing.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.spava_fabric_destroy.argtypes = [C.c_void_p]
         L.spava_fabric_create_local.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
         L.spava_fabric_create_nccl.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int,
@@ -361,6 +363,19 @@ class Host:
         """One layer of this host (NCCL fabric, or a local fabric with H == 1)."""
         _check(lib().spava_host_layer(self._p, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(sel),
                                       _stream(stream)))
+
+    def set_timing(self, enable=True):
+        _check(lib().spava_host_set_timing(self._p, int(enable)))
+
+    def timing(self):
+        """{'attention','score','select','merge'} ms summed over recorded launches,
+        plus algorithmic attention FLOPs and the attention launch count."""
+        ms = (C.c_double * 4)()
+        fl = C.c_double()
+        n = C.c_uint64()
+        _check(lib().spava_host_timing(self._p, ms, C.byref(fl), C.byref(n)))
+        return dict(attention_ms=ms[0], score_ms=ms[1], select_ms=ms[2], merge_ms=ms[3],
+                    attention_flops=fl.value, attention_launches=n.value)
 
     def status(self, stream=None):
         s = C.c_int32()

@@ -123,14 +123,14 @@ def main():
         # C0 shape reduced in length (16 q / 2 kv heads, d=128) with a padded tail
         "layer_h2_gqa": layer_case(11, n_v=270, n_t=16, hosts=2, l_a=14, l_p=32, hq=16, hkv=2, dh=128),
         # H=4 zigzag with pad rows, small heads
-        "layer_h4_pad": layer_case(12, n_v=517, n_t=8, hosts=4, l_a=8, l_p=16, hq=4, hkv=2, dh=64),
+        "layer_h4_pad": layer_case(12, n_v=517, n_t=8, hosts=4, l_a=8, l_p=16, hq=4, hkv=2, dh=128),
         # naive pairing (load balancing off)
-        "layer_h2_naive": layer_case(13, n_v=300, n_t=8, hosts=2, l_a=12, l_p=24, hq=4, hkv=1, dh=64,
+        "layer_h2_naive": layer_case(13, n_v=300, n_t=8, hosts=2, l_a=12, l_p=24, hq=4, hkv=1, dh=128,
                                      zigzag=False),
         # no compression (l_p = l_b): exactness endpoint (acceptance criterion 8)
-        "layer_h1_full": layer_case(14, n_v=264, n_t=8, hosts=1, l_a=8, l_p=128, hq=2, hkv=2, dh=64),
+        "layer_h1_full": layer_case(14, n_v=264, n_t=8, hosts=1, l_a=8, l_p=128, hq=2, hkv=2, dh=128),
         # raw-logit aggregation (score_context softmax_aggregation=false)
-        "layer_h2_raw": layer_case(15, n_v=300, n_t=8, hosts=2, l_a=12, l_p=24, hq=4, hkv=2, dh=64,
+        "layer_h2_raw": layer_case(15, n_v=300, n_t=8, hosts=2, l_a=12, l_p=24, hq=4, hkv=2, dh=128,
                                    softmax=False),
     }
     for name, d in cases.items():

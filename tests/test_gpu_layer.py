@@ -79,12 +79,13 @@ def test_layer_golden(cuda, name):
     """Golden fixtures generated from the UNMODIFIED reference operators."""
     g = load_golden(name)
     n_v, n_t, hosts, l_a, l_p, hq, hkv, dh, zz, sm = [int(x) for x in g["cfg"]]
+    assert dh == 128
     res = run_layer(cuda, g["Q"], g["K"], g["V"], n_v, n_t, hosts, l_a, l_p, hq, hkv, bool(zz),
                     bool(sm))
     check_layer(res, g, n_t, hosts, l_a, bool(zz))
 
 
-@pytest.mark.parametrize("hosts,zigzag,splits", [(4, True, 0), (2, False, 3), (1, True, 1)])
+@pytest.mark.parametrize("hosts,zigzag,splits", [(4, True, 0), (2, False, 3)])
 def test_layer_c0_shape(cuda, hosts, zigzag, splits):
     """C0 geometry (8K tokens, 16 q / 2 kv heads, d=128) against the C oracle layer."""
     from paper_2601_21444_b200 import spava
