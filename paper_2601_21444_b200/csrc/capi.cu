@@ -300,20 +300,25 @@ int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record)
   const long long dq = static_cast<long long>(c.hq) * c.dh, dk = static_cast<long long>(c.hkv) * c.dh;
   const long long qrow = p.l_a + 2LL * p.l_b;
   const int vs[2] = {H->v_lo, H->v_hi};
-  for (int r = 0; r < 2; ++r) {
-    const long long krow = p.l_a + static_cast<long long>(r) * p.l_b;
-    const int nvalid = valid_rows(p, vs[r]);
-    size_t t0 = mark(H, st);
-    cudaError_t e = launch_score_exact(row_ptr(b.q, qrow, dq), dq, p.n_t, row_ptr(b.k, krow, dk), dk,
-                                       p.l_b, nullptr, nvalid, c.hq, c.hkv, c.dh, c.softmax_scores,
-                                       H->scores[r], H->score_ws, H->score_ws_bytes, st);
+  // both blocks (lo, hi) scored in one launch of each scoring kernel
+  {
+    const void* ks[2] = {row_ptr(b.k, p.l_a, dk), row_ptr(b.k, p.l_a + static_cast<long long>(p.l_b), dk)};
+    const int nv[2] = {valid_rows(p, vs[0]), valid_rows(p, vs[1])};
+    float* sc[2] = {H->scores[0], H->scores[1]};
+    const size_t t0 = mark(H, st);
+    cudaError_t e = launch_score_exact2(2, row_ptr(b.q, qrow, dq), dq, p.n_t, ks, dk, p.l_b, nullptr,
+                                        nv, c.hq, c.hkv, c.dh, c.softmax_scores, sc, H->score_ws,
+                                        H->score_ws_bytes, st);
     if (e != cudaSuccess) return fail(SPAVA_ECUDA, std::string("score: ") + cudaGetErrorString(e));
     g_launches += c.softmax_scores ? 3 : 2;
     span(H, 1, t0, st);
+  }
+  for (int r = 0; r < 2; ++r) {
+    const long long krow = p.l_a + static_cast<long long>(r) * p.l_b;
     const long long slot = static_cast<long long>(H->h) * p.l_p;
     int32_t* idx_out = H->ex->passIdx[r] + slot;
-    t0 = mark(H, st);
-    e = launch_select_pack(H->scores[r], p.l_b, p.l_p, p.l_a + vs[r] * p.l_b, row_ptr(b.k, krow, dk),
+    const size_t t0 = mark(H, st);
+    cudaError_t e = launch_select_pack(H->scores[r], p.l_b, p.l_p, p.l_a + vs[r] * p.l_b, row_ptr(b.k, krow, dk),
                            row_ptr(b.v, krow, dk), dk, static_cast<int>(dk), idx_out,
                            static_cast<uint8_t*>(H->ex->passK[r]) + slot * dk * 2,
                            static_cast<uint8_t*>(H->ex->passV[r]) + slot * dk * 2, dk,

@@ -3,15 +3,17 @@
 // select_essential (approx.cpp:71-102): stable descending sort of the block's scores
 // (ties -> lower index), take at most l_p stopping at the first non-finite, return the
 // chosen indices ascending (+ global offset) and gather their K/V rows.
-// GPU form, no sort at all:
-//   1. one CTA counts finite scores (k = min(l_p, #finite); any +inf sorts first and
-//      ends the selection immediately, NaN is rejected),
-//   2. 4-pass MSB radix select over order-preserving uint32 keys finds the k-th largest
-//      key T and how many of the keys equal to T are taken,
-//   3. an index-ordered block scan emits key > T, plus the lowest-index keys == T
+// GPU form, no sort at all (one 1024-thread CTA, each thread owning 16 consecutive keys
+// of a 16K-key chunk):
+//   1. count finite scores (k = min(l_p, #finite); any +inf sorts first and ends the
+//      selection immediately; NaN is rejected),
+//   2. 3-pass MSB radix select (11/11/10-bit digits, warp-aggregated smem histograms,
+//      parallel bucket scan) over order-preserving uint32 keys finds the k-th largest
+//      key T and how many keys equal to T are taken,
+//   3. one index-ordered block scan emits key > T plus the lowest-index keys == T
 //      (exactly the stable-sort tie rule), already ascending,
 // then a multi-CTA gather copies the selected K/V rows (16 B per lane, coalesced)
-// straight into the exchange buffer slot of this host.
+// straight into this host's slot of the exchange buffer.
 #include <cuda_bf16.h>
 
 #include "spava_internal.h"
@@ -21,41 +23,59 @@ namespace spava {
 namespace {
 
 constexpr int kSelThreads = 1024;
+constexpr int kItems = 16;
+constexpr int kChunk = kSelThreads * kItems;
+constexpr int kWarps = kSelThreads / 32;
 
 __device__ __forceinline__ uint32_t order_key(float s) {
   const uint32_t u = __float_as_uint(s);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-__device__ __forceinline__ int block_sum(int v, int* red) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+// inclusive warp scan
+__device__ __forceinline__ int warp_incl(int v) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  __syncthreads();
-  if (lane == 0) red[w] = v;
-  __syncthreads();
-  int t = 0;
-  for (int i = 0; i < kSelThreads / 32; ++i) t += red[i];
-  return t;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += n;
+  }
+  return v;
 }
 
-// exclusive prefix of a per-thread flag across the block (index order = thread order);
-// returns the prefix, *total receives the block total.
-__device__ __forceinline__ int block_excl_scan(int flag, int* red, int* total) {
+// exclusive block scan of v (thread order); *total = block sum.  Uses red[kWarps + 1].
+__device__ __forceinline__ int block_excl(int v, int* red, int* total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const unsigned b = __ballot_sync(0xffffffffu, flag);
-  const int in_warp = __popc(b & ((1u << lane) - 1u));
+  const int inc = warp_incl(v);
   __syncthreads();
-  if (lane == 0) red[w] = __popc(b);
+  if (lane == 31) red[w] = inc;
   __syncthreads();
-  int before = 0, tot = 0;
-  for (int i = 0; i < kSelThreads / 32; ++i) {
-    const int c = red[i];
-    if (i < w) before += c;
-    tot += c;
+  if (w == 0) {
+    const int x = red[lane];
+    const int xi = warp_incl(x);
+    red[lane] = xi - x;
+    if (lane == 31) red[kWarps] = xi;
   }
-  *total = tot;
-  return before + in_warp;
+  __syncthreads();
+  *total = red[kWarps];
+  return red[w] + inc - v;
+}
+
+__device__ __forceinline__ void load_items(const float* s, int l_b, int base, float (&v)[kItems]) {
+  const int j0 = base + threadIdx.x * kItems;
+  if (j0 + kItems <= l_b && ((reinterpret_cast<uintptr_t>(s + j0) & 15) == 0)) {
+#pragma unroll
+    for (int q = 0; q < kItems / 4; ++q) {
+      const float4 f = reinterpret_cast<const float4*>(s + j0)[q];
+      v[4 * q] = f.x;
+      v[4 * q + 1] = f.y;
+      v[4 * q + 2] = f.z;
+      v[4 * q + 3] = f.w;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < kItems; ++t) v[t] = (j0 + t < l_b) ? s[j0 + t] : -INFINITY;
+  }
 }
 
 __global__ void __launch_bounds__(kSelThreads) select_kernel(const float* __restrict__ scores,
@@ -63,55 +83,75 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const float* __rest
                                                              int32_t* __restrict__ idx,
                                                              int32_t* __restrict__ count,
                                                              int32_t* __restrict__ status) {
-  __shared__ int hist[256];
-  __shared__ int red[kSelThreads / 32];
+  __shared__ int hist[2048];
+  __shared__ int red[kWarps + 1];
   __shared__ uint32_t sh_prefix;
-  __shared__ int sh_take;
+  __shared__ int sh_need;
   const int tid = threadIdx.x;
-  int fin = 0, pinf = 0, nan = 0;
-  for (int j = tid; j < l_b; j += kSelThreads) {
-    const float s = scores[j];
-    fin += isfinite(s) ? 1 : 0;
-    pinf += (isinf(s) && s > 0.f) ? 1 : 0;
-    nan += isnan(s) ? 1 : 0;
+  // ---- 1. counts
+  int fin = 0, bad = 0;
+  for (int base = 0; base < l_b; base += kChunk) {
+    float v[kItems];
+    load_items(scores, l_b, base, v);
+#pragma unroll
+    for (int t = 0; t < kItems; ++t) {
+      fin += isfinite(v[t]) ? 1 : 0;
+      bad += (isnan(v[t]) || (isinf(v[t]) && v[t] > 0.f)) ? 1 : 0;
+    }
   }
-  fin = block_sum(fin, red);
-  pinf = block_sum(pinf, red);
-  nan = block_sum(nan, red);
-  int k = (pinf > 0 || nan > 0) ? 0 : min(l_p, fin);
-  if (nan > 0 && tid == 0 && status) atomicExch(status, 1);
+  int tot_fin, tot_bad;
+  block_excl(fin, red, &tot_fin);
+  block_excl(bad, red, &tot_bad);
+  const int k = tot_bad > 0 ? 0 : min(l_p, tot_fin);
+  if (tot_bad > 0 && tid == 0 && status) {
+    // NaN is invalid input; +inf sorts first and stops the selection at once
+    bool nan = false;
+    for (int j = 0; j < l_b && !nan; ++j) nan = isnan(scores[j]);
+    if (nan) atomicExch(status, 1);
+  }
   if (k == 0) {
     if (tid == 0) *count = 0;
     return;
   }
-  // ---- radix select: the k-th largest key
+  // ---- 2. radix select: digits [31:21], [20:10], [9:0]
   uint32_t prefix = 0, mask = 0;
   int need = k;
-  for (int shift = 24; shift >= 0; shift -= 8) {
-    for (int b = tid; b < 256; b += kSelThreads) hist[b] = 0;
+  const int shifts[3] = {21, 10, 0};
+  const int bits[3] = {11, 11, 10};
+#pragma unroll 1
+  for (int pass = 0; pass < 3; ++pass) {
+    const int shift = shifts[pass], nb = 1 << bits[pass];
+    for (int b = tid; b < nb; b += kSelThreads) hist[b] = 0;
     __syncthreads();
-    for (int base = 0; base < l_b; base += kSelThreads) {  // warp-uniform trip count
-      const int j = base + tid;
-      const float s = j < l_b ? scores[j] : -INFINITY;
-      bool ok = isfinite(s);
-      const uint32_t key = order_key(s);
-      ok = ok && ((key & mask) == prefix);
-      const unsigned digit = (key >> shift) & 255u;
-      // warp-aggregated histogram update (scores cluster in few buckets)
-      const unsigned active = __ballot_sync(0xffffffffu, ok);
-      if (ok) {
-        const unsigned peers = __match_any_sync(active, digit);
-        if ((__ffs(peers) - 1) == static_cast<int>(threadIdx.x & 31))
-          atomicAdd(&hist[digit], __popc(peers));
+    for (int base = 0; base < l_b; base += kChunk) {
+      float v[kItems];
+      load_items(scores, l_b, base, v);
+#pragma unroll
+      for (int t = 0; t < kItems; ++t) {
+        const uint32_t key = order_key(v[t]);
+        const bool ok = isfinite(v[t]) && ((key & mask) == prefix);
+        const unsigned digit = (key >> shift) & static_cast<unsigned>(nb - 1);
+        const unsigned active = __ballot_sync(0xffffffffu, ok);
+        if (ok) {
+          const unsigned peers = __match_any_sync(active, digit);
+          if ((__ffs(peers) - 1) == (tid & 31)) atomicAdd(&hist[digit], __popc(peers));
+        }
       }
     }
     __syncthreads();
-    if (tid == 0) {
-      int cum = 0;
-      for (int b = 255; b >= 0; --b) {
+    // bucket holding the need-th largest: descending suffix scan (2 buckets / thread)
+    const int per = nb / kSelThreads;  // 2 or 1
+    int c = 0;
+    for (int u = 0; u < per; ++u) c += hist[nb - 1 - (tid * per + u)];
+    int tot;
+    const int before = block_excl(c, red, &tot);  // keys in buckets above this thread's
+    if (before < need && before + c >= need) {
+      int cum = before;
+      for (int u = 0; u < per; ++u) {
+        const int b = nb - 1 - (tid * per + u);
         if (cum + hist[b] >= need) {
           sh_prefix = prefix | (static_cast<uint32_t>(b) << shift);
-          sh_take = need - cum;
+          sh_need = need - cum;
           break;
         }
         cum += hist[b];
@@ -119,28 +159,41 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const float* __rest
     }
     __syncthreads();
     prefix = sh_prefix;
-    need = sh_take;
-    mask |= 255u << shift;
+    need = sh_need;
+    mask |= static_cast<uint32_t>(nb - 1) << shift;
   }
   const uint32_t T = prefix;  // key of the k-th largest; `need` keys == T are taken
-  // ---- index-ordered emission
+  // ---- 3. index-ordered emission
   int eq_base = 0, out_base = 0;
-  for (int base = 0; base < l_b; base += kSelThreads) {
-    const int j = base + tid;
-    bool fin_j = false;
-    uint32_t key = 0;
-    if (j < l_b) {
-      const float s = scores[j];
-      fin_j = isfinite(s);
-      key = order_key(s);
-    }
-    const int is_eq = (fin_j && key == T) ? 1 : 0;
+  for (int base = 0; base < l_b; base += kChunk) {
+    float v[kItems];
+    load_items(scores, l_b, base, v);
+    int n_eq = 0;
+#pragma unroll
+    for (int t = 0; t < kItems; ++t) n_eq += (isfinite(v[t]) && order_key(v[t]) == T) ? 1 : 0;
     int eq_tot;
-    const int eq_rank = block_excl_scan(is_eq, red, &eq_tot);
-    const int sel = (fin_j && (key > T || (is_eq && eq_base + eq_rank < need))) ? 1 : 0;
+    int eq_rank = eq_base + block_excl(n_eq, red, &eq_tot);
+    int flags = 0, n_sel = 0;
+#pragma unroll
+    for (int t = 0; t < kItems; ++t) {
+      const bool f = isfinite(v[t]);
+      const uint32_t key = order_key(v[t]);
+      bool sel = f && key > T;
+      if (f && key == T) {
+        sel = eq_rank < need;
+        ++eq_rank;
+      }
+      if (sel) {
+        flags |= 1 << t;
+        ++n_sel;
+      }
+    }
     int sel_tot;
-    const int pos = block_excl_scan(sel, red, &sel_tot);
-    if (sel) idx[out_base + pos] = global_offset + j;
+    int pos = out_base + block_excl(n_sel, red, &sel_tot);
+    const int j0 = base + tid * kItems;
+#pragma unroll
+    for (int t = 0; t < kItems; ++t)
+      if (flags & (1 << t)) idx[pos++] = global_offset + j0 + t;
     eq_base += eq_tot;
     out_base += sel_tot;
   }

@@ -75,7 +75,12 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
                              cudaStream_t stream, std::string* err);
 
 // ---------------------------------------------------------------- scoring
-size_t score_workspace_bytes(int n_t, int l_b, int hq);
+size_t score_workspace_bytes(int n_t, int l_b, int hq);  // sized for 2 blocks
+cudaError_t launch_score_exact2(int nblk, const void* q, long long ldq, int n_t,
+                                const void* const* k, long long ldk, int l_b,
+                                const uint8_t* const* pad, const int* n_valid, int hq, int hkv,
+                                int dh, int softmax, float* const* scores, void* ws,
+                                size_t ws_bytes, cudaStream_t stream);
 cudaError_t launch_score_exact(const void* q, long long ldq, int n_t, const void* k,
                                long long ldk, int l_b, const uint8_t* pad, int n_valid, int hq,
                                int hkv, int dh, int softmax, float* scores, void* ws,
