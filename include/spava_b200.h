@@ -195,6 +195,10 @@ int spava_host_set_timing(spava_host* host, int enable);
 int spava_host_timing(spava_host* host, double* ms_by_class4, double* attn_flops,
                       uint64_t* attn_launches);
 
+/* Development: read-and-reset the cycle counters of the instrumented attention
+ * variant (SPAVA_ATTN_VARIANT=5): 16 uint64 (see attention.cu).            */
+int spava_debug_attn_prof(uint64_t* out16);
+
 /* Number of kernels the library launched since process start (for bench's
  * gpu_launches claim). */
 uint64_t spava_kernel_launches(void);

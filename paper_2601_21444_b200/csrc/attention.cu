@@ -27,6 +27,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -37,7 +38,8 @@ namespace spava {
 
 namespace {
 
-constexpr int kStages = 2;
+constexpr int kVStages = 2;      // V ring depth
+constexpr int kMaxKStages = 3;   // K ring depth (template parameter, <= 3)
 constexpr int kSoftmaxWarps = 8;
 constexpr int kProducerWarp = 8;
 constexpr int kMmaWarp = 9;
@@ -46,16 +48,52 @@ constexpr uint32_t kBoxBytes = 128 * 64 * 2;    // 128 rows x 64 bf16, one SW128
 constexpr uint32_t kTileBytes = 2 * kBoxBytes;  // 128 rows x 128 dh
 constexpr uint32_t kTmemCols = 512;             // S0 | S1 | O0 | O1
 
+template <int KS>
 struct Smem {
   static constexpr uint32_t q = 0;
   static constexpr uint32_t k = q + kTilesPerCta * kTileBytes;
-  static constexpr uint32_t v = k + kStages * kTileBytes;
-  static constexpr uint32_t bar = v + kStages * kTileBytes;
+  static constexpr uint32_t v = k + KS * kTileBytes;
+  static constexpr uint32_t bar = v + kVStages * kTileBytes;
   static constexpr uint32_t total = bar + 256;
+  static constexpr uint32_t bytes = total + 1024;  // + alignment slack
 };
-constexpr uint32_t kSmemBytes = Smem::total + 1024;  // + alignment slack
 
 enum : int { kSkip = 0, kFull = 1, kPart = 2 };
+
+// dev-only cycle accounting (variant 5): 0 mma wait K, 1 mma wait V, 2 mma wait P,
+// 3 mma loop total, 4 softmax wait S, 5 softmax body, 6 softmax tiles, 7 rescales,
+// 8 softmax S-load, 9 softmax max
+__device__ unsigned long long g_attn_prof[16];
+#define PROF_NOW() (kProf ? clock64() : 0ll)
+
+
+// 2^x for finite x <= 8 (x clamped at -125), fp32 pair: x = n + f, n = rint(x) via the
+// 1.5*2^23 magic add, 2^f (|f| <= 1/2) by a minimax cubic (max rel. err 7.8e-5), and n
+// added to the exponent field.
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 magic = make_float2(0x1.8p23f, 0x1.8p23f);
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 r = __fadd2_rn(t, make_float2(-0x1.8p23f, -0x1.8p23f));
+  const float2 f = __ffma2_rn(r, make_float2(-1.f, -1.f), x);
+  float2 p = __ffma2_rn(make_float2(0x1.c4c0d0p-5f, 0x1.c4c0d0p-5f), f,
+                        make_float2(0x1.f0e306p-3f, 0x1.f0e306p-3f));
+  p = __ffma2_rn(p, f, make_float2(0x1.62f0d0p-1f, 0x1.62f0d0p-1f));
+  p = __ffma2_rn(p, f, make_float2(0x1.fff66cp-1f, 0x1.fff66cp-1f));
+  // bits(t) = bits(1.5*2^23) + n and bits(1.5*2^23) << 23 == 0 (mod 2^32): one IMAD per lane
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&pk)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]), "r"(pk[4]), "r"(pk[5]), "r"(pk[6]),
+      "r"(pk[7]), "r"(pk[8]), "r"(pk[9]), "r"(pk[10]), "r"(pk[11]), "r"(pk[12]), "r"(pk[13]),
+      "r"(pk[14]), "r"(pk[15]));
+}
 
 __device__ __forceinline__ int seg_tiles(const AttnSeg& s, int imax) {
   const int klen = s.causal ? min(s.len, imax) : s.len;
@@ -96,22 +134,26 @@ __device__ __forceinline__ void cursor_next(const AttnProb& p, int imax, Cursor&
   }
 }
 
+template <int kEmu, int KS, bool kProf = false>
 __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ AttnParams P) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::bar);
+  using SL = Smem<KS>;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SL::bar);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;    // [kStages]
-  uint64_t* v_full = bars + 3;    // [kStages]
-  uint64_t* kv_empty = bars + 5;  // [kStages]
-  uint64_t* s_full = bars + 7;    // [2] S_t ready in TMEM
-  uint64_t* p_full = bars + 9;    // [2] P_t written (and O_t corrected)
-  uint64_t* o_full = bars + 11;   // [2] PV_t complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+  uint64_t* k_full = bars + 1;                // [KS]
+  uint64_t* k_empty = k_full + kMaxKStages;   // [KS] freed once both QK of the tile completed
+  uint64_t* v_full = k_empty + kMaxKStages;   // [kVStages]
+  uint64_t* v_empty = v_full + kVStages;      // [kVStages] freed once both PV completed
+  uint64_t* s_full = v_empty + kVStages;      // [2] S_t ready in TMEM
+  uint64_t* p_full = s_full + 2;              // [2] P_t written (and O_t corrected)
+  uint64_t* o_full = p_full + 2;              // [2] PV_t complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
 
   const int warp = warp_id();
   const int lane = lane_id();
+  long long pr[14] = {};
 
   // ---- decode the work item: problem, 256-row unit (heaviest first), head, split
   int pi = 0;
@@ -120,13 +162,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   int local = static_cast<int>(blockIdx.x) - prob.work_begin;
   const int split = local % prob.splits;
   local /= prob.splits;
-  const int head = local % P.hq;
-  local /= P.hq;
+  // head pairing (nq <= 128, even GQA group): the two Q tiles are q-heads h, h+1 of one
+  // kv group over the same rows, sharing every K/V tile
+  const int pair = prob.head_pair;
+  const int nheads = pair ? P.hq / 2 : P.hq;
+  const int head = pair ? 2 * (local % nheads) : local % nheads;
+  local /= nheads;
   const int unit = prob.units - 1 - local;
-  const int i0 = unit * (kTilesPerCta * kBlockM);
+  const int i0 = pair ? 0 : unit * (kTilesPerCta * kBlockM);
   const int nq = prob.nq;
-  const int imax = min(i0 + kTilesPerCta * kBlockM, nq);
+  const int imax = min(i0 + (pair ? kBlockM : kTilesPerCta * kBlockM), nq);
   const int hk = head / (P.hq / P.hkv);
+  // Q tile t covers rows [r0(t), r0(t)+128) of q-head head + pair*t
+#define TILE_R0(t) (pair ? 0 : i0 + (t) * kBlockM)
+#define TILE_HEAD(t) (head + pair * (t))
 
   int T = 0;
   for (int s = 0; s < prob.nseg; ++s) T += seg_tiles(prob.seg[s], imax);
@@ -137,10 +186,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 
   if (warp == kProducerWarp && elect_one()) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < KS; ++s) {
       mbar_init(k_full + s, 1);
+      mbar_init(k_empty + s, 1);
+    }
+    for (int s = 0; s < kVStages; ++s) {
       mbar_init(v_full + s, 1);
-      mbar_init(kv_empty + s, 1);
+      mbar_init(v_empty + s, 1);
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(s_full + t, 1);
@@ -163,25 +215,26 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   if (warp == kProducerWarp) {
     // ======================================================== TMA producer
     if (elect_one()) {
-      const bool has1 = i0 + kBlockM < nq;
+      const bool has1 = TILE_R0(1) < nq;
       mbar_expect_tx(q_full, (has1 ? 2u : 1u) * kTileBytes);
       for (int qt = 0; qt < (has1 ? 2 : 1); ++qt)
         for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + Smem::q + qt * kTileBytes + c * kBoxBytes, &tm[0], q_full,
-                      head * kHeadDim + c * 64, i0 + qt * kBlockM);
+          tma_load_2d(smem + SL::q + qt * kTileBytes + c * kBoxBytes, &tm[0], q_full,
+                      TILE_HEAD(qt) * kHeadDim + c * 64, TILE_R0(qt));
       Cursor cur = cursor_at(prob, imax, t_begin);
       for (int it = 0; it < ntiles; ++it) {
-        const int stage = it % kStages;
-        if (it >= kStages) mbar_wait(kv_empty + stage, ((it / kStages) - 1) & 1);
         const CUtensorMap* km = &tm[1 + 2 * cur.seg];
         const CUtensorMap* vm = &tm[2 + 2 * cur.seg];
-        mbar_expect_tx(k_full + stage, kTileBytes);
+        const int ks = it % KS, vs = it % kVStages;
+        if (it >= KS) mbar_wait(k_empty + ks, ((it / KS) - 1) & 1);
+        mbar_expect_tx(k_full + ks, kTileBytes);
         for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + Smem::k + stage * kTileBytes + c * kBoxBytes, km, k_full + stage,
+          tma_load_2d(smem + SL::k + ks * kTileBytes + c * kBoxBytes, km, k_full + ks,
                       hk * kHeadDim + c * 64, cur.kt * kBlockN);
-        mbar_expect_tx(v_full + stage, kTileBytes);
+        if (it >= kVStages) mbar_wait(v_empty + vs, ((it / kVStages) - 1) & 1);
+        mbar_expect_tx(v_full + vs, kTileBytes);
         for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + Smem::v + stage * kTileBytes + c * kBoxBytes, vm, v_full + stage,
+          tma_load_2d(smem + SL::v + vs * kTileBytes + c * kBoxBytes, vm, v_full + vs,
                       hk * kHeadDim + c * 64, cur.kt * kBlockN);
         cursor_next(prob, imax, cur);
       }
@@ -191,9 +244,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     if (elect_one()) {
       const uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);  // Q, K both K-major
       const uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);  // P (TMEM), V MN-major
-      const uint32_t sq = smem_u32(smem + Smem::q);
-      const uint32_t sk = smem_u32(smem + Smem::k);
-      const uint32_t sv = smem_u32(smem + Smem::v);
+      const uint32_t sq = smem_u32(smem + SL::q);
+      const uint32_t sk = smem_u32(smem + SL::k);
+      const uint32_t sv = smem_u32(smem + SL::v);
       auto issue_qk = [&](int qt, int stage) {
         const uint32_t d = tmem + qt * 128;
 #pragma unroll
@@ -216,13 +269,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 
       mbar_wait(q_full, 0);
       tc_fence_after();
+      const long long tm0 = PROF_NOW();
       Cursor cur = cursor_at(prob, imax, t_begin);
       int mode[2] = {kSkip, kSkip};
       uint32_t p_cnt[2] = {0, 0};
       bool o_acc[2] = {false, false};
       if (ntiles > 0) {
         for (int qt = 0; qt < 2; ++qt)
-          mode[qt] = tile_mode(prob.seg[cur.seg], cur.kt, i0 + qt * kBlockM, nq);
+          mode[qt] = tile_mode(prob.seg[cur.seg], cur.kt, TILE_R0(qt), nq);
         mbar_wait(k_full + 0, 0);
         tc_fence_after();
         for (int qt = 0; qt < 2; ++qt)
@@ -230,47 +284,60 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
             issue_qk(qt, 0);
             tc_commit(s_full + qt);
           }
+        tc_commit(k_empty + 0);
       }
+      // Issue order per tile it: PV0(it) QK0(it+1) PV1(it) [free V(it)] QK1(it+1) [free K(it+1)].
+      // P_t aliases S_t in TMEM, so QK_t(it+1) may only follow PV_t(it) (tcgen05 is in-order).
       for (int it = 0; it < ntiles; ++it) {
-        const int stage = it % kStages;
-        const uint32_t ph = (it / kStages) & 1;
+        const int vs = it % kVStages;
         const bool has_next = it + 1 < ntiles;
         Cursor nxt = cur;
         int nmode[2] = {kSkip, kSkip};
-        const int nstage = (it + 1) % kStages;
+        const int kn = (it + 1) % KS;
         if (has_next) {
           cursor_next(prob, imax, nxt);
           for (int qt = 0; qt < 2; ++qt)
-            nmode[qt] = tile_mode(prob.seg[nxt.seg], nxt.kt, i0 + qt * kBlockM, nq);
-          mbar_wait(k_full + nstage, ((it + 1) / kStages) & 1);
+            nmode[qt] = tile_mode(prob.seg[nxt.seg], nxt.kt, TILE_R0(qt), nq);
+          const long long tw = PROF_NOW();
+          mbar_wait(k_full + kn, ((it + 1) / KS) & 1);
+          if (kProf) pr[0] += PROF_NOW() - tw;
         }
-        mbar_wait(v_full + stage, ph);
+        {
+          const long long tw = PROF_NOW();
+          mbar_wait(v_full + vs, (it / kVStages) & 1);
+          if (kProf) pr[1] += PROF_NOW() - tw;
+        }
         tc_fence_after();
         for (int qt = 0; qt < 2; ++qt) {
           if (mode[qt] != kSkip) {
+            const long long tw = PROF_NOW();
             mbar_wait(p_full + qt, p_cnt[qt] & 1);
+            if (kProf) pr[2] += PROF_NOW() - tw;
             tc_fence_after();
-            issue_pv(qt, stage, o_acc[qt]);
+            issue_pv(qt, vs, o_acc[qt]);
             o_acc[qt] = true;
             ++p_cnt[qt];
             tc_commit(o_full + qt);
           }
+          if (qt == 1) tc_commit(v_empty + vs);
           if (nmode[qt] != kSkip) {
-            issue_qk(qt, nstage);
+            issue_qk(qt, kn);
             tc_commit(s_full + qt);
           }
         }
-        tc_commit(kv_empty + stage);
+        if (has_next) tc_commit(k_empty + kn);
         cur = nxt;
         mode[0] = nmode[0];
         mode[1] = nmode[1];
       }
+      if (kProf) pr[3] += PROF_NOW() - tm0;
     }
-  } else {
+  } else if (warp < kProducerWarp) {
     // ======================================================== softmax warpgroups
     const int qt = warp >> 2;
     const int quad = warp & 3;
-    const int row = i0 + qt * kBlockM + quad * 32 + lane;  // problem-local query row
+    const int row = TILE_R0(qt) + quad * 32 + lane;  // problem-local query row
+    const int qhead = TILE_HEAD(qt);
     const uint32_t t_lane = static_cast<uint32_t>(quad * 32) << 16;
     const uint32_t tS = tmem + t_lane + qt * 128;
     const uint32_t tO = tmem + t_lane + 256 + qt * 128;
@@ -281,59 +348,112 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     Cursor cur = cursor_at(prob, imax, t_begin);
     for (int it = 0; it < ntiles; ++it, cursor_next(prob, imax, cur)) {
       const AttnSeg sg = prob.seg[cur.seg];
-      const int mode = tile_mode(sg, cur.kt, i0 + qt * kBlockM, nq);
+      const int mode = tile_mode(sg, cur.kt, TILE_R0(qt), nq);
       if (mode == kSkip) continue;
+      const long long tw0 = PROF_NOW();
       mbar_wait(s_full + qt, cnt & 1);
+      const long long tw1 = PROF_NOW();
+      if (kProf) pr[4] += tw1 - tw0;
       tc_fence_after();
-      uint32_t sr[4][32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(tS + 32 * c, sr[c]);
-      tmem_wait_ld();
+      float alpha = 1.f;
+      bool rescale = false;
+      float2 sum2 = make_float2(0.f, 0.f);
+      int lim = kBlockN;  // keys c < lim visible (kPart tiles only)
       if (mode == kPart) {
         const int k0 = cur.kt * kBlockN;
-        int lim = sg.len - k0;
+        lim = sg.len - k0;
         if (sg.causal) lim = min(lim, row - k0 + 1);
+      }
+      const float2 sl2v = make_float2(sl2, sl2);
+      uint32_t sr[4][32];
+      uint32_t pk[4][16];
+      // exp + bf16 pack of one 32-key chunk against reference max m (-m in negm)
+      auto chunk_exp = [&](int c, float2 negm, bool emu, float2 (&sacc)[4]) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 x2 = __ffma2_rn(
+              make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1])), sl2v, negm);
+          float2 p2;
+          if (kEmu > 0 && emu && (j % (16 / kEmu)) == (16 / kEmu) - 1)
+            p2 = exp2_poly2(x2);
+          else
+            p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));  // -inf -> 0
+          sacc[j & 3] = __fadd2_rn(sacc[j & 3], p2);
+          __nv_bfloat162 b = __floats2bfloat162_rn(p2.x, p2.y);  // .x (low) = even key
+          pk[c][j] = *reinterpret_cast<uint32_t*>(&b);
+        }
+      };
+      auto chunk_max = [&](int c, float (&mxp)[8]) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const int t = (j / 2) & 7;
+          mxp[t] = fmaxf(mxp[t], fmaxf(__uint_as_float(sr[c][j]), __uint_as_float(sr[c][j + 1])));
+        }
+      };
+      auto load_s = [&]() {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(tS + 32 * c, sr[c]);
+        tmem_wait_ld();
+      };
+      float mxp[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
+      float2 sacc[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
+      bool done = false;
+      load_s();
+      if (mode == kFull && m_ref != -INFINITY) {
+        // speculative pass against the running max m_ref: the tile max is folded in on the
+        // side instead of sitting on the critical path; P is kept in registers and only
+        // committed to TMEM if the tile max stayed within m_ref + 8 (P <= 2^8), the common
+        // case after the first tiles; otherwise S is re-read and the exact path runs.
+        const float2 negm = make_float2(-m_ref, -m_ref);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          chunk_max(c, mxp);
+          chunk_exp(c, negm, true, sacc);
+        }
+        const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                               fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+        done = !(mx * sl2 > m_ref + 8.f);
+        if (!done) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
+          load_s();
+        }
+      } else if (mode == kPart) {
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             if (c * 32 + j >= lim) sr[c][j] = __float_as_uint(-INFINITY);
       }
-      float mx = -INFINITY;
+      if (kProf) pr[8] += PROF_NOW() - tw1;
+      if (!done) {
+        // max first, lazy rescale (keep a stale max while p <= 2^8), then exps
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+        for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(sr[c][j]));
-      const float m_new = fmaxf(m_ref, mx * sl2);
-      float alpha = 1.f;
-      bool rescale = false;
-      if (m_new > m_ref + 8.f) {  // lazy rescale: keep a stale max while p <= 2^8
-        alpha = exp2f(m_ref - m_new);
-        m_ref = m_new;
-        rescale = true;
-      }
-      const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
-      float sum0 = 0.f, sum1 = 0.f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float p0 = fast_exp2(fmaf(__uint_as_float(sr[c][2 * j]), sl2, -m_use));
-          const float p1 = fast_exp2(fmaf(__uint_as_float(sr[c][2 * j + 1]), sl2, -m_use));
-          sum0 += p0;
-          sum1 += p1;
-          __nv_bfloat162 b = __floats2bfloat162_rn(p0, p1);  // .x (low) = even key
-          pk[j] = *reinterpret_cast<uint32_t*>(&b);
+        for (int c = 0; c < 4; ++c) chunk_max(c, mxp);
+        const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                               fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+        const float m_new = fmaxf(m_ref, mx * sl2);
+        if (m_new > m_ref + 8.f) {
+          alpha = exp2f(m_ref - m_new);
+          m_ref = m_new;
+          rescale = true;
         }
-        asm volatile(
-            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-            "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(tS + 16 * c),
-            "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]), "r"(pk[4]), "r"(pk[5]), "r"(pk[6]),
-            "r"(pk[7]), "r"(pk[8]), "r"(pk[9]), "r"(pk[10]), "r"(pk[11]), "r"(pk[12]),
-            "r"(pk[13]), "r"(pk[14]), "r"(pk[15]));
+        const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+        const float2 negm = make_float2(-m_use, -m_use);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) chunk_exp(c, negm, mode == kFull, sacc);
       }
-      l = l * alpha + (sum0 + sum1);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_st16(tS + 16 * c, pk[c]);
+      sum2 = __fadd2_rn(__fadd2_rn(sacc[0], sacc[1]), __fadd2_rn(sacc[2], sacc[3]));
+      const long long tp3 = PROF_NOW();
+      l = l * alpha + (sum2.x + sum2.y);
       if (rescale && cnt > 0) {
         mbar_wait(o_full + qt, (cnt - 1) & 1);  // PV_{cnt-1} has landed in O
         tc_fence_after();
@@ -350,6 +470,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(p_full + qt);
+      if (kProf) {
+        pr[12] += PROF_NOW() - tp3;
+        pr[5] += PROF_NOW() - tw1;
+        pr[6] += 1;
+        pr[7] += rescale ? 1 : 0;
+      }
       ++cnt;
     }
     // ---- epilogue: O / l, lse
@@ -360,7 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     const bool valid_row = row < nq;
     const float inv = (l > 0.f) ? 1.f / l : 0.f;
     const long long obase = static_cast<long long>(split) * prob.split_stride_out +
-                            static_cast<long long>(row) * prob.ldo + head * kHeadDim;
+                            static_cast<long long>(row) * prob.ldo + qhead * kHeadDim;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       uint32_t o[32];
@@ -398,14 +524,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     if (valid_row && prob.lse) {
       const float lse = (l > 0.f) ? (m_ref + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
       prob.lse[static_cast<long long>(split) * prob.split_stride_lse +
-               static_cast<long long>(row) * prob.ld_lse + head] = lse;
+               static_cast<long long>(row) * prob.ld_lse + qhead] = lse;
     }
   }
 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (kProf && (warp == kMmaWarp || (warp < kProducerWarp && lane == 0)))
+    for (int i = 0; i < 14; ++i)
+      if (pr[i]) atomicAdd(&g_attn_prof[i], static_cast<unsigned long long>(pr[i]));
   if (warp == kMmaWarp) tmem_dealloc(tmem, kTmemCols);
+#undef TILE_R0
+#undef TILE_HEAD
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
@@ -476,7 +607,8 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
     AttnProb& p = P.prob[np];
     p.nq = v.nq;
     p.nseg = v.nseg;
-    p.units = (v.nq + kTilesPerCta * kBlockM - 1) / (kTilesPerCta * kBlockM);
+    p.head_pair = (v.nq <= kBlockM && (hq / hkv) % 2 == 0) ? 1 : 0;
+    p.units = p.head_pair ? 1 : (v.nq + kTilesPerCta * kBlockM - 1) / (kTilesPerCta * kBlockM);
     p.splits = v.splits;
     p.work_begin = work;
     p.out_f32 = v.out_f32;
@@ -501,21 +633,54 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
                      static_cast<long long>(hkv) * dh, v.seg[s].ld, err))
         return cudaErrorInvalidValue;
     }
-    work += p.units * hq * p.splits;
+    work += p.units * (p.head_pair ? hq / 2 : hq) * p.splits;
     ++np;
   }
   P.nprob = np;
   P.total_work = work;
   if (work == 0) return cudaSuccess;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmemBytes));
+  // kernel variant: <emulated exp2 pairs per 32-key chunk, K ring depth[, cycle counters]>
+  using KFn = void (*)(AttnParams);
+  struct Var { KFn fn; uint32_t smem; };
+  // 0: production (MUFU exp2, speculative stale-max softmax, 2-deep K/V rings)
+  // 1: 25% of exp2 on the FMA pipe (FA4-style; measured slightly slower here)
+  // 2: production + per-phase cycle counters (dev, SPAVA_ATTN_VARIANT=2)
+  static const Var variants[] = {{attn_fwd_kernel<0, 2>, Smem<2>::bytes},
+                                 {attn_fwd_kernel<4, 2>, Smem<2>::bytes},
+                                 {attn_fwd_kernel<0, 2, true>, Smem<2>::bytes}};
+  constexpr int kNumVar = sizeof(variants) / sizeof(variants[0]);
+  static int vsel = [] {
+    const char* e = getenv("SPAVA_ATTN_VARIANT");
+    const int v = e ? atoi(e) : 0;
+    return (v >= 0 && v < kNumVar) ? v : 0;
+  }();
+  static bool attr_set[kNumVar] = {};
+  const KFn fn = variants[vsel].fn;
+  const uint32_t smem_bytes = variants[vsel].smem;
+  if (!attr_set[vsel]) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem_bytes));
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[vsel] = true;
   }
-  attn_fwd_kernel<<<work, kThreads, kSmemBytes, stream>>>(P);
-  return cudaGetLastError();
+  fn<<<work, kThreads, smem_bytes, stream>>>(P);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && err) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, fn);
+    *err = std::string("attention launch: ") + cudaGetErrorString(e) + " (regs " +
+           std::to_string(fa.numRegs) + ", maxThreads " + std::to_string(fa.maxThreadsPerBlock) +
+           ", static smem " + std::to_string(fa.sharedSizeBytes) + ", local " +
+           std::to_string(fa.localSizeBytes) + ", params " + std::to_string(sizeof(AttnParams)) + ")";
+  }
+  return e;
+}
+
+// dev: read and reset the cycle counters of the profiling variant
+void attn_prof_read(unsigned long long* out16) {
+  cudaMemcpyFromSymbol(out16, g_attn_prof, sizeof(unsigned long long) * 16);
+  static const unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(g_attn_prof, z, sizeof(z));
 }
 
 }  // namespace spava

@@ -270,10 +270,12 @@ int merge_impl(const MergeParams& mp, cudaStream_t st, spava_host* H = nullptr) 
   return SPAVA_OK;
 }
 
-int auto_splits(int nq, int hq, int total_keys) {
-  const int units = (nq + 255) / 256;
+// split-KV factor giving about one wave of CTAs (148 SMs) for a short query block
+int auto_splits(int nq, int hq, int hkv, int total_keys) {
+  const bool pair = nq <= kBlockM && (hq / hkv) % 2 == 0;  // mirrors launch_attention
+  const int ctas = pair ? hq / 2 : hq * ((nq + 255) / 256);
   const int tiles = std::max(1, (total_keys + kBlockN - 1) / kBlockN);
-  int s = (2 * 148 + hq * units - 1) / (hq * units);
+  int s = (148 + ctas - 1) / ctas;
   s = std::min(s, tiles);
   s = std::min(s, 32);
   return std::max(1, s);
@@ -520,6 +522,11 @@ const char* spava_last_error(void) { return g_err.c_str(); }
 const char* spava_version(void) { return "spava-b200 0.1 (sm_100a)"; }
 int spava_device_ok(void) { return device_ok_impl() ? 1 : 0; }
 uint64_t spava_kernel_launches(void) { return g_launches.load(); }
+
+int spava_debug_attn_prof(uint64_t* out16) {
+  attn_prof_read(reinterpret_cast<unsigned long long*>(out16));
+  return SPAVA_OK;
+}
 
 int spava_make_plan(int n_v, int n_t, int hosts, int l_a, int l_p, int zigzag, spava_plan* out) {
   return plan_impl(n_v, n_t, hosts, l_a, l_p, zigzag, out);
@@ -779,7 +786,7 @@ int spava_host_create(spava_fabric* F, int h, spava_host** out) {
   const int designated = c.designated < 0 ? p.hosts - 1 : c.designated;
   H->self_keys = c.query_self_all || h == designated;
   const int keys = (H->a1 - H->a0) + 2 * p.l_b + (H->self_keys ? p.n_t : 0);
-  H->splits = c.query_splits > 0 ? std::min(c.query_splits, kMaxMergeParts) : auto_splits(p.n_t, c.hq, keys);
+  H->splits = c.query_splits > 0 ? std::min(c.query_splits, kMaxMergeParts) : auto_splits(p.n_t, c.hq, c.hkv, keys);
   if (F->nccl) {
     int s = H->own.alloc(c, p);
     if (s != SPAVA_OK) {

@@ -60,6 +60,54 @@ __device__ __forceinline__ bool is_pad(const uint8_t* pad, int n_valid, int j) {
   return j >= n_valid || (pad && pad[j]);
 }
 
+// 2^(j/64), j = 0..63, correctly rounded (generated with 60-digit decimal arithmetic)
+__device__ __constant__ double c_exp2_64[64] = {
+    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
+    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
+    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
+    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
+    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
+    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
+    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
+    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
+    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
+    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
+    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0};
+
+// exp(x) for x <= 0 to ~1 fp64 ulp, branch-free: x = k ln2/64 + r (Cody-Waite, |r| <=
+// ln2/128), exp(r) by a degree-7 polynomial, 2^(k/64) from a 64-entry smem table.
+// Returns 0 below -110: such terms change neither an fp64 normaliser >= 1 nor any fp32
+// probability (e^-110 < FLT_TRUE_MIN / 2), so the result equals the reference's.
+__device__ __forceinline__ double exp_neg(double x_in, const double* tab) {
+  const bool live = x_in >= -110.0;  // false for -inf
+  const double x = live ? x_in : -110.0;
+  const double kd = rint(x * 0x1.71547652b82fep+6);  // 64 / ln2
+  const int k = static_cast<int>(kd);
+  double r = fma(-kd, 0x1.62e42fefa0000p-7, x);       // ln2/64 high (36 bits)
+  r = fma(-kd, 0x1.cf79abc9e3b3ap-46, r);              // ln2/64 low
+  double p = 0x1.a01a01a01a01ap-13;
+  p = fma(p, r, 0x1.6c16c16c16c17p-10);
+  p = fma(p, r, 0x1.1111111111111p-7);
+  p = fma(p, r, 0x1.5555555555555p-5);
+  p = fma(p, r, 0x1.5555555555555p-3);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double y = p * tab[k & 63];
+  const double r2 = __hiloint2double(__double2hiint(y) + ((k >> 6) << 20), __double2loint(y));
+  return live ? r2 : 0.0;
+}
+
+__device__ __forceinline__ void load_exp_table(double* tab) {
+  for (int i = threadIdx.x + threadIdx.y * blockDim.x; i < 64; i += blockDim.x * blockDim.y)
+    tab[i] = c_exp2_64[i];
+}
+
 __device__ __forceinline__ void load_chunk(const ScoreArgs& a, const __nv_bfloat16* k, int h, int hk,
                                            int r0, int j0, int c0, float4 (&qr)[2], float4 (&kr)[2]) {
   // 256 threads x 8 elements = 128 rows x 16 c for Q, same for K (lane walks the row
@@ -111,6 +159,8 @@ __device__ __forceinline__ void store_chunk(float* Qs, float* Ks, const float4 (
 __global__ void __launch_bounds__(kThr, 2) logits_kernel(const __grid_constant__ ScoreArgs a) {
   __shared__ __align__(16) float Qs[2][kKC * kTM];
   __shared__ __align__(16) float Ks[2][kKC * kTN];
+  __shared__ double tab[64];
+  load_exp_table(tab);
   const int tile = blockIdx.x, h = blockIdx.y, blk = blockIdx.z;
   const int hk = h / (a.hq / a.hkv);
   const int j0 = tile * kTN;
@@ -118,11 +168,13 @@ __global__ void __launch_bounds__(kThr, 2) logits_kernel(const __grid_constant__
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   const double sc = static_cast<double>(a.scale);
   for (int r0 = 0; r0 < a.n_t; r0 += kTM) {
-    float acc[8][8];
+    // accumulators as fp32 pairs over adjacent keys: one packed FFMA2 (fma.rn.f32x2,
+    // two independent IEEE fp32 FMAs) per pair -- sm_100's full fp32 rate.
+    float2 acc2[8][4];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+      for (int j = 0; j < 4; ++j) acc2[i][j] = make_float2(0.f, 0.f);
     float4 qr[2], kr[2];
     load_chunk(a, k, h, hk, r0, j0, 0, qr, kr);
     store_chunk(Qs[0], Ks[0], qr, kr);
@@ -138,11 +190,14 @@ __global__ void __launch_bounds__(kThr, 2) logits_kernel(const __grid_constant__
         const float4 ka = *reinterpret_cast<const float4*>(&Ks[cur][c * kTN + tx * 4]);
         const float4 kb = *reinterpret_cast<const float4*>(&Ks[cur][c * kTN + 64 + tx * 4]);
         const float qv[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
-        const float kv[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
+        const float2 k2[4] = {make_float2(ka.x, ka.y), make_float2(ka.z, ka.w),
+                              make_float2(kb.x, kb.y), make_float2(kb.z, kb.w)};
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < 8; ++i) {
+          const float2 q2 = make_float2(qv[i], qv[i]);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[i][j] = __fmaf_rn(qv[i], kv[j], acc[i][j]);
+          for (int j = 0; j < 4; ++j) acc2[i][j] = __ffma2_rn(q2, k2[j], acc2[i][j]);
+        }
       }
       if (ch + 1 < kChunks) {
         store_chunk(Qs[cur ^ 1], Ks[cur ^ 1], qr, kr);
@@ -150,6 +205,21 @@ __global__ void __launch_bounds__(kThr, 2) logits_kernel(const __grid_constant__
       }
     }
     // ---- epilogue: L and per-(row, tile) softmax partials
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[i][2 * j] = acc2[i][j].x;
+        acc[i][2 * j + 1] = acc2[i][j].y;
+      }
+    bool kval[8];
+    {
+      const uint8_t* pb = a.pad[blk];
+      const int nv = a.n_valid[blk];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) kval[j] = !is_pad(pb, nv, j0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4)));
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int row = r0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
@@ -162,22 +232,18 @@ __global__ void __launch_bounds__(kThr, 2) logits_kernel(const __grid_constant__
       if (a.softmax) {
         float mxf = -INFINITY;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int key = j0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
-          if (!is_pad(a.pad[blk], a.n_valid[blk], key)) mxf = fmaxf(mxf, acc[i][j]);
-        }
+        for (int j = 0; j < 8; ++j) mxf = kval[j] ? fmaxf(mxf, acc[i][j]) : mxf;
 #pragma unroll
         for (int o = 1; o < 16; o <<= 1) mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
-        double s = 0.0;
+        const bool any = mxf != -INFINITY;
         const double mt = static_cast<double>(mxf) * sc;
-        if (mxf != -INFINITY) {
+        double e[8];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int key = j0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
-            if (!is_pad(a.pad[blk], a.n_valid[blk], key))
-              s += exp(__dsub_rn(__dmul_rn(static_cast<double>(acc[i][j]), sc), mt));
-          }
+        for (int j = 0; j < 8; ++j) {
+          const double x = __dsub_rn(__dmul_rn(static_cast<double>(acc[i][j]), sc), any ? mt : 0.0);
+          e[j] = (kval[j] && any) ? exp_neg(x, tab) : 0.0;
         }
+        double s = ((e[0] + e[1]) + (e[2] + e[3])) + ((e[4] + e[5]) + (e[6] + e[7]));
 #pragma unroll
         for (int o = 1; o < 16; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (tx == 0 && rok)
@@ -224,49 +290,74 @@ __device__ __forceinline__ float prob_f32(double e, double sum, double rinv) {
   return __double2float_rn(y);
 }
 
-// block (32, 8): thread (x, y) owns key j = blockIdx.x*32+x of block blockIdx.y for heads
-// y, y+8, ...; rows i ascending per head, heads ascending for the total.
+// block (32, 8): thread (x, y) owns keys j, j+1 (j = blockIdx.x*64 + 2x) of block blockIdx.y
+// for heads y, y+8, ...; rows i ascending per head (8-row batches keep 8 loads and 16
+// independent exps in flight), heads ascending for the total.
 __global__ void __launch_bounds__(256) colsum_kernel(const __grid_constant__ ScoreArgs a) {
-  __shared__ float part[32][33];
+  __shared__ float part[32][65];
+  __shared__ double tab[64];
+  load_exp_table(tab);
+  __syncthreads();
   const int x = threadIdx.x, y = threadIdx.y, blk = blockIdx.y;
-  const int j = blockIdx.x * 32 + x;
-  const bool inb = j < a.l_b;
+  const int j = blockIdx.x * 64 + 2 * x;
+  const bool inb = j < a.l_b;  // j+1 < ldL always (ldL is a multiple of 128)
   const double sc = static_cast<double>(a.scale);
   for (int h = y; h < a.hq; h += 8) {
-    float acc = 0.f;
+    float acc0 = 0.f, acc1 = 0.f;
     if (inb) {
       const long long hb = (static_cast<long long>(blk) * a.hq + h) * a.n_t;
       const float* L = a.L + hb * a.ldL + j;
       const double* st = a.stats + hb * 3;
       if (a.softmax) {
         int i = 0;
-        for (; i + 4 <= a.n_t; i += 4) {
-          float p[4];
+        for (; i + 8 <= a.n_t; i += 8) {
+          float2 l[8];
+          double m[8], sm[8], ri[8];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const double e = exp(__dsub_rn(__dmul_rn(static_cast<double>(L[(i + u) * a.ldL]), sc),
-                                           st[(i + u) * 3]));
-            p[u] = prob_f32(e, st[(i + u) * 3 + 1], st[(i + u) * 3 + 2]);
+          for (int u = 0; u < 8; ++u) {
+            l[u] = *reinterpret_cast<const float2*>(L + (i + u) * a.ldL);
+            m[u] = st[(i + u) * 3];
+            sm[u] = st[(i + u) * 3 + 1];
+            ri[u] = st[(i + u) * 3 + 2];
+          }
+          float p0[8], p1[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            p0[u] = prob_f32(exp_neg(__dsub_rn(__dmul_rn(static_cast<double>(l[u].x), sc), m[u]), tab), sm[u], ri[u]);
+            p1[u] = prob_f32(exp_neg(__dsub_rn(__dmul_rn(static_cast<double>(l[u].y), sc), m[u]), tab), sm[u], ri[u]);
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) acc = __fadd_rn(acc, p[u]);
+          for (int u = 0; u < 8; ++u) {
+            acc0 = __fadd_rn(acc0, p0[u]);
+            acc1 = __fadd_rn(acc1, p1[u]);
+          }
         }
         for (; i < a.n_t; ++i) {
-          const double e = exp(__dsub_rn(__dmul_rn(static_cast<double>(L[i * a.ldL]), sc), st[i * 3]));
-          acc = __fadd_rn(acc, prob_f32(e, st[i * 3 + 1], st[i * 3 + 2]));
+          const float2 l = *reinterpret_cast<const float2*>(L + i * a.ldL);
+          acc0 = __fadd_rn(acc0, prob_f32(exp_neg(__dsub_rn(__dmul_rn(static_cast<double>(l.x), sc), st[i * 3]), tab),
+                                          st[i * 3 + 1], st[i * 3 + 2]));
+          acc1 = __fadd_rn(acc1, prob_f32(exp_neg(__dsub_rn(__dmul_rn(static_cast<double>(l.y), sc), st[i * 3]), tab),
+                                          st[i * 3 + 1], st[i * 3 + 2]));
         }
       } else {
-        for (int i = 0; i < a.n_t; ++i) acc = __fadd_rn(acc, __fmul_rn(L[i * a.ldL], a.scale));
+        for (int i = 0; i < a.n_t; ++i) {
+          const float2 l = *reinterpret_cast<const float2*>(L + i * a.ldL);
+          acc0 = __fadd_rn(acc0, __fmul_rn(l.x, a.scale));
+          acc1 = __fadd_rn(acc1, __fmul_rn(l.y, a.scale));
+        }
       }
     }
-    part[h][x] = acc;
+    part[h][2 * x] = acc0;
+    part[h][2 * x + 1] = acc1;
   }
   __syncthreads();
-  if (y == 0 && inb) {
+  const int t = y * 32 + x;
+  const int jj = blockIdx.x * 64 + t;
+  if (t < 64 && jj < a.l_b) {
     float total = 0.f;
-    for (int h = 0; h < a.hq; ++h) total = __fadd_rn(total, part[h][x]);
+    for (int h = 0; h < a.hq; ++h) total = __fadd_rn(total, part[h][t]);
     // pad keys -> -inf (approx.cpp:64-66); a block without visible keys is all pads
-    a.scores[blk][j] = is_pad(a.pad[blk], a.n_valid[blk], j) ? -INFINITY : total;
+    a.scores[blk][jj] = is_pad(a.pad[blk], a.n_valid[blk], jj) ? -INFINITY : total;
   }
 }
 
@@ -320,7 +411,7 @@ cudaError_t launch_score_exact2(int nblk, const void* q, long long ldq, int n_t,
     const long long rows = static_cast<long long>(nblk) * hq * n_t;
     stats_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, stream>>>(a);
   }
-  colsum_kernel<<<dim3((l_b + 31) / 32, nblk), dim3(32, 8), 0, stream>>>(a);
+  colsum_kernel<<<dim3((l_b + 63) / 64, nblk), dim3(32, 8), 0, stream>>>(a);
   return cudaGetLastError();
 }
 

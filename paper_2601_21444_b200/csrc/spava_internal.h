@@ -26,7 +26,8 @@ struct AttnProb {
   int nq;                    // query rows
   int nseg;
   AttnSeg seg[kMaxSegs];
-  int units;                 // ceil(nq / 256)
+  int units;                 // ceil(nq / 256), or 1 with head pairing
+  int head_pair;             // nq <= 128: the CTA's two Q tiles are q-heads h, h+1
   int splits;                // split-KV factor; >1 writes per-split partials
   int work_begin;            // first work index of this problem
   int out_f32;               // 0: bf16 output, 1: f32 output
@@ -71,6 +72,7 @@ struct ProbView {
   long long split_stride_out;
   long long split_stride_lse;
 };
+void attn_prof_read(unsigned long long* out16);  // dev: cycle counters of variant 5
 cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, int dh,
                              cudaStream_t stream, std::string* err);
 

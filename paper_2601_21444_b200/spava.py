@@ -37,6 +37,7 @@ EXPORTED_SYMBOLS = [
     "spava_fabric_destroy", "spava_host_create", "spava_host_destroy", "spava_host_plan",
     "spava_host_rows", "spava_host_layer", "spava_sim_layer", "spava_host_status",
     "spava_host_set_timing", "spava_host_timing", "spava_kernel_launches",
+    "spava_debug_attn_prof",
 ]
 
 
