@@ -402,7 +402,7 @@ def run_spava_arm(args):
     achieved = attn_flops_step / (tim["attention_ms"] / args.steps / 1e3) / 1e12
     peak = pk["bf16_sustained"]
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "attn_ncu_summary.json")
+    tp = os.path.join(ROOT, "profiles", "r01_ncu_step.json")
     if os.path.exists(tp):
         try:
             with open(tp) as f:

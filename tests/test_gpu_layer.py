@@ -100,3 +100,37 @@ def test_layer_c0_shape(cuda, hosts, zigzag, splits):
     want = O.spava_layer(Q, K, V, n_v, n_t, hosts, l_a, l_p, hq, hkv, 128, zigzag=zigzag)
     res = run_layer(cuda, Q, K, V, n_v, n_t, hosts, l_a, l_p, hq, hkv, zigzag, True, splits)
     check_layer(res, want, n_t, hosts, l_a, zigzag)
+
+
+def test_nccl_fabric_world1_matches_local(cuda):
+    """The NCCL fabric (in-place allgathers on the comm stream, event-ordered) at world
+    size 1 gives the same layer as the local fabric (H=1)."""
+    import torch
+
+    from paper_2601_21444_b200 import spava
+
+    n_v, n_t, l_a, l_p, hq, hkv = 1300, 32, 20, 96, 4, 2
+    cfg = spava.LayerConfig.make(n_v, n_t, 1, l_a, l_p, hq, hkv)
+    loc = spava.Fabric(cfg, 0)
+    nc = spava.Fabric(cfg, 0, unique_id=spava.nccl_unique_id(), world=1, rank=0)
+    h_loc, h_nc = loc.host(0), nc.host(0)
+    rows = h_loc.rows
+    g = torch.Generator(device=cuda).manual_seed(5)
+    q = torch.randn(rows, hq * 128, device=cuda, generator=g).to(torch.bfloat16)
+    k = torch.randn(rows, hkv * 128, device=cuda, generator=g).to(torch.bfloat16)
+    v = torch.randn(rows, hkv * 128, device=cuda, generator=g).to(torch.bfloat16)
+    outs, sels = [], []
+    for host in (h_loc, h_nc):
+        o = torch.zeros(rows, hq * 128, dtype=torch.bfloat16, device=cuda)
+        s = torch.zeros(2, l_p, dtype=torch.int32, device=cuda)
+        host.layer(q, k, v, o, s)
+        torch.cuda.synchronize()
+        assert host.status() == 0
+        outs.append(o)
+        sels.append(s)
+    assert torch.equal(sels[0], sels[1])
+    assert torch.equal(outs[0], outs[1])
+    for x in (h_loc, h_nc):
+        x.close()
+    loc.close()
+    nc.close()
