@@ -39,12 +39,17 @@ def sources():
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
 
 
+def host_sources():
+    """Host-only C++ (the seqpar:: mirror) is compiled by g++."""
+    return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cpp")))
+
+
 def needs_build():
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + glob.glob(
-        os.path.join(HERE, "csrc", "*.h")) + [os.path.join(ROOT, "include", "spava_b200.h")]
+    deps = sources() + host_sources() + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + glob.glob(
+        os.path.join(HERE, "csrc", "*.h")) + glob.glob(os.path.join(ROOT, "include", "*"))
     return any(os.path.getmtime(d) > t for d in deps)
 
 
@@ -52,9 +57,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     inc, libdir = nccl_dirs()
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
+    objs = []
+    for src in host_sources():
+        obj = os.path.join(HERE, "csrc", os.path.basename(src)[:-4] + ".o")
+        r = subprocess.run(["g++", "-std=c++20", "-O2", "-fPIC", "-c", src, "-o", obj,
+                            "-I", "/usr/local/cuda/include", "-I", os.path.join(ROOT, "include")],
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("g++ failed:\n" + r.stdout + r.stderr)
+        objs.append(obj)
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++20", "--expt-relaxed-constexpr",
            "-Xcompiler", "-fPIC,-O2", "-shared", "-I", inc, "-I", os.path.join(ROOT, "include"),
-           *sources(), "-o", LIB + ".tmp", "-L", libdir, "-l:libnccl.so.2",
+           *sources(), *objs, "-o", LIB + ".tmp", "-L", libdir, "-l:libnccl.so.2",
            "-Xlinker", f"-rpath,{libdir}"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
