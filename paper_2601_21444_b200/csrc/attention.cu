@@ -134,7 +134,7 @@ __device__ __forceinline__ void cursor_next(const AttnProb& p, int imax, Cursor&
   }
 }
 
-template <int kEmu, int KS, bool kProf = false>
+template <int kEmu, int KS, bool kProf = false, bool kPipe = false>
 __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ AttnParams P) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -368,6 +368,32 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       uint32_t sr[4][32];
       uint32_t pk[4][16];
       // exp + bf16 pack of one 32-key chunk against reference max m (-m in negm)
+      // kPipe: exps are written back in place (sr[c] := p bits) and summed/packed by
+      // chunk_pack one chunk later, so the FADD2/F2FP never sit right behind the MUFU
+      // pair that feeds them (in-order issue stalled on MUFU latency there).
+      auto chunk_exp_ip = [&](int c, float2 negm, bool emu) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 x2 = __ffma2_rn(
+              make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1])), sl2v, negm);
+          float2 p2;
+          if (kEmu > 0 && emu && (j % (16 / kEmu)) == (16 / kEmu) - 1)
+            p2 = exp2_poly2(x2);
+          else
+            p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));  // -inf -> 0
+          sr[c][2 * j] = __float_as_uint(p2.x);
+          sr[c][2 * j + 1] = __float_as_uint(p2.y);
+        }
+      };
+      auto chunk_pack = [&](int c, float2 (&sacc)[4]) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 p2 = make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1]));
+          sacc[j & 3] = __fadd2_rn(sacc[j & 3], p2);
+          __nv_bfloat162 b = __floats2bfloat162_rn(p2.x, p2.y);
+          pk[c][j] = *reinterpret_cast<uint32_t*>(&b);
+        }
+      };
       auto chunk_exp = [&](int c, float2 negm, bool emu, float2 (&sacc)[4]) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -403,16 +429,29 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
       bool done = false;
       load_s();
+      if (kProf) pr[9] += PROF_NOW() - tw1;
       if (mode == kFull && m_ref != -INFINITY) {
         // speculative pass against the running max m_ref: the tile max is folded in on the
         // side instead of sitting on the critical path; P is kept in registers and only
         // committed to TMEM if the tile max stayed within m_ref + 8 (P <= 2^8), the common
         // case after the first tiles; otherwise S is re-read and the exact path runs.
         const float2 negm = make_float2(-m_ref, -m_ref);
+        if constexpr (kPipe) {
+          chunk_max(0, mxp);
+          chunk_exp_ip(0, negm, true);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          chunk_max(c, mxp);
-          chunk_exp(c, negm, true, sacc);
+          for (int c = 1; c < 4; ++c) {
+            chunk_max(c, mxp);
+            chunk_exp_ip(c, negm, true);
+            chunk_pack(c - 1, sacc);
+          }
+          chunk_pack(3, sacc);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            chunk_max(c, mxp);
+            chunk_exp(c, negm, true, sacc);
+          }
         }
         const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
                                fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
@@ -446,8 +485,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         }
         const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
         const float2 negm = make_float2(-m_use, -m_use);
+        if constexpr (kPipe) {
+          chunk_exp_ip(0, negm, mode == kFull);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) chunk_exp(c, negm, mode == kFull, sacc);
+          for (int c = 1; c < 4; ++c) {
+            chunk_exp_ip(c, negm, mode == kFull);
+            chunk_pack(c - 1, sacc);
+          }
+          chunk_pack(3, sacc);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) chunk_exp(c, negm, mode == kFull, sacc);
+        }
       }
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_st16(tS + 16 * c, pk[c]);
@@ -539,6 +588,360 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 #undef TILE_HEAD
 }
 
+// ============================================================================ variant family 1
+// One Q tile (128 rows of one q-head) per CTA with the score accumulator double-buffered
+// in TMEM: S_0 | S_1 | O (384 of 512 columns).  The MMA warp issues QK(j+2) into the buffer
+// of tile j right behind PV(j), so S(j+1) is already resident when the softmax finishes
+// tile j: the per-tile critical loop is the softmax body alone (not body + PV + QK as in
+// the ping-pong family, whose QK(j+1) must wait for PV(j) because P aliases S).
+//   warps 0-3  softmax (thread = TMEM lane = query row), epilogue
+//   warp 4     TMA producer (Q once, then K/V rings)
+//   warp 5     TMEM allocator + single-thread tcgen05.mma issuer
+constexpr int kThreads1 = 192;
+constexpr int kKS1 = 3, kVS1 = 2;
+struct Smem1 {
+  static constexpr uint32_t q = 0;
+  static constexpr uint32_t k = q + kTileBytes;
+  static constexpr uint32_t v = k + kKS1 * kTileBytes;
+  static constexpr uint32_t bar = v + kVS1 * kTileBytes;
+  static constexpr uint32_t total = bar + 256;
+  static constexpr uint32_t bytes = total + 1024;
+};
+
+template <int kEmu, bool kPipe>
+__global__ void __launch_bounds__(kThreads1, 1) attn_fwd1_kernel(const __grid_constant__ AttnParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem1::bar);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;           // [kKS1]
+  uint64_t* k_empty = k_full + kKS1;     // [kKS1]
+  uint64_t* v_full = k_empty + kKS1;     // [kVS1]
+  uint64_t* v_empty = v_full + kVS1;     // [kVS1]
+  uint64_t* s_full = v_empty + kVS1;     // [2] S buffer b holds a fresh QK
+  uint64_t* p_full = s_full + 2;         // [2] P written into buffer b (O corrected)
+  uint64_t* o_full = p_full + 2;         // PV complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+
+  int pi = 0;
+  while (pi + 1 < P.nprob && static_cast<int>(blockIdx.x) >= P.prob[pi + 1].work_begin) ++pi;
+  const AttnProb& prob = P.prob[pi];
+  int local = static_cast<int>(blockIdx.x) - prob.work_begin;
+  const int split = local % prob.splits;
+  local /= prob.splits;
+  const int head = local % P.hq;
+  local /= P.hq;
+  const int unit = prob.units - 1 - local;  // heaviest (latest causal rows) first
+  const int i0 = unit * kBlockM;
+  const int nq = prob.nq;
+  const int imax = min(i0 + kBlockM, nq);
+  const int hk = head / (P.hq / P.hkv);
+
+  int T = 0;
+  for (int s = 0; s < prob.nseg; ++s) T += seg_tiles(prob.seg[s], imax);
+  const int t_begin = static_cast<int>(static_cast<long long>(T) * split / prob.splits);
+  const int t_end = static_cast<int>(static_cast<long long>(T) * (split + 1) / prob.splits);
+  const int ntiles = t_end - t_begin;
+  const CUtensorMap* tm = P.tmap[pi];
+
+  if (warp == 4 && elect_one()) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < kKS1; ++s) {
+      mbar_init(k_full + s, 1);
+      mbar_init(k_empty + s, 1);
+    }
+    for (int s = 0; s < kVS1; ++s) {
+      mbar_init(v_full + s, 1);
+      mbar_init(v_empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(s_full + b, 1);
+      mbar_init(p_full + b, 128);
+    }
+    mbar_init(o_full, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm[0]);
+    for (int s = 0; s < prob.nseg; ++s) {
+      tma_prefetch_desc(&tm[1 + 2 * s]);
+      tma_prefetch_desc(&tm[2 + 2 * s]);
+    }
+  }
+  if (warp == 5) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    // ======================================================== TMA producer
+    if (elect_one()) {
+      mbar_expect_tx(q_full, kTileBytes);
+      for (int c = 0; c < 2; ++c)
+        tma_load_2d(smem + Smem1::q + c * kBoxBytes, &tm[0], q_full, head * kHeadDim + c * 64, i0);
+      Cursor cur = cursor_at(prob, imax, t_begin);
+      for (int it = 0; it < ntiles; ++it) {
+        const CUtensorMap* km = &tm[1 + 2 * cur.seg];
+        const CUtensorMap* vm = &tm[2 + 2 * cur.seg];
+        const int ks = it % kKS1, vs = it % kVS1;
+        if (it >= kKS1) mbar_wait(k_empty + ks, ((it / kKS1) - 1) & 1);
+        mbar_expect_tx(k_full + ks, kTileBytes);
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d(smem + Smem1::k + ks * kTileBytes + c * kBoxBytes, km, k_full + ks,
+                      hk * kHeadDim + c * 64, cur.kt * kBlockN);
+        if (it >= kVS1) mbar_wait(v_empty + vs, ((it / kVS1) - 1) & 1);
+        mbar_expect_tx(v_full + vs, kTileBytes);
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d(smem + Smem1::v + vs * kTileBytes + c * kBoxBytes, vm, v_full + vs,
+                      hk * kHeadDim + c * 64, cur.kt * kBlockN);
+        cursor_next(prob, imax, cur);
+      }
+    }
+  } else if (warp == 5) {
+    // ======================================================== MMA issuer
+    if (elect_one()) {
+      const uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
+      const uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
+      const uint32_t sq = smem_u32(smem + Smem1::q);
+      const uint32_t sk = smem_u32(smem + Smem1::k);
+      const uint32_t sv = smem_u32(smem + Smem1::v);
+      auto issue_qk = [&](int b, int it) {
+        const int ks = it % kKS1;
+        mbar_wait(k_full + ks, (it / kKS1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + b * 128;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t koff = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
+          mma_ss(d, sdesc_sw128(sq + koff, 16, 1024), sdesc_sw128(sk + ks * kTileBytes + koff, 16, 1024),
+                 idesc_qk, kk > 0 ? 1u : 0u);
+        }
+        tc_commit(s_full + b);
+        tc_commit(k_empty + ks);
+      };
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      if (ntiles > 0) issue_qk(0, 0);
+      if (ntiles > 1) issue_qk(1, 1);
+      for (int it = 0; it < ntiles; ++it) {
+        const int b = it & 1, vs = it % kVS1;
+        mbar_wait(v_full + vs, (it / kVS1) & 1);
+        mbar_wait(p_full + b, (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + 256;
+        const uint32_t a = tmem + b * 128;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(d, a + kk * 8, sdesc_sw128(sv + vs * kTileBytes + kk * 2048, kBoxBytes, 1024), idesc_pv,
+                 (it > 0 || kk > 0) ? 1u : 0u);
+        tc_commit(o_full);
+        tc_commit(v_empty + vs);
+        // QK(it+2) reuses buffer b: issued behind PV(it), the in-order tensor pipe keeps
+        // P(it) intact until PV(it) has read it.
+        if (it + 2 < ntiles) issue_qk(b, it + 2);
+      }
+    }
+  } else {
+    // ======================================================== softmax warpgroup
+    const int quad = warp;
+    const int row = i0 + quad * 32 + lane;
+    const uint32_t t_lane = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t tO = tmem + t_lane + 256;
+    const float sl2 = P.scale_log2;
+    const float2 sl2v = make_float2(sl2, sl2);
+    float m_ref = -INFINITY;
+    float l = 0.f;
+    Cursor cur = cursor_at(prob, imax, t_begin);
+    uint32_t sr[4][32];
+    uint32_t pk[4][16];
+    for (int it = 0; it < ntiles; ++it, cursor_next(prob, imax, cur)) {
+      const int b = it & 1;
+      const uint32_t tS = tmem + t_lane + b * 128;
+      const AttnSeg sg = prob.seg[cur.seg];
+      const int mode = tile_mode(sg, cur.kt, i0, nq);
+      mbar_wait(s_full + b, (it >> 1) & 1);
+      tc_fence_after();
+      auto load_s = [&]() {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(tS + 32 * c, sr[c]);
+        tmem_wait_ld();
+      };
+      auto chunk_max = [&](int c, float (&mxp)[8]) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const int t = (j / 2) & 7;
+          mxp[t] = fmaxf(mxp[t], fmaxf(__uint_as_float(sr[c][j]), __uint_as_float(sr[c][j + 1])));
+        }
+      };
+      auto chunk_exp = [&](int c, float2 negm, bool emu) {  // in place: sr[c] := p
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 x2 = __ffma2_rn(
+              make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1])), sl2v, negm);
+          float2 p2;
+          if (kEmu > 0 && emu && (j % (16 / kEmu)) == (16 / kEmu) - 1)
+            p2 = exp2_poly2(x2);
+          else
+            p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));  // -inf -> 0
+          sr[c][2 * j] = __float_as_uint(p2.x);
+          sr[c][2 * j + 1] = __float_as_uint(p2.y);
+        }
+      };
+      auto chunk_pack = [&](int c, float2 (&sacc)[4]) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 p2 = make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1]));
+          sacc[j & 3] = __fadd2_rn(sacc[j & 3], p2);
+          __nv_bfloat162 bb = __floats2bfloat162_rn(p2.x, p2.y);
+          pk[c][j] = *reinterpret_cast<uint32_t*>(&bb);
+        }
+      };
+      auto exp_pack_all = [&](float2 negm, bool emu, float2 (&sacc)[4]) {
+        if constexpr (kPipe) {
+          chunk_exp(0, negm, emu);
+#pragma unroll
+          for (int c = 1; c < 4; ++c) {
+            chunk_exp(c, negm, emu);
+            chunk_pack(c - 1, sacc);
+          }
+          chunk_pack(3, sacc);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            chunk_exp(c, negm, emu);
+            chunk_pack(c, sacc);
+          }
+        }
+      };
+      float alpha = 1.f;
+      bool rescale = false;
+      float mxp[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
+      float2 sacc[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
+      bool done = false;
+      load_s();
+      if (mode == kFull && m_ref != -INFINITY) {
+        // speculative pass against the running max (see the ping-pong kernel)
+        const float2 negm = make_float2(-m_ref, -m_ref);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) chunk_max(c, mxp);
+        exp_pack_all(negm, true, sacc);
+        const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                               fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+        done = !(mx * sl2 > m_ref + 8.f);
+        if (!done) {
+#pragma unroll
+          for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
+          load_s();
+        }
+      } else if (mode == kPart) {
+        const int k0 = cur.kt * kBlockN;
+        int lim = sg.len - k0;
+        if (sg.causal) lim = min(lim, row - k0 + 1);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c * 32 + j >= lim) sr[c][j] = __float_as_uint(-INFINITY);
+      }
+      if (!done) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) chunk_max(c, mxp);
+        const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                               fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+        const float m_new = fmaxf(m_ref, mx * sl2);
+        if (m_new > m_ref + 8.f) {
+          alpha = exp2f(m_ref - m_new);
+          m_ref = m_new;
+          rescale = true;
+        }
+        const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+        exp_pack_all(make_float2(-m_use, -m_use), mode == kFull, sacc);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_st16(tS + 16 * c, pk[c]);
+      const float2 sum2 = __fadd2_rn(__fadd2_rn(sacc[0], sacc[1]), __fadd2_rn(sacc[2], sacc[3]));
+      l = l * alpha + (sum2.x + sum2.y);
+      if (rescale && it > 0) {
+        mbar_wait(o_full, (it - 1) & 1);  // PV(it-1) has landed in O
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          tmem_ld32(tO + 32 * c, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
+          tmem_st32(tO + 32 * c, o);
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_full + b);
+    }
+    // ---- epilogue: O / l, lse
+    if (ntiles > 0) {
+      mbar_wait(o_full, (ntiles - 1) & 1);
+      tc_fence_after();
+    }
+    const bool valid_row = row < nq;
+    const float inv = (l > 0.f) ? 1.f / l : 0.f;
+    const long long obase = static_cast<long long>(split) * prob.split_stride_out +
+                            static_cast<long long>(row) * prob.ldo + head * kHeadDim;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t o[32];
+      if (ntiles > 0) {
+        tmem_ld32(tO + 32 * c, o);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o[j] = 0u;
+      }
+      if (valid_row) {
+        if (prob.out_f32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(prob.out) + obase + 32 * c);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(__uint_as_float(o[4 * j]) * inv, __uint_as_float(o[4 * j + 1]) * inv,
+                                 __uint_as_float(o[4 * j + 2]) * inv, __uint_as_float(o[4 * j + 3]) * inv);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(prob.out) + obase + 32 * c);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 bb = __floats2bfloat162_rn(__uint_as_float(o[8 * j + 2 * e]) * inv,
+                                                        __uint_as_float(o[8 * j + 2 * e + 1]) * inv);
+              w[e] = *reinterpret_cast<uint32_t*>(&bb);
+            }
+            dst[j] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+    }
+    if (valid_row && prob.lse) {
+      const float lse = (l > 0.f) ? (m_ref + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+      prob.lse[static_cast<long long>(split) * prob.split_stride_lse +
+               static_cast<long long>(row) * prob.ld_lse + head] = lse;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_dealloc(tmem, kTmemCols);
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -595,6 +998,27 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
   P.hq = hq;
   P.hkv = hkv;
   P.scale_log2 = (1.0f / sqrtf(static_cast<float>(dh))) * 1.4426950408889634f;
+  // kernel variants (SPAVA_ATTN_VARIANT): family 0 = ping-pong (2 Q tiles per CTA, 320
+  // threads), family 1 = one Q tile per CTA with double-buffered S (192 threads).
+  using KFn = void (*)(AttnParams);
+  struct Var { KFn fn; uint32_t smem; int threads; int family; };
+  static const Var variants[] = {
+      {attn_fwd_kernel<0, 2, false, true>, Smem<2>::bytes, kThreads, 0},  // 0 production
+      {attn_fwd1_kernel<0, true>, Smem1::bytes, kThreads1, 1},            // 1 single tile, S x2
+      {attn_fwd_kernel<0, 2, true, true>, Smem<2>::bytes, kThreads, 0},   // 2 0 + cycle counters
+      {attn_fwd1_kernel<4, true>, Smem1::bytes, kThreads1, 1},            // 3 1 + 25% FMA exp2
+      {attn_fwd_kernel<4, 2, false, true>, Smem<2>::bytes, kThreads, 0},  // 4 0 + 25% FMA exp2
+      {attn_fwd1_kernel<2, true>, Smem1::bytes, kThreads1, 1},            // 5 1 + 12.5% FMA exp2
+      {attn_fwd_kernel<0, 2>, Smem<2>::bytes, kThreads, 0}};              // 6 0 without the
+                                                                          //   one-chunk-behind pack
+  constexpr int kNumVar = sizeof(variants) / sizeof(variants[0]);
+  static int vsel = [] {
+    const char* e = getenv("SPAVA_ATTN_VARIANT");
+    const int v = e ? atoi(e) : 0;
+    return (v >= 0 && v < kNumVar) ? v : 0;
+  }();
+  const Var& var = variants[vsel];
+  const int rows_per_cta = var.family == 1 ? kBlockM : kTilesPerCta * kBlockM;
   int work = 0;
   int np = 0;
   for (int i = 0; i < nprob; ++i) {
@@ -607,8 +1031,8 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
     AttnProb& p = P.prob[np];
     p.nq = v.nq;
     p.nseg = v.nseg;
-    p.head_pair = (v.nq <= kBlockM && (hq / hkv) % 2 == 0) ? 1 : 0;
-    p.units = p.head_pair ? 1 : (v.nq + kTilesPerCta * kBlockM - 1) / (kTilesPerCta * kBlockM);
+    p.head_pair = (var.family == 0 && v.nq <= kBlockM && (hq / hkv) % 2 == 0) ? 1 : 0;
+    p.units = p.head_pair ? 1 : (v.nq + rows_per_cta - 1) / rows_per_cta;
     p.splits = v.splits;
     p.work_begin = work;
     p.out_f32 = v.out_f32;
@@ -639,31 +1063,16 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
   P.nprob = np;
   P.total_work = work;
   if (work == 0) return cudaSuccess;
-  // kernel variant: <emulated exp2 pairs per 32-key chunk, K ring depth[, cycle counters]>
-  using KFn = void (*)(AttnParams);
-  struct Var { KFn fn; uint32_t smem; };
-  // 0: production (MUFU exp2, speculative stale-max softmax, 2-deep K/V rings)
-  // 1: 25% of exp2 on the FMA pipe (FA4-style; measured slightly slower here)
-  // 2: production + per-phase cycle counters (dev, SPAVA_ATTN_VARIANT=2)
-  static const Var variants[] = {{attn_fwd_kernel<0, 2>, Smem<2>::bytes},
-                                 {attn_fwd_kernel<4, 2>, Smem<2>::bytes},
-                                 {attn_fwd_kernel<0, 2, true>, Smem<2>::bytes}};
-  constexpr int kNumVar = sizeof(variants) / sizeof(variants[0]);
-  static int vsel = [] {
-    const char* e = getenv("SPAVA_ATTN_VARIANT");
-    const int v = e ? atoi(e) : 0;
-    return (v >= 0 && v < kNumVar) ? v : 0;
-  }();
   static bool attr_set[kNumVar] = {};
-  const KFn fn = variants[vsel].fn;
-  const uint32_t smem_bytes = variants[vsel].smem;
+  const KFn fn = var.fn;
+  const uint32_t smem_bytes = var.smem;
   if (!attr_set[vsel]) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem_bytes));
     if (e != cudaSuccess) return e;
     attr_set[vsel] = true;
   }
-  fn<<<work, kThreads, smem_bytes, stream>>>(P);
+  fn<<<work, var.threads, smem_bytes, stream>>>(P);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess && err) {
     cudaFuncAttributes fa{};
