@@ -622,7 +622,8 @@ __global__ void __launch_bounds__(kThreads1, 1) attn_fwd1_kernel(const __grid_co
   uint64_t* s_full = v_empty + kVS1;     // [2] S buffer b holds a fresh QK
   uint64_t* p_full = s_full + 2;         // [2] P written into buffer b (O corrected)
   uint64_t* o_full = p_full + 2;         // PV complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
+  uint64_t* o_done = o_full + 1;         // every MMA of the CTA complete (epilogue)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -663,6 +664,7 @@ __global__ void __launch_bounds__(kThreads1, 1) attn_fwd1_kernel(const __grid_co
       mbar_init(p_full + b, 128);
     }
     mbar_init(o_full, 1);
+    mbar_init(o_done, 1);
     fence_barrier_init();
     tma_prefetch_desc(&tm[0]);
     for (int s = 0; s < prob.nseg; ++s) {
@@ -743,6 +745,7 @@ __global__ void __launch_bounds__(kThreads1, 1) attn_fwd1_kernel(const __grid_co
         // P(it) intact until PV(it) has read it.
         if (it + 2 < ntiles) issue_qk(b, it + 2);
       }
+      tc_commit(o_done);
     }
   } else {
     // ======================================================== softmax warpgroup
@@ -888,10 +891,10 @@ __global__ void __launch_bounds__(kThreads1, 1) attn_fwd1_kernel(const __grid_co
       mbar_arrive(p_full + b);
     }
     // ---- epilogue: O / l, lse
-    if (ntiles > 0) {
-      mbar_wait(o_full, (ntiles - 1) & 1);
-      tc_fence_after();
-    }
+    // S double-buffered: PV(n-1) and PV(n) may both be in flight, which a parity wait on
+    // o_full cannot disambiguate -- wait for the MMA warp's final commit instead.
+    mbar_wait(o_done, 0);
+    tc_fence_after();
     const bool valid_row = row < nq;
     const float inv = (l > 0.f) ? 1.f / l : 0.f;
     const long long obase = static_cast<long long>(split) * prob.split_stride_out +
@@ -942,6 +945,441 @@ __global__ void __launch_bounds__(kThreads1, 1) attn_fwd1_kernel(const __grid_co
   if (warp == 5) tmem_dealloc(tmem, kTmemCols);
 }
 
+// ============================================================================ variant family 2
+// Two Q tiles (256 rows, or two q-heads of one GQA group) per CTA as in the ping-pong
+// family, but with 64-key KV tiles so each Q tile's score accumulator fits TMEM twice:
+// S_0[2] | S_1[2] (64 columns each) | O_0 | O_1 = 512 columns.  QK_t(j+2) is issued right
+// behind PV_t(j) into the buffer PV_t(j) just drained, so S_t(j+1) is resident when softmax
+// t finishes tile j: the two softmax warpgroups (one warp of each per SMSP) run back to back
+// and interleave their MUFU streams instead of each waiting one PV+QK per tile.
+constexpr int kBN2 = 64;
+constexpr int kKS2 = 4, kVS2 = 4;
+constexpr uint32_t kKvBox2 = kBN2 * 64 * 2;     // 64 rows x 64 bf16 (SW128 box)
+constexpr uint32_t kKvTile2 = 2 * kKvBox2;      // 64 keys x 128 dh
+struct Smem2 {
+  static constexpr uint32_t q = 0;
+  static constexpr uint32_t k = q + kTilesPerCta * kTileBytes;
+  static constexpr uint32_t v = k + kKS2 * kKvTile2;
+  static constexpr uint32_t bar = v + kVS2 * kKvTile2;
+  static constexpr uint32_t total = bar + 256;
+  static constexpr uint32_t bytes = total + 1024;
+};
+
+__device__ __forceinline__ int seg_tiles2(const AttnSeg& s, int imax) {
+  const int klen = s.causal ? min(s.len, imax) : s.len;
+  return klen > 0 ? (klen + kBN2 - 1) / kBN2 : 0;
+}
+__device__ __forceinline__ int tile_mode2(const AttnSeg& s, int kt, int r0, int nq) {
+  if (r0 >= nq) return kSkip;
+  const int k0 = kt * kBN2;
+  const bool tail = k0 + kBN2 > s.len;
+  if (s.causal) {
+    const int rlast = min(r0 + kBlockM, nq) - 1;
+    if (k0 > rlast) return kSkip;
+    return (k0 + kBN2 - 1 > r0 || tail) ? kPart : kFull;
+  }
+  return tail ? kPart : kFull;
+}
+__device__ __forceinline__ Cursor cursor_at2(const AttnProb& p, int imax, int t) {
+  for (int s = 0; s < p.nseg; ++s) {
+    const int n = seg_tiles2(p.seg[s], imax);
+    if (t < n) return {s, t};
+    t -= n;
+  }
+  return {p.nseg, 0};
+}
+__device__ __forceinline__ void cursor_next2(const AttnProb& p, int imax, Cursor& c) {
+  ++c.kt;
+  while (c.seg < p.nseg && c.kt >= seg_tiles2(p.seg[c.seg], imax)) {
+    ++c.seg;
+    c.kt = 0;
+  }
+}
+
+template <int kEmu>
+__global__ void __launch_bounds__(kThreads, 1) attn_fwd2_kernel(const __grid_constant__ AttnParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem2::bar);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;          // [kKS2]
+  uint64_t* k_empty = k_full + kKS2;    // [kKS2]
+  uint64_t* v_full = k_empty + kKS2;    // [kVS2]
+  uint64_t* v_empty = v_full + kVS2;    // [kVS2]
+  uint64_t* s_full = v_empty + kVS2;    // [2 tiles][2 buffers]
+  uint64_t* p_full = s_full + 4;        // [2][2]
+  uint64_t* o_full = p_full + 4;        // [2] PV_t complete
+  uint64_t* o_done = o_full + 2;        // every MMA of the CTA complete (epilogue)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+
+  int pi = 0;
+  while (pi + 1 < P.nprob && static_cast<int>(blockIdx.x) >= P.prob[pi + 1].work_begin) ++pi;
+  const AttnProb& prob = P.prob[pi];
+  int local = static_cast<int>(blockIdx.x) - prob.work_begin;
+  const int split = local % prob.splits;
+  local /= prob.splits;
+  const int pair = prob.head_pair;
+  const int nheads = pair ? P.hq / 2 : P.hq;
+  const int head = pair ? 2 * (local % nheads) : local % nheads;
+  local /= nheads;
+  const int unit = prob.units - 1 - local;
+  const int i0 = pair ? 0 : unit * (kTilesPerCta * kBlockM);
+  const int nq = prob.nq;
+  const int imax = min(i0 + (pair ? kBlockM : kTilesPerCta * kBlockM), nq);
+  const int hk = head / (P.hq / P.hkv);
+#define TILE_R0(t) (pair ? 0 : i0 + (t) * kBlockM)
+#define TILE_HEAD(t) (head + pair * (t))
+
+  int T = 0;
+  for (int s = 0; s < prob.nseg; ++s) T += seg_tiles2(prob.seg[s], imax);
+  const int t_begin = static_cast<int>(static_cast<long long>(T) * split / prob.splits);
+  const int t_end = static_cast<int>(static_cast<long long>(T) * (split + 1) / prob.splits);
+  const int ntiles = t_end - t_begin;
+  const CUtensorMap* tm = P.tmap[pi];
+
+  if (warp == kProducerWarp && elect_one()) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < kKS2; ++s) {
+      mbar_init(k_full + s, 1);
+      mbar_init(k_empty + s, 1);
+    }
+    for (int s = 0; s < kVS2; ++s) {
+      mbar_init(v_full + s, 1);
+      mbar_init(v_empty + s, 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(s_full + i, 1);
+      mbar_init(p_full + i, 128);
+    }
+    mbar_init(o_full + 0, 1);
+    mbar_init(o_full + 1, 1);
+    mbar_init(o_done, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm[0]);
+    for (int s = 0; s < prob.nseg; ++s) {
+      tma_prefetch_desc(&tm[1 + 2 * s]);
+      tma_prefetch_desc(&tm[2 + 2 * s]);
+    }
+  }
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kProducerWarp) {
+    // ======================================================== TMA producer
+    if (elect_one()) {
+      const bool has1 = TILE_R0(1) < nq;
+      mbar_expect_tx(q_full, (has1 ? 2u : 1u) * kTileBytes);
+      for (int qt = 0; qt < (has1 ? 2 : 1); ++qt)
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d(smem + Smem2::q + qt * kTileBytes + c * kBoxBytes, &tm[0], q_full,
+                      TILE_HEAD(qt) * kHeadDim + c * 64, TILE_R0(qt));
+      Cursor cur = cursor_at2(prob, imax, t_begin);
+      for (int it = 0; it < ntiles; ++it) {
+        const CUtensorMap* km = &tm[1 + 2 * cur.seg];
+        const CUtensorMap* vm = &tm[2 + 2 * cur.seg];
+        const int ks = it % kKS2, vs = it % kVS2;
+        if (it >= kKS2) mbar_wait(k_empty + ks, ((it / kKS2) - 1) & 1);
+        mbar_expect_tx(k_full + ks, kKvTile2);
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d(smem + Smem2::k + ks * kKvTile2 + c * kKvBox2, km, k_full + ks,
+                      hk * kHeadDim + c * 64, cur.kt * kBN2);
+        if (it >= kVS2) mbar_wait(v_empty + vs, ((it / kVS2) - 1) & 1);
+        mbar_expect_tx(v_full + vs, kKvTile2);
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d(smem + Smem2::v + vs * kKvTile2 + c * kKvBox2, vm, v_full + vs,
+                      hk * kHeadDim + c * 64, cur.kt * kBN2);
+        cursor_next2(prob, imax, cur);
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ======================================================== MMA issuer
+    if (elect_one()) {
+      const uint32_t idesc_qk = idesc_bf16_f32(128, kBN2, 0, 0);  // Q, K both K-major
+      const uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);   // P (TMEM), V MN-major
+      const uint32_t sq = smem_u32(smem + Smem2::q);
+      const uint32_t sk = smem_u32(smem + Smem2::k);
+      const uint32_t sv = smem_u32(smem + Smem2::v);
+      // per (tile, buffer) use counters -> mbarrier parities
+      uint32_t s_cnt[2][2] = {{0, 0}, {0, 0}}, p_cnt[2][2] = {{0, 0}, {0, 0}};
+      bool o_acc[2] = {false, false};
+      auto issue_qk = [&](int qt, int b, int ks) {
+        const uint32_t d = tmem + (qt * 2 + b) * kBN2;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t qoff = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
+          const uint32_t koff = (kk >> 2) * kKvBox2 + (kk & 3) * 32;
+          mma_ss(d, sdesc_sw128(sq + qt * kTileBytes + qoff, 16, 1024),
+                 sdesc_sw128(sk + ks * kKvTile2 + koff, 16, 1024), idesc_qk, kk > 0 ? 1u : 0u);
+        }
+        tc_commit(s_full + qt * 2 + b);
+        ++s_cnt[qt][b];
+      };
+      auto issue_pv = [&](int qt, int b, int vs) {
+        const uint32_t d = tmem + 256 + qt * 128;
+        const uint32_t a = tmem + (qt * 2 + b) * kBN2;
+#pragma unroll
+        for (int kk = 0; kk < kBN2 / 16; ++kk)
+          mma_ts(d, a + kk * 8, sdesc_sw128(sv + vs * kKvTile2 + kk * 2048, kKvBox2, 1024), idesc_pv,
+                 (o_acc[qt] || kk > 0) ? 1u : 0u);
+        o_acc[qt] = true;
+        tc_commit(o_full + qt);
+      };
+      auto modes_at = [&](const Cursor& c, int (&m)[2]) {
+        for (int qt = 0; qt < 2; ++qt) m[qt] = tile_mode2(prob.seg[c.seg], c.kt, TILE_R0(qt), nq);
+      };
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      // prologue: QK of tiles 0 and 1 into buffers 0 and 1
+      Cursor cq = cursor_at2(prob, imax, t_begin);  // cursor of the next QK tile
+      for (int it = 0; it < 2 && it < ntiles; ++it) {
+        int m[2];
+        modes_at(cq, m);
+        const int ks = it % kKS2;
+        mbar_wait(k_full + ks, (it / kKS2) & 1);
+        tc_fence_after();
+        for (int qt = 0; qt < 2; ++qt)
+          if (m[qt] != kSkip) issue_qk(qt, it & 1, ks);
+        tc_commit(k_empty + ks);
+        cursor_next2(prob, imax, cq);
+      }
+      Cursor cp = cursor_at2(prob, imax, t_begin);  // cursor of the PV tile
+      for (int it = 0; it < ntiles; ++it) {
+        const int b = it & 1, vs = it % kVS2;
+        int m[2], mn[2] = {kSkip, kSkip};
+        modes_at(cp, m);
+        const bool has_next = it + 2 < ntiles;
+        const int ksn = (it + 2) % kKS2;
+        if (has_next) modes_at(cq, mn);
+        mbar_wait(v_full + vs, (it / kVS2) & 1);
+        bool k_ready = false;
+        for (int qt = 0; qt < 2; ++qt) {
+          if (m[qt] != kSkip) {
+            mbar_wait(p_full + qt * 2 + b, p_cnt[qt][b] & 1);
+            ++p_cnt[qt][b];
+            tc_fence_after();
+            issue_pv(qt, b, vs);
+          }
+          if (qt == 1) tc_commit(v_empty + vs);
+          // QK_t(it+2) into the buffer PV_t(it) just drained (in-order tensor pipe)
+          if (has_next && mn[qt] != kSkip) {
+            if (!k_ready) {
+              mbar_wait(k_full + ksn, ((it + 2) / kKS2) & 1);
+              tc_fence_after();
+              k_ready = true;
+            }
+            issue_qk(qt, b, ksn);
+          }
+        }
+        if (has_next) {
+          tc_commit(k_empty + ksn);
+          cursor_next2(prob, imax, cq);
+        }
+        cursor_next2(prob, imax, cp);
+      }
+      tc_commit(o_done);
+    }
+  } else if (warp < kProducerWarp) {
+    // ======================================================== softmax warpgroups
+    const int qt = warp >> 2;
+    const int quad = warp & 3;
+    const int row = TILE_R0(qt) + quad * 32 + lane;
+    const int qhead = TILE_HEAD(qt);
+    const uint32_t t_lane = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t tO = tmem + t_lane + 256 + qt * 128;
+    const float sl2 = P.scale_log2;
+    const float2 sl2v = make_float2(sl2, sl2);
+    float m_ref = -INFINITY;
+    float l = 0.f;
+    uint32_t cnt = 0;                 // PV_t issued so far (o_full parity)
+    uint32_t bcnt[2] = {0, 0};        // uses of S buffer b (s_full parity)
+    Cursor cur = cursor_at2(prob, imax, t_begin);
+    uint32_t sr[2][32];
+    uint32_t pk[2][16];
+    for (int it = 0; it < ntiles; ++it, cursor_next2(prob, imax, cur)) {
+      const AttnSeg sg = prob.seg[cur.seg];
+      const int mode = tile_mode2(sg, cur.kt, TILE_R0(qt), nq);
+      if (mode == kSkip) continue;
+      const int b = it & 1;
+      const uint32_t tS = tmem + t_lane + (qt * 2 + b) * kBN2;
+      mbar_wait(s_full + qt * 2 + b, bcnt[b] & 1);
+      ++bcnt[b];
+      tc_fence_after();
+      auto load_s = [&]() {
+        tmem_ld32(tS, sr[0]);
+        tmem_ld32(tS + 32, sr[1]);
+        tmem_wait_ld();
+      };
+      auto chunk_max = [&](int c, float (&mxp)[8]) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const int t = (j / 2) & 7;
+          mxp[t] = fmaxf(mxp[t], fmaxf(__uint_as_float(sr[c][j]), __uint_as_float(sr[c][j + 1])));
+        }
+      };
+      auto chunk_exp = [&](int c, float2 negm, bool emu) {  // in place: sr[c] := p
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 x2 = __ffma2_rn(
+              make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1])), sl2v, negm);
+          float2 p2;
+          if (kEmu > 0 && emu && (j % (16 / kEmu)) == (16 / kEmu) - 1)
+            p2 = exp2_poly2(x2);
+          else
+            p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));  // -inf -> 0
+          sr[c][2 * j] = __float_as_uint(p2.x);
+          sr[c][2 * j + 1] = __float_as_uint(p2.y);
+        }
+      };
+      auto chunk_pack = [&](int c, float2 (&sacc)[4]) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 p2 = make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1]));
+          sacc[j & 3] = __fadd2_rn(sacc[j & 3], p2);
+          __nv_bfloat162 bb = __floats2bfloat162_rn(p2.x, p2.y);
+          pk[c][j] = *reinterpret_cast<uint32_t*>(&bb);
+        }
+      };
+      auto exp_pack_all = [&](float2 negm, bool emu, float2 (&sacc)[4]) {
+        chunk_exp(0, negm, emu);
+        chunk_exp(1, negm, emu);
+        chunk_pack(0, sacc);
+        chunk_pack(1, sacc);
+      };
+      float alpha = 1.f;
+      bool rescale = false;
+      float mxp[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
+      float2 sacc[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
+      bool done = false;
+      load_s();
+      if (mode == kFull && m_ref != -INFINITY) {
+        const float2 negm = make_float2(-m_ref, -m_ref);
+        chunk_max(0, mxp);
+        chunk_max(1, mxp);
+        exp_pack_all(negm, true, sacc);
+        const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                               fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+        done = !(mx * sl2 > m_ref + 8.f);
+        if (!done) {
+#pragma unroll
+          for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
+          load_s();
+        }
+      } else if (mode == kPart) {
+        const int k0 = cur.kt * kBN2;
+        int lim = sg.len - k0;
+        if (sg.causal) lim = min(lim, row - k0 + 1);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c * 32 + j >= lim) sr[c][j] = __float_as_uint(-INFINITY);
+      }
+      if (!done) {
+        chunk_max(0, mxp);
+        chunk_max(1, mxp);
+        const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                               fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+        const float m_new = fmaxf(m_ref, mx * sl2);
+        if (m_new > m_ref + 8.f) {
+          alpha = exp2f(m_ref - m_new);
+          m_ref = m_new;
+          rescale = true;
+        }
+        const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+        exp_pack_all(make_float2(-m_use, -m_use), mode == kFull, sacc);
+      }
+      tmem_st16(tS, pk[0]);
+      tmem_st16(tS + 16, pk[1]);
+      const float2 sum2 = __fadd2_rn(__fadd2_rn(sacc[0], sacc[1]), __fadd2_rn(sacc[2], sacc[3]));
+      l = l * alpha + (sum2.x + sum2.y);
+      if (rescale && cnt > 0) {
+        mbar_wait(o_full + qt, (cnt - 1) & 1);  // PV_t of the previous tile has landed
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          tmem_ld32(tO + 32 * c, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
+          tmem_st32(tO + 32 * c, o);
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_full + qt * 2 + b);
+      ++cnt;
+    }
+    // ---- epilogue: O / l, lse.  With S double-buffered, PV(n-1) and PV(n) may both be in
+    // flight here, which a parity wait on o_full cannot disambiguate: wait for the one-shot
+    // barrier the MMA warp commits after its last instruction instead.
+    mbar_wait(o_done, 0);
+    tc_fence_after();
+    const bool valid_row = row < nq;
+    const float inv = (l > 0.f) ? 1.f / l : 0.f;
+    const long long obase = static_cast<long long>(split) * prob.split_stride_out +
+                            static_cast<long long>(row) * prob.ldo + qhead * kHeadDim;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t o[32];
+      if (cnt > 0) {
+        tmem_ld32(tO + 32 * c, o);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o[j] = 0u;
+      }
+      if (valid_row) {
+        if (prob.out_f32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(prob.out) + obase + 32 * c);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(__uint_as_float(o[4 * j]) * inv, __uint_as_float(o[4 * j + 1]) * inv,
+                                 __uint_as_float(o[4 * j + 2]) * inv, __uint_as_float(o[4 * j + 3]) * inv);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(prob.out) + obase + 32 * c);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 bb = __floats2bfloat162_rn(__uint_as_float(o[8 * j + 2 * e]) * inv,
+                                                        __uint_as_float(o[8 * j + 2 * e + 1]) * inv);
+              w[e] = *reinterpret_cast<uint32_t*>(&bb);
+            }
+            dst[j] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+    }
+    if (valid_row && prob.lse) {
+      const float lse = (l > 0.f) ? (m_ref + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+      prob.lse[static_cast<long long>(split) * prob.split_stride_lse +
+               static_cast<long long>(row) * prob.ld_lse + qhead] = lse;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == kMmaWarp) tmem_dealloc(tmem, kTmemCols);
+#undef TILE_R0
+#undef TILE_HEAD
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -958,7 +1396,7 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 
 // 2D bf16 [rows x cols] row-major (row stride ld elements), box 64 cols x 128 rows, SW128.
 bool make_tmap(CUtensorMap* m, const void* base, long long rows, long long cols, long long ld,
-               std::string* err) {
+               std::string* err, int box_rows = 128) {
   auto enc = tensor_map_encoder();
   if (!enc) {
     if (err) *err = "cuTensorMapEncodeTiled unavailable";
@@ -967,7 +1405,7 @@ bool make_tmap(CUtensorMap* m, const void* base, long long rows, long long cols,
   if (rows < 1) rows = 1;  // empty segments are never loaded
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1009,8 +1447,11 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
       {attn_fwd1_kernel<4, true>, Smem1::bytes, kThreads1, 1},            // 3 1 + 25% FMA exp2
       {attn_fwd_kernel<4, 2, false, true>, Smem<2>::bytes, kThreads, 0},  // 4 0 + 25% FMA exp2
       {attn_fwd1_kernel<2, true>, Smem1::bytes, kThreads1, 1},            // 5 1 + 12.5% FMA exp2
-      {attn_fwd_kernel<0, 2>, Smem<2>::bytes, kThreads, 0}};              // 6 0 without the
+      {attn_fwd_kernel<0, 2>, Smem<2>::bytes, kThreads, 0},               // 6 0 without the
                                                                           //   one-chunk-behind pack
+      {attn_fwd2_kernel<0>, Smem2::bytes, kThreads, 2},                   // 7 64-key tiles, S x2
+      {attn_fwd2_kernel<2>, Smem2::bytes, kThreads, 2},                   // 8 7 + 25% FMA exp2
+      {attn_fwd2_kernel<1>, Smem2::bytes, kThreads, 2}};                  // 9 7 + 12.5% FMA exp2
   constexpr int kNumVar = sizeof(variants) / sizeof(variants[0]);
   static int vsel = [] {
     const char* e = getenv("SPAVA_ATTN_VARIANT");
@@ -1031,7 +1472,7 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
     AttnProb& p = P.prob[np];
     p.nq = v.nq;
     p.nseg = v.nseg;
-    p.head_pair = (var.family == 0 && v.nq <= kBlockM && (hq / hkv) % 2 == 0) ? 1 : 0;
+    p.head_pair = (var.family != 1 && v.nq <= kBlockM && (hq / hkv) % 2 == 0) ? 1 : 0;
     p.units = p.head_pair ? 1 : (v.nq + rows_per_cta - 1) / rows_per_cta;
     p.splits = v.splits;
     p.work_begin = work;
@@ -1051,10 +1492,11 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
         if (err) *err = "attention: causal segment longer than the query";
         return cudaErrorInvalidValue;
       }
+      const int kv_box = var.family == 2 ? kBN2 : kBlockN;
       if (!make_tmap(&P.tmap[np][1 + 2 * s], v.seg[s].k, v.seg[s].len,
-                     static_cast<long long>(hkv) * dh, v.seg[s].ld, err) ||
+                     static_cast<long long>(hkv) * dh, v.seg[s].ld, err, kv_box) ||
           !make_tmap(&P.tmap[np][2 + 2 * s], v.seg[s].v, v.seg[s].len,
-                     static_cast<long long>(hkv) * dh, v.seg[s].ld, err))
+                     static_cast<long long>(hkv) * dh, v.seg[s].ld, err, kv_box))
         return cudaErrorInvalidValue;
     }
     work += p.units * (p.head_pair ? hq / 2 : hq) * p.splits;
