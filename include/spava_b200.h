@@ -178,6 +178,17 @@ int spava_host_layer(spava_host* host, const void* q, const void* k, const void*
                      int32_t* sel, void* stream);
 /* Local fabric: every host of the fabric, phase by phase, on one stream.
  * q/k/v/out/sel are arrays of H per-host pointers (host arrays).            */
+/* spava_host_layer with HOST buffers (the reference's run_host takes host Matrix inputs,
+ * simhost.cpp:317-437): q/k/v host rows are copied to the caller-owned device staging
+ * buffers in the order the phases consume them (k, v and query rows; anchor + block-lo rows
+ * of q; block-hi rows of q) on an internal copy stream, each phase waits only for its rows,
+ * and each output row range (anchor + lo after stage 1, hi after stage 2, query after the
+ * merge) is copied back while later phases still run.  Host buffers should be pinned for
+ * the copies to overlap.  `stream` waits for the last copy before returning control to the
+ * caller's stream order; sel_h/sel_d may be NULL. */
+int spava_host_layer_hostbuf(spava_host* host, const void* q_h, const void* k_h, const void* v_h,
+                             void* out_h, int32_t* sel_h, void* q_d, void* k_d, void* v_d,
+                             void* out_d, int32_t* sel_d, void* stream);
 int spava_sim_layer(spava_fabric* fab, spava_host* const* hosts, const void* const* q,
                     const void* const* k, const void* const* v, void* const* out,
                     int32_t* const* sel, void* stream);
@@ -187,7 +198,9 @@ int spava_host_status(spava_host* host, void* stream, int32_t* status_out);
 
 /* Device timing of this host's launches, by kernel class (0 attention, 1 score,
  * 2 select+pack, 3 merge): CUDA events on the launching stream around every
- * launch while enabled.  spava_host_set_timing resets the counters;
+ * launch while enabled (enable = 2 additionally runs the scorer on the caller's stream
+ * instead of the overlapping side stream, so kernels are timed in isolation).
+ * spava_host_set_timing resets the counters;
  * spava_host_timing synchronises on the recorded events and returns the summed
  * milliseconds per class, the algorithmic attention FLOPs launched (reference
  * convention, attention.cpp:33-36) and the attention launch count.           */

@@ -181,9 +181,18 @@ struct spava_host {
   int32_t* status = nullptr;
   void* base = nullptr;
   cudaEvent_t ev[6] = {};  // pass1_ready, pass2_ready, q_ready, pass1_done, pass2_done, q_done
+  // scoring runs on a high-priority side stream forked from the caller's stream, so the
+  // CUDA-core/FP64 scorer overlaps the query / stage-1 attention that does not need it
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_sel = nullptr;
+  // host-buffer layer (spava_host_layer_hostbuf): H2D / D2H copy streams and their edges
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_in[3] = {};   // k/v + query rows, anchor + lo rows of q, hi rows of q
+  cudaEvent_t ev_out[4] = {};  // stage1 done, stage2 done, merge done, d2h done
   // optional per-kernel-class device timing (bench roofline): CUDA events recorded on the
   // launching stream around every launch; classes 0 attention, 1 score, 2 select, 3 merge
   bool timing = false;
+  bool serial = false;  // timing mode 2: scoring on the caller's stream (isolated kernels)
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<std::pair<size_t, size_t>> spans[4];
@@ -817,6 +826,15 @@ int spava_host_create(spava_fabric* F, int h, spava_host** out) {
   H->qsplit_lse = reinterpret_cast<float*>(b); b += ql;
   H->status = reinterpret_cast<int32_t*>(b);
   for (auto& e : H->ev) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CU_TRY(cudaEventCreateWithFlags(&H->ev_fork, cudaEventDisableTiming));
+  CU_TRY(cudaEventCreateWithFlags(&H->ev_sel, cudaEventDisableTiming));
+  int prio_lo = 0, prio_hi = 0;
+  CU_TRY(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CU_TRY(cudaStreamCreateWithPriority(&H->side, cudaStreamNonBlocking, prio_hi));
+  CU_TRY(cudaStreamCreateWithFlags(&H->h2d, cudaStreamNonBlocking));
+  CU_TRY(cudaStreamCreateWithFlags(&H->d2h, cudaStreamNonBlocking));
+  for (auto& e : H->ev_in) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : H->ev_out) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   *out = H;
   return SPAVA_OK;
 }
@@ -824,6 +842,15 @@ int spava_host_create(spava_fabric* F, int h, spava_host** out) {
 int spava_host_destroy(spava_host* H) {
   if (!H) return SPAVA_OK;
   for (auto& e : H->ev)
+    if (e) cudaEventDestroy(e);
+  if (H->ev_fork) cudaEventDestroy(H->ev_fork);
+  if (H->ev_sel) cudaEventDestroy(H->ev_sel);
+  if (H->side) cudaStreamDestroy(H->side);
+  if (H->h2d) cudaStreamDestroy(H->h2d);
+  if (H->d2h) cudaStreamDestroy(H->d2h);
+  for (auto& e : H->ev_in)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : H->ev_out)
     if (e) cudaEventDestroy(e);
   for (auto& e : H->ev_pool) cudaEventDestroy(e);
   H->own.release();
@@ -842,41 +869,137 @@ int spava_host_rows(const spava_host* H) {
   return p.l_a + 2 * p.l_b + p.n_t;
 }
 
-int spava_host_layer(spava_host* H, const void* q, const void* k, const void* v, void* out,
-                     int32_t* sel, void* stream) {
+namespace {
+
+// Optional host<->device copy pipeline around one layer: each compute phase waits only for
+// the rows it reads (ev_in) and each finished output row range is copied back while later
+// phases still run (ev_out).  Inputs arrive in the order the phases need them.
+struct CopyEdges {
+  bool on = false;
+};
+
+int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdges& cp) {
   spava_fabric* F = H->fab;
-  if (!F->nccl && F->plan.hosts != 1)
-    return fail(SPAVA_EINVAL, "host_layer: local fabric with H > 1 must be driven by spava_sim_layer");
-  CU_TRY(cudaSetDevice(F->device));
-  cudaStream_t st = as_stream(stream);
-  HostBufs b{static_cast<const uint8_t*>(q), static_cast<const uint8_t*>(k),
-             static_cast<const uint8_t*>(v), static_cast<uint8_t*>(out), sel};
+  cudaStream_t ss = H->serial ? st : H->side;
+  auto need = [&](cudaStream_t s, int i) -> cudaError_t {
+    return cp.on ? cudaStreamWaitEvent(s, H->ev_in[i], 0) : cudaSuccess;
+  };
+  auto done = [&](cudaStream_t s, int i) -> cudaError_t {
+    return cp.on ? cudaEventRecord(H->ev_out[i], s) : cudaSuccess;
+  };
+  // fork: scoring + selection on the side stream (its inputs are this step's q/k on st)
+  CU_TRY(cudaEventRecord(H->ev_fork, st));
+  CU_TRY(cudaStreamWaitEvent(ss, H->ev_fork, 0));
+  CU_TRY(need(ss, 0));
+  CU_TRY(need(st, 0));
   if (!F->nccl) {
-    ST_TRY(phase_select(H, b, st, false));
+    // H = 1: block lo (v = 0) has no passing segment, so only stage 2 waits for selection
+    ST_TRY(phase_select(H, b, ss, false));
+    CU_TRY(cudaEventRecord(H->ev_sel, ss));
     ST_TRY(phase_query(H, b, st, false));
+    CU_TRY(need(st, 1));
     ST_TRY(phase_stage1(H, b, st));
+    CU_TRY(done(st, 0));
+    CU_TRY(cudaStreamWaitEvent(st, H->ev_sel, 0));
+    CU_TRY(need(st, 2));
     ST_TRY(phase_stage2(H, b, st));
-    return phase_merge(H, b, st);
+    CU_TRY(done(st, 1));
+    ST_TRY(phase_merge(H, b, st));
+    return done(st, 2) == cudaSuccess ? SPAVA_OK : fail(SPAVA_ECUDA, "event record");
   }
   cudaStream_t cs = F->comm_stream;
-  ST_TRY(phase_select(H, b, st, true));  // records pass1_ready, pass2_ready
+  ST_TRY(phase_select(H, b, ss, true));  // records pass1_ready, pass2_ready on ss
+  CU_TRY(cudaEventRecord(H->ev_sel, ss));
   CU_TRY(cudaStreamWaitEvent(cs, H->ev[0], 0));
   ST_TRY(nccl_round(F, H->ex, 0));
   CU_TRY(cudaEventRecord(H->ev[3], cs));
   CU_TRY(cudaStreamWaitEvent(cs, H->ev[1], 0));
   ST_TRY(nccl_round(F, H->ex, 1));
   CU_TRY(cudaEventRecord(H->ev[4], cs));
-  ST_TRY(phase_query(H, b, st, true));  // overlaps the pass rounds
+  ST_TRY(phase_query(H, b, st, true));  // overlaps scoring and the pass rounds
   CU_TRY(cudaStreamWaitEvent(cs, H->ev[2], 0));
   ST_TRY(nccl_qround(F, H->ex));
   CU_TRY(cudaEventRecord(H->ev[5], cs));
   CU_TRY(cudaStreamWaitEvent(st, H->ev[3], 0));
   if (!F->plan.zigzag) CU_TRY(cudaStreamWaitEvent(st, H->ev[4], 0));  // simhost.cpp:392-402
+  CU_TRY(need(st, 1));
   ST_TRY(phase_stage1(H, b, st));
+  CU_TRY(done(st, 0));
   CU_TRY(cudaStreamWaitEvent(st, H->ev[4], 0));
+  CU_TRY(cudaStreamWaitEvent(st, H->ev_sel, 0));  // join the side stream (sel copy-out)
+  CU_TRY(need(st, 2));
   ST_TRY(phase_stage2(H, b, st));
+  CU_TRY(done(st, 1));
   CU_TRY(cudaStreamWaitEvent(st, H->ev[5], 0));
-  return phase_merge(H, b, st);
+  ST_TRY(phase_merge(H, b, st));
+  return done(st, 2) == cudaSuccess ? SPAVA_OK : fail(SPAVA_ECUDA, "event record");
+}
+
+}  // namespace
+
+int spava_host_layer(spava_host* H, const void* q, const void* k, const void* v, void* out,
+                     int32_t* sel, void* stream) {
+  spava_fabric* F = H->fab;
+  if (!F->nccl && F->plan.hosts != 1)
+    return fail(SPAVA_EINVAL, "host_layer: local fabric with H > 1 must be driven by spava_sim_layer");
+  CU_TRY(cudaSetDevice(F->device));
+  HostBufs b{static_cast<const uint8_t*>(q), static_cast<const uint8_t*>(k),
+             static_cast<const uint8_t*>(v), static_cast<uint8_t*>(out), sel};
+  return layer_impl(H, b, as_stream(stream), CopyEdges{});
+}
+
+int spava_host_layer_hostbuf(spava_host* H, const void* q_h, const void* k_h, const void* v_h,
+                             void* out_h, int32_t* sel_h, void* q_d, void* k_d, void* v_d,
+                             void* out_d, int32_t* sel_d, void* stream) {
+  spava_fabric* F = H->fab;
+  if (!F->nccl && F->plan.hosts != 1)
+    return fail(SPAVA_EINVAL, "host_layer_hostbuf: local fabric with H > 1 must be driven by spava_sim_layer");
+  if (!q_h || !k_h || !v_h || !out_h || !q_d || !k_d || !v_d || !out_d)
+    return fail(SPAVA_EINVAL, "host_layer_hostbuf: null buffer");
+  CU_TRY(cudaSetDevice(F->device));
+  const spava_layer_cfg& c = F->cfg;
+  const spava_plan& p = F->plan;
+  cudaStream_t st = as_stream(stream);
+  const size_t rq = static_cast<size_t>(c.hq) * c.dh * 2, rk = static_cast<size_t>(c.hkv) * c.dh * 2;
+  const size_t rows = static_cast<size_t>(p.l_a) + 2ull * p.l_b + p.n_t;
+  const size_t qrow = static_cast<size_t>(p.l_a) + 2ull * p.l_b, lo_end = static_cast<size_t>(p.l_a) + p.l_b;
+  auto* qd = static_cast<uint8_t*>(q_d);
+  auto* od = static_cast<uint8_t*>(out_d);
+  const auto* qh = static_cast<const uint8_t*>(q_h);
+  auto* oh = static_cast<uint8_t*>(out_h);
+  cudaStream_t hs = H->h2d, ds = H->d2h;
+  // inputs, in the order the phases consume them (the previous step's work on st is done
+  // before the buffers are overwritten: h2d waits for the fork point of this step)
+  CU_TRY(cudaEventRecord(H->ev_fork, st));
+  CU_TRY(cudaStreamWaitEvent(hs, H->ev_fork, 0));
+  CU_TRY(cudaMemcpyAsync(k_d, k_h, rows * rk, cudaMemcpyHostToDevice, hs));
+  CU_TRY(cudaMemcpyAsync(v_d, v_h, rows * rk, cudaMemcpyHostToDevice, hs));
+  CU_TRY(cudaMemcpyAsync(qd + qrow * rq, qh + qrow * rq, static_cast<size_t>(p.n_t) * rq, cudaMemcpyHostToDevice, hs));
+  CU_TRY(cudaEventRecord(H->ev_in[0], hs));
+  CU_TRY(cudaMemcpyAsync(qd, qh, lo_end * rq, cudaMemcpyHostToDevice, hs));
+  CU_TRY(cudaEventRecord(H->ev_in[1], hs));
+  CU_TRY(cudaMemcpyAsync(qd + lo_end * rq, qh + lo_end * rq, static_cast<size_t>(p.l_b) * rq,
+                         cudaMemcpyHostToDevice, hs));
+  CU_TRY(cudaEventRecord(H->ev_in[2], hs));
+  HostBufs b{static_cast<const uint8_t*>(q_d), static_cast<const uint8_t*>(k_d),
+             static_cast<const uint8_t*>(v_d), od, sel_d};
+  CopyEdges cp;
+  cp.on = true;
+  ST_TRY(layer_impl(H, b, st, cp));
+  // outputs as soon as each row range is final
+  CU_TRY(cudaStreamWaitEvent(ds, H->ev_out[0], 0));
+  CU_TRY(cudaMemcpyAsync(oh, od, lo_end * rq, cudaMemcpyDeviceToHost, ds));
+  CU_TRY(cudaStreamWaitEvent(ds, H->ev_out[1], 0));
+  CU_TRY(cudaMemcpyAsync(oh + lo_end * rq, od + lo_end * rq, static_cast<size_t>(p.l_b) * rq,
+                         cudaMemcpyDeviceToHost, ds));
+  CU_TRY(cudaStreamWaitEvent(ds, H->ev_out[2], 0));
+  CU_TRY(cudaMemcpyAsync(oh + qrow * rq, od + qrow * rq, static_cast<size_t>(p.n_t) * rq,
+                         cudaMemcpyDeviceToHost, ds));
+  if (sel_h && sel_d && p.l_p > 0)
+    CU_TRY(cudaMemcpyAsync(sel_h, sel_d, 2ull * p.l_p * sizeof(int32_t), cudaMemcpyDeviceToHost, ds));
+  CU_TRY(cudaEventRecord(H->ev_out[3], ds));
+  CU_TRY(cudaStreamWaitEvent(st, H->ev_out[3], 0));  // the caller's stream covers the copies
+  return SPAVA_OK;
 }
 
 int spava_sim_layer(spava_fabric* F, spava_host* const* hosts, const void* const* q,
@@ -909,6 +1032,7 @@ int spava_sim_layer(spava_fabric* F, spava_host* const* hosts, const void* const
 
 int spava_host_set_timing(spava_host* H, int enable) {
   H->timing = enable != 0;
+  H->serial = enable == 2;
   H->ev_used = 0;
   for (auto& s : H->spans) s.clear();
   H->attn_flops = 0.0;

@@ -35,7 +35,8 @@ EXPORTED_SYMBOLS = [
     "spava_attention_workspace", "spava_attention", "spava_mha_merge",
     "spava_fabric_create_local", "spava_nccl_unique_id", "spava_fabric_create_nccl",
     "spava_fabric_destroy", "spava_host_create", "spava_host_destroy", "spava_host_plan",
-    "spava_host_rows", "spava_host_layer", "spava_sim_layer", "spava_host_status",
+    "spava_host_rows", "spava_host_layer", "spava_host_layer_hostbuf", "spava_sim_layer",
+    "spava_host_status",
     "spava_host_set_timing", "spava_host_timing", "spava_kernel_launches",
     "spava_debug_attn_prof",
 ]
@@ -102,6 +103,7 @@ def lib():
                                       C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_int,
                                       C.c_void_p, C.c_void_p, C.c_void_p]
         L.spava_host_layer.argtypes = [C.c_void_p] * 7
+        L.spava_host_layer_hostbuf.argtypes = [C.c_void_p] * 12
         L.spava_sim_layer.argtypes = [C.c_void_p] * 8
         L.spava_host_create.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
         L.spava_host_destroy.argtypes = [C.c_void_p]
@@ -364,6 +366,18 @@ class Host:
         """One layer of this host (NCCL fabric, or a local fabric with H == 1)."""
         _check(lib().spava_host_layer(self._p, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(sel),
                                       _stream(stream)))
+
+    def layer_hostbuf(self, q_h, k_h, v_h, out_h, q_d, k_d, v_d, out_d, sel_h=None, sel_d=None,
+                      stream=None):
+        """One layer from HOST buffers (pinned CPU tensors) through caller-owned device
+        staging buffers; copies are pipelined with the phases (spava_host_layer_hostbuf)."""
+        for t in (q_h, k_h, v_h, out_h):
+            if t.is_cuda or not t.is_contiguous():
+                raise ValueError("layer_hostbuf: host tensors must be contiguous CPU tensors")
+        _check(lib().spava_host_layer_hostbuf(
+            self._p, C.c_void_p(q_h.data_ptr()), C.c_void_p(k_h.data_ptr()), C.c_void_p(v_h.data_ptr()),
+            C.c_void_p(out_h.data_ptr()), C.c_void_p(sel_h.data_ptr()) if sel_h is not None else None,
+            _ptr(q_d), _ptr(k_d), _ptr(v_d), _ptr(out_d), _ptr(sel_d), _stream(stream)))
 
     def set_timing(self, enable=True):
         _check(lib().spava_host_set_timing(self._p, int(enable)))

@@ -134,3 +134,40 @@ def test_nccl_fabric_world1_matches_local(cuda):
         x.close()
     loc.close()
     nc.close()
+
+
+@pytest.mark.parametrize("nccl", [False, True])
+def test_host_buffer_layer_matches_device_layer(cuda, nccl):
+    """spava_host_layer_hostbuf (pinned host in/out, copies pipelined with the phases) gives
+    bit-identical outputs and indices to spava_host_layer on device buffers, and runs
+    back to back without the copies of one step racing the kernels of the next."""
+    import torch
+
+    from paper_2601_21444_b200 import spava
+
+    n_v, n_t, l_a, l_p, hq, hkv = 2100, 64, 32, 128, 4, 2
+    cfg = spava.LayerConfig.make(n_v, n_t, 1, l_a, l_p, hq, hkv)
+    fab = (spava.Fabric(cfg, 0, unique_id=spava.nccl_unique_id(), world=1, rank=0) if nccl
+           else spava.Fabric(cfg, 0))
+    host = fab.host(0)
+    rows = host.rows
+    g = torch.Generator(device=cuda).manual_seed(11)
+    ins = [torch.randn(rows, w * 128, device=cuda, generator=g).to(torch.bfloat16) for w in (hq, hkv, hkv)]
+    o_ref = torch.zeros(rows, hq * 128, dtype=torch.bfloat16, device=cuda)
+    s_ref = torch.zeros(2, l_p, dtype=torch.int32, device=cuda)
+    host.layer(*ins, o_ref, s_ref)
+    torch.cuda.synchronize()
+    hins = [x.cpu().pin_memory() for x in ins]
+    dev_bufs = [torch.empty_like(x) for x in ins]
+    o_d = torch.empty_like(o_ref)
+    s_d = torch.empty_like(s_ref)
+    for it in range(3):
+        o_h = torch.zeros(o_ref.shape, dtype=o_ref.dtype).pin_memory()
+        s_h = torch.zeros(s_ref.shape, dtype=s_ref.dtype).pin_memory()
+        host.layer_hostbuf(*hins, o_h, *dev_bufs, o_d, s_h, s_d)
+        torch.cuda.synchronize()
+        assert host.status() == 0
+        assert torch.equal(s_h, s_ref.cpu()), it
+        assert torch.equal(o_h, o_ref.cpu()), it
+    host.close()
+    fab.close()
