@@ -192,6 +192,13 @@ int spava_host_layer_hostbuf(spava_host* host, const void* q_h, const void* k_h,
 int spava_sim_layer(spava_fabric* fab, spava_host* const* hosts, const void* const* q,
                     const void* const* k, const void* const* v, void* const* out,
                     int32_t* const* sel, void* stream);
+/* spava_sim_layer with every host's phases bracketed by events and run alone on the GPU:
+ * ms_per_host[h] = host h's device time for one layer (excluding any exchange cost).  The
+ * max over hosts is the per-GPU layer time an H-GPU run would see before communication --
+ * used to measure load balance (zigzag vs naive pairing) on real kernels.  Synchronises. */
+int spava_sim_layer_timed(spava_fabric* fab, spava_host* const* hosts, const void* const* q,
+                          const void* const* k, const void* const* v, void* const* out,
+                          int32_t* const* sel, void* stream, float* ms_per_host);
 /* Device-side status word of the last layer (0 ok; non-zero: NaN score or a
  * merge row invalid everywhere).  Synchronises the given stream.            */
 int spava_host_status(spava_host* host, void* stream, int32_t* status_out);

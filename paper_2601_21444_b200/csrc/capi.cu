@@ -1030,6 +1030,50 @@ int spava_sim_layer(spava_fabric* F, spava_host* const* hosts, const void* const
   return SPAVA_OK;
 }
 
+int spava_sim_layer_timed(spava_fabric* F, spava_host* const* hosts, const void* const* q,
+                          const void* const* k, const void* const* v, void* const* out,
+                          int32_t* const* sel, void* stream, float* ms_per_host) {
+  if (!F || F->nccl) return fail(SPAVA_EINVAL, "sim_layer_timed: needs a local fabric");
+  if (!ms_per_host) return fail(SPAVA_EINVAL, "sim_layer_timed: null ms_per_host");
+  CU_TRY(cudaSetDevice(F->device));
+  cudaStream_t st = as_stream(stream);
+  const int H = F->plan.hosts;
+  std::vector<HostBufs> b(H);
+  for (int h = 0; h < H; ++h) {
+    if (!hosts[h] || hosts[h]->fab != F || hosts[h]->h != h)
+      return fail(SPAVA_EINVAL, "sim_layer_timed: hosts[h] must be host h of this fabric");
+    b[h] = HostBufs{static_cast<const uint8_t*>(q[h]), static_cast<const uint8_t*>(k[h]),
+                    static_cast<const uint8_t*>(v[h]), static_cast<uint8_t*>(out[h]),
+                    sel ? sel[h] : nullptr};
+  }
+  // events bracket each host's phase-1 and phase-2 work (run alone on the GPU, in order)
+  std::vector<cudaEvent_t> ev(4 * H);
+  for (auto& e : ev) CU_TRY(cudaEventCreate(&e));
+  int rc = SPAVA_OK;
+  for (int h = 0; h < H && rc == SPAVA_OK; ++h) {
+    cudaEventRecord(ev[4 * h], st);
+    rc = phase_select(hosts[h], b[h], st, false);
+    if (rc == SPAVA_OK) rc = phase_query(hosts[h], b[h], st, false);
+    cudaEventRecord(ev[4 * h + 1], st);
+  }
+  for (int h = 0; h < H && rc == SPAVA_OK; ++h) {
+    cudaEventRecord(ev[4 * h + 2], st);
+    rc = phase_stage1(hosts[h], b[h], st);
+    if (rc == SPAVA_OK) rc = phase_stage2(hosts[h], b[h], st);
+    if (rc == SPAVA_OK) rc = phase_merge(hosts[h], b[h], st);
+    cudaEventRecord(ev[4 * h + 3], st);
+  }
+  if (rc == SPAVA_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = fail(SPAVA_ECUDA, "sim_layer_timed: sync");
+  for (int h = 0; h < H && rc == SPAVA_OK; ++h) {
+    float a = 0.f, c = 0.f;
+    cudaEventElapsedTime(&a, ev[4 * h], ev[4 * h + 1]);
+    cudaEventElapsedTime(&c, ev[4 * h + 2], ev[4 * h + 3]);
+    ms_per_host[h] = a + c;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
+}
+
 int spava_host_set_timing(spava_host* H, int enable) {
   H->timing = enable != 0;
   H->serial = enable == 2;

@@ -36,6 +36,7 @@ EXPORTED_SYMBOLS = [
     "spava_fabric_create_local", "spava_nccl_unique_id", "spava_fabric_create_nccl",
     "spava_fabric_destroy", "spava_host_create", "spava_host_destroy", "spava_host_plan",
     "spava_host_rows", "spava_host_layer", "spava_host_layer_hostbuf", "spava_sim_layer",
+    "spava_sim_layer_timed",
     "spava_host_status",
     "spava_host_set_timing", "spava_host_timing", "spava_kernel_launches",
     "spava_debug_attn_prof",
@@ -105,6 +106,7 @@ def lib():
         L.spava_host_layer.argtypes = [C.c_void_p] * 7
         L.spava_host_layer_hostbuf.argtypes = [C.c_void_p] * 12
         L.spava_sim_layer.argtypes = [C.c_void_p] * 8
+        L.spava_sim_layer_timed.argtypes = [C.c_void_p] * 9
         L.spava_host_create.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
         L.spava_host_destroy.argtypes = [C.c_void_p]
         L.spava_host_rows.argtypes = [C.c_void_p]
@@ -433,6 +435,16 @@ class Fabric:
         _check(lib().spava_sim_layer(self._p, (C.c_void_p * n)(*[h._p.value for h in hosts]),
                                      arr(qs), arr(ks), arr(vs), arr(outs),
                                      arr(sels) if sels is not None else None, _stream(stream)))
+
+    def sim_layer_timed(self, hosts, qs, ks, vs, outs, sels=None, stream=None):
+        """sim_layer with each host's phases timed alone on the GPU: list of ms per host."""
+        n = len(hosts)
+        arr = lambda ts: (C.c_void_p * n)(*[t.data_ptr() if t is not None else None for t in ts])
+        ms = (C.c_float * n)()
+        _check(lib().spava_sim_layer_timed(self._p, (C.c_void_p * n)(*[h._p.value for h in hosts]),
+                                           arr(qs), arr(ks), arr(vs), arr(outs),
+                                           arr(sels) if sels is not None else None, _stream(stream), ms))
+        return list(ms)
 
     def close(self):
         if self._p:

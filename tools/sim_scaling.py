@@ -1,0 +1,46 @@
+"""Per-host layer time of H Spava hosts simulated on ONE B200 (each host's phases run alone,
+exchange through device memory): max over hosts = the per-GPU layer time an H-GPU run sees
+before NCCL exchange cost.  Compares zigzag (load-balanced) vs naive pairing.
+
+    python tools/sim_scaling.py [C3] [hosts ...]      -> JSON lines (projection, not a bench value)
+"""
+import json, sys, torch
+sys.path.insert(0, '.')
+import bench
+from paper_2601_21444_b200 import spava
+
+cfg_name = sys.argv[1] if len(sys.argv) > 1 else "C3"
+host_list = [int(x) for x in sys.argv[2:]] or [1, 2, 4, 8]
+cfg = bench.CONFIGS[cfg_name]
+dev = torch.device("cuda:0")
+hq, hkv = cfg["hq"], cfg["hkv"]
+for H in host_list:
+    for zz in ((True, False) if H > 1 else (True,)):
+        g = bench.geometry(cfg, H, zz)
+        lc = spava.LayerConfig.make(g["n_v"], g["n_t"], H, g["l_a"], g["l_p"], hq, hkv, 128, zigzag=zz)
+        fab = spava.Fabric(lc, 0)
+        hosts = [fab.host(h) for h in range(H)]
+        gen = torch.Generator(device=dev).manual_seed(7)
+        rows = hosts[0].rows
+        qs = [torch.randn(rows, hq * 128, device=dev, generator=gen).to(torch.bfloat16) for _ in range(H)]
+        ks = [torch.randn(rows, hkv * 128, device=dev, generator=gen).to(torch.bfloat16) for _ in range(H)]
+        vs = [torch.randn(rows, hkv * 128, device=dev, generator=gen).to(torch.bfloat16) for _ in range(H)]
+        outs = [torch.empty(rows, hq * 128, dtype=torch.bfloat16, device=dev) for _ in range(H)]
+        for _ in range(2):
+            fab.sim_layer_timed(hosts, qs, ks, vs, outs)
+        runs = [fab.sim_layer_timed(hosts, qs, ks, vs, outs) for _ in range(5)]
+        ms = [min(r[h] for r in runs) for h in range(H)]
+        fl = [bench.attn_flops_host(g, hq, h, zz) for h in range(H)]
+        mx = max(ms)
+        print(json.dumps({"config": cfg_name, "n": g["n"], "hosts": H, "pairing": "zigzag" if zz else "naive",
+                          "ms_per_host": [round(x, 3) for x in ms], "max_ms": round(mx, 3),
+                          "max_over_min": round(mx / min(ms), 3),
+                          "flops_max_over_min": round(max(fl) / min(fl), 3),
+                          "projected_tokens_per_s_excl_comm": round(g["n"] / (mx / 1e3)),
+                          "attn_tflops_per_s_on_max_host": round(fl[ms.index(mx)] / (mx / 1e3) / 1e12, 1)}),
+              flush=True)
+        for h in hosts:
+            h.close()
+        fab.close()
+        del qs, ks, vs, outs
+        torch.cuda.empty_cache()
