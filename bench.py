@@ -490,6 +490,47 @@ def run_spava_arm(args):
         except Exception as e:  # pragma: no cover
             extra["dense_torch_sdpa"] = {"error": str(e)[:200]}
         del qd, kd, vd
+        # same layer with the tensor-core scorer (score_mode=1): not bit-faithful, so it is
+        # reported beside the exact headline with its index agreement on these inputs
+        try:
+            lcf = spava.LayerConfig.make(g["n_v"], g["n_t"], 1, g["l_a"], g["l_p"], hq, hkv, DH, score_mode=1)
+            fabf = spava.Fabric(lcf, local)
+            hostf = fabf.host(0)
+            outf = torch.empty_like(out)
+            self_sel = sel.clone()
+            self_sel_f = torch.empty_like(sel)
+            for _ in range(args.warmup):
+                hostf.layer(q, k, v, outf, self_sel_f, stream)
+            torch.cuda.synchronize()
+            evf = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            for i in range(args.steps):
+                flush.zero_()
+                evf[i][0].record(stream)
+                hostf.layer(q, k, v, outf, self_sel_f, stream)
+                evf[i][1].record(stream)
+            torch.cuda.synchronize()
+            fms = sum(a.elapsed_time(b) for a, b in evf) / args.steps
+            hostf.set_timing(2)
+            hostf.layer(q, k, v, outf, self_sel_f, stream)
+            torch.cuda.synchronize()
+            ft = hostf.timing()
+            hostf.set_timing(False)
+            host.layer(q, k, v, out, self_sel, stream)  # exact selection on the same inputs
+            torch.cuda.synchronize()
+            a_ex, a_f = self_sel.cpu().numpy(), self_sel_f.cpu().numpy()
+            lp = g["l_p"]
+            common = sum(len(set(a_ex[r][:lp].tolist()) & set(a_f[r][:lp].tolist())) for r in range(2))
+            extra["fast_scoring"] = {
+                "tokens_per_s": g["n"] / (fms / 1e3), "ms_per_step": round(fms, 4),
+                "score_ms_per_step_isolated": round(ft["score_ms"], 4),
+                "index_agreement": round(common / (2 * lp), 6), "indices_differing": 2 * lp - common,
+                "note": "score_mode=1: tcgen05 logits + exp2 scorer; same layer otherwise; indices "
+                        "compared with the exact (bit-faithful) scorer on the same inputs"}
+            hostf.close()
+            fabf.close()
+        except Exception as e:  # pragma: no cover
+            extra["fast_scoring"] = {"error": str(e)[:200]}
         if not args.no_cpu:
             threads = os.cpu_count() or 1
             tps, layer_s, rate, desc, kind = reference_tokens_per_s(g, hq, hkv, threads, args.cpu_budget)

@@ -89,6 +89,15 @@ size_t spava_score_workspace(int n_t, int l_b, int hq);
 int spava_score_block(const void* q, int64_t ldq, int n_t, const void* k, int64_t ldk, int l_b,
                       const uint8_t* pad, int n_valid, int hq, int hkv, int dh, int softmax,
                       float* scores, void* workspace, size_t workspace_bytes, void* stream);
+/* Fast score_block on the tensor cores (score_fast.cu): same definition, logits from bf16
+ * tcgen05 MMAs with fp32 accumulation, softmax via exp2 -- NOT bit-faithful (the exact
+ * entry point above is); passing indices agree except where two scores tie within that
+ * error.  Softmax aggregation only; n_t <= 128, hkv <= 4, dh = 128.
+ * ws_bytes >= spava_score_fast_workspace(n_t, l_b, hq). */
+size_t spava_score_fast_workspace(int n_t, int l_b, int hq);
+int spava_score_block_fast(const void* q, int64_t ldq, int n_t, const void* k, int64_t ldk, int l_b,
+                           const uint8_t* pad, int n_valid, int hq, int hkv, int dh,
+                           float* scores, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------- select + pack
  * select_essential (approx.cpp:71-102): top-l_p by score, ties -> lower index,
@@ -155,6 +164,9 @@ typedef struct {
   int softmax_scores; /* SimOptions::softmax_scores                           */
   int hq, hkv, dh;
   int query_splits;   /* split-KV factor of query attention; 0 = auto         */
+  int score_mode;     /* 0 = exact (bit-faithful to score_block), 1 = fast:
+                         tcgen05 logits + exp2 (needs softmax_scores, n_t <= 128,
+                         hkv <= 4); indices agree except near-ties              */
 } spava_layer_cfg;
 
 typedef struct spava_fabric spava_fabric;

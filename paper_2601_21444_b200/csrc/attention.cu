@@ -1419,6 +1419,11 @@ bool make_tmap(CUtensorMap* m, const void* base, long long rows, long long cols,
 
 }  // namespace
 
+bool make_tmap_bf16(CUtensorMap* m, const void* base, long long rows, long long cols, long long ld,
+                    int box_rows, std::string* err) {
+  return make_tmap(m, base, rows, cols, ld, err, box_rows);
+}
+
 cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, int dh,
                              cudaStream_t stream, std::string* err) {
   if (dh != kHeadDim) {

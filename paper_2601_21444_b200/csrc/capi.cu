@@ -249,6 +249,9 @@ int cfg_check(const spava_layer_cfg* c, spava_plan* plan) {
     return fail(SPAVA_EINVAL,
                 "layer: degenerate plan (pad > l_b puts pad rows in a passing source block)");
   if (c->hosts > kMaxMergeParts) return fail(SPAVA_EINVAL, "layer: too many hosts");
+  if (c->score_mode != 0 && c->score_mode != 1) return fail(SPAVA_EINVAL, "layer: score_mode is 0 or 1");
+  if (c->score_mode == 1 && (!c->softmax_scores || c->n_t > 128 || c->hkv > 4))
+    return fail(SPAVA_EINVAL, "layer: fast scoring needs softmax_scores, n_t <= 128, hkv <= 4");
   return SPAVA_OK;
 }
 
@@ -317,11 +320,19 @@ int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record)
     const int nv[2] = {valid_rows(p, vs[0]), valid_rows(p, vs[1])};
     float* sc[2] = {H->scores[0], H->scores[1]};
     const size_t t0 = mark(H, st);
-    cudaError_t e = launch_score_exact2(2, row_ptr(b.q, qrow, dq), dq, p.n_t, ks, dk, p.l_b, nullptr,
-                                        nv, c.hq, c.hkv, c.dh, c.softmax_scores, sc, H->score_ws,
-                                        H->score_ws_bytes, st);
-    if (e != cudaSuccess) return fail(SPAVA_ECUDA, std::string("score: ") + cudaGetErrorString(e));
-    g_launches += c.softmax_scores ? 3 : 2;
+    if (c.score_mode == 1) {
+      std::string err;
+      cudaError_t e = launch_score_fast2(2, row_ptr(b.q, qrow, dq), dq, p.n_t, ks, dk, p.l_b, nullptr, nv,
+                                         c.hq, c.hkv, c.dh, sc, H->score_ws, H->score_ws_bytes, st, &err);
+      if (e != cudaSuccess) return fail(SPAVA_ECUDA, "score (fast): " + (err.empty() ? std::string(cudaGetErrorString(e)) : err));
+      g_launches += 3;
+    } else {
+      cudaError_t e = launch_score_exact2(2, row_ptr(b.q, qrow, dq), dq, p.n_t, ks, dk, p.l_b, nullptr,
+                                          nv, c.hq, c.hkv, c.dh, c.softmax_scores, sc, H->score_ws,
+                                          H->score_ws_bytes, st);
+      if (e != cudaSuccess) return fail(SPAVA_ECUDA, std::string("score: ") + cudaGetErrorString(e));
+      g_launches += c.softmax_scores ? 3 : 2;
+    }
     span(H, 1, t0, st);
   }
   for (int r = 0; r < 2; ++r) {
@@ -614,6 +625,28 @@ int spava_score_block(const void* q, int64_t ldq, int n_t, const void* k, int64_
   return SPAVA_OK;
 }
 
+size_t spava_score_fast_workspace(int n_t, int l_b, int hq) { return score_fast_workspace_bytes(n_t, l_b, hq); }
+
+int spava_score_block_fast(const void* q, int64_t ldq, int n_t, const void* k, int64_t ldk, int l_b,
+                           const uint8_t* pad, int n_valid, int hq, int hkv, int dh,
+                           float* scores, void* ws, size_t ws_bytes, void* stream) {
+  if (n_t < 1) return fail(SPAVA_EINVAL, "score_context: empty query");
+  if (ldq % 8 || ldk % 8) return fail(SPAVA_EINVAL, "score_block_fast: row strides must be multiples of 8");
+  ST_TRY(require_device());
+  const void* ks[1] = {k};
+  const uint8_t* pads[1] = {pad};
+  const int nv[1] = {n_valid};
+  float* sc[1] = {scores};
+  std::string err;
+  cudaError_t e = launch_score_fast2(1, q, ldq, n_t, ks, ldk, l_b, pad ? pads : nullptr, nv, hq, hkv, dh,
+                                     sc, ws, ws_bytes, as_stream(stream), &err);
+  if (e != cudaSuccess)
+    return fail(e == cudaErrorInvalidValue ? SPAVA_EINVAL : SPAVA_ECUDA,
+                "score_block_fast: " + (err.empty() ? std::string(cudaGetErrorString(e)) : err));
+  g_launches += 3;
+  return SPAVA_OK;
+}
+
 int spava_select_pack(const float* scores, int l_b, int l_p, int global_offset, const void* k,
                       const void* v, int64_t ld, int width, int32_t* idx_out, void* k_out,
                       void* v_out, int64_t ld_out, int32_t* count_out, int32_t* status_out,
@@ -807,7 +840,8 @@ int spava_host_create(spava_fabric* F, int h, spava_host** out) {
     H->ex = &F->shared;
   }
   const size_t dq = static_cast<size_t>(c.hq) * c.dh;
-  H->score_ws_bytes = score_workspace_bytes(p.n_t, p.l_b, c.hq);
+  H->score_ws_bytes = std::max(score_workspace_bytes(p.n_t, p.l_b, c.hq),
+                               score_fast_workspace_bytes(p.n_t, p.l_b, c.hq));
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   const size_t sc = al(static_cast<size_t>(p.l_b) * 4);
   const size_t qo = al(static_cast<size_t>(H->splits) * p.n_t * dq * 4);

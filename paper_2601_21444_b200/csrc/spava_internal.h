@@ -76,6 +76,10 @@ void attn_prof_read(unsigned long long* out16);  // dev: cycle counters of varia
 cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, int dh,
                              cudaStream_t stream, std::string* err);
 
+// 2D bf16 [rows x cols] tensor map, box 64 cols x box_rows rows, 128B swizzle
+bool make_tmap_bf16(CUtensorMap* m, const void* base, long long rows, long long cols, long long ld,
+                    int box_rows, std::string* err);
+
 // ---------------------------------------------------------------- scoring
 size_t score_workspace_bytes(int n_t, int l_b, int hq);  // sized for 2 blocks
 cudaError_t launch_score_exact2(int nblk, const void* q, long long ldq, int n_t,
@@ -87,6 +91,15 @@ cudaError_t launch_score_exact(const void* q, long long ldq, int n_t, const void
                                long long ldk, int l_b, const uint8_t* pad, int n_valid, int hq,
                                int hkv, int dh, int softmax, float* scores, void* ws,
                                size_t ws_bytes, cudaStream_t stream);
+
+// fast (tensor-core) scoring: same definition as score_block, logits from tcgen05 bf16
+// MMAs with fp32 accumulation (not bit-faithful; see score_fast.cu)
+size_t score_fast_workspace_bytes(int n_t, int l_b, int hq);  // sized for 2 blocks
+cudaError_t launch_score_fast2(int nblk, const void* q, long long ldq, int n_t,
+                               const void* const* k, long long ldk, int l_b,
+                               const uint8_t* const* pad, const int* n_valid, int hq, int hkv,
+                               int dh, float* const* scores, void* ws, size_t ws_bytes,
+                               cudaStream_t stream, std::string* err);
 
 // ---------------------------------------------------------------- selection
 cudaError_t launch_select_pack(const float* scores, int l_b, int l_p, int global_offset,

@@ -31,7 +31,8 @@ EXPORTED_SYMBOLS = [
     "spava_default_plan", "spava_virtual_pair", "spava_physical_of", "spava_slice_anchor",
     "spava_block_offset", "spava_query_offset", "spava_pad_mask", "spava_block_valid_rows",
     "spava_passing_ranges",
-    "spava_score_workspace", "spava_score_block", "spava_select_pack",
+    "spava_score_workspace", "spava_score_block", "spava_score_fast_workspace",
+    "spava_score_block_fast", "spava_select_pack",
     "spava_attention_workspace", "spava_attention", "spava_mha_merge",
     "spava_fabric_create_local", "spava_nccl_unique_id", "spava_fabric_create_nccl",
     "spava_fabric_destroy", "spava_host_create", "spava_host_destroy", "spava_host_plan",
@@ -65,13 +66,14 @@ class _Segment(C.Structure):
 class LayerConfig(C.Structure):
     _fields_ = [(n, C.c_int) for n in (
         "n_v", "n_t", "hosts", "l_a", "l_p", "zigzag", "designated", "query_self_all",
-        "softmax_scores", "hq", "hkv", "dh", "query_splits")]
+        "softmax_scores", "hq", "hkv", "dh", "query_splits", "score_mode")]
 
     @classmethod
     def make(cls, n_v, n_t, hosts, l_a, l_p, hq, hkv, dh=128, zigzag=True, designated=-1,
-             query_self_all=False, softmax_scores=True, query_splits=0):
+             query_self_all=False, softmax_scores=True, query_splits=0, score_mode=0):
+        """score_mode 0 = exact (bit-faithful scorer), 1 = fast (tensor-core scorer)."""
         return cls(n_v, n_t, hosts, l_a, l_p, int(zigzag), designated, int(query_self_all),
-                   int(softmax_scores), hq, hkv, dh, query_splits)
+                   int(softmax_scores), hq, hkv, dh, query_splits, int(score_mode))
 
 
 _lib = None
@@ -88,6 +90,11 @@ def lib():
         L.spava_version.restype = C.c_char_p
         L.spava_score_workspace.restype = C.c_size_t
         L.spava_score_workspace.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.spava_score_fast_workspace.restype = C.c_size_t
+        L.spava_score_fast_workspace.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.spava_score_block_fast.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64,
+                                             C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                             C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
         L.spava_attention_workspace.restype = C.c_size_t
         L.spava_attention_workspace.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
         L.spava_kernel_launches.restype = C.c_uint64
@@ -234,6 +241,26 @@ def score_block(q, k, hq, hkv, dh=128, pad=None, n_valid=None, softmax=True, str
     _check(lib().spava_score_block(_ptr(q), q.stride(0), n_t, _ptr(k), k.stride(0), l_b, _ptr(padt),
                                    l_b if n_valid is None else n_valid, hq, hkv, dh, int(softmax),
                                    _ptr(out), _ptr(ws), ws_bytes, _stream(stream)))
+    return out
+
+
+def score_block_fast(q, k, hq, hkv, dh=128, pad=None, n_valid=None, stream=None):
+    """score_block on the tensor cores (spava_score_block_fast): same definition, not
+    bit-faithful -- indices agree with the exact scorer except near-ties."""
+    import torch
+
+    _require(q, torch.bfloat16, "q")
+    _require(k, torch.bfloat16, "k")
+    n_t, l_b = q.shape[0], k.shape[0]
+    ws_bytes = lib().spava_score_fast_workspace(n_t, l_b, hq)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
+    out = torch.empty(l_b, dtype=torch.float32, device=q.device)
+    padt = None
+    if pad is not None:
+        padt = torch.as_tensor(np.asarray(pad, np.uint8)).to(q.device)
+    _check(lib().spava_score_block_fast(_ptr(q), q.stride(0), n_t, _ptr(k), k.stride(0), l_b, _ptr(padt),
+                                        l_b if n_valid is None else n_valid, hq, hkv, dh,
+                                        _ptr(out), _ptr(ws), ws_bytes, _stream(stream)))
     return out
 
 

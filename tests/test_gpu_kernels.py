@@ -57,6 +57,68 @@ def test_score_block_matches_oracle(cuda, n_t, l_b, hq, hkv, n_valid, softmax):
         assert np.array_equal(idx.cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("n_t,l_b,hq,hkv,n_valid", [
+    (128, 1000, 16, 2, 1000),
+    (128, 3000, 16, 2, 2950),   # padded tail, ragged last tile
+    (64, 777, 28, 4, 777),      # 7B head shape
+    (5, 130, 2, 1, 130),
+])
+def test_score_fast_close_to_exact(cuda, n_t, l_b, hq, hkv, n_valid):
+    """The tensor-core scorer: same definition, fp32-accumulated bf16 logits + exp2.  Scores
+    within 2e-3 relative of the reference's; top-l_p sets agree except at near-ties
+    (every mismatch sits at a relative score gap below 1e-3)."""
+    from paper_2601_21444_b200 import spava
+
+    rng = np.random.default_rng(n_t * 3 + l_b)
+    q = randn(rng, n_t, hq * 128)
+    k = randn(rng, l_b, hkv * 128)
+    pad = (np.arange(l_b) >= n_valid).astype(np.uint8)
+    ref = O.score_block(q, k, hq, hkv, 128, pad, True)
+    got = host(spava.score_block_fast(dev(q, cuda), dev(k, cuda), hq, hkv, 128, n_valid=n_valid))
+    assert np.array_equal(np.isinf(got), np.isinf(ref))
+    fin = np.isfinite(ref)
+    rel = np.abs(got[fin] - ref[fin]) / np.abs(ref[fin]).max()
+    assert rel.max() < 2e-3, rel.max()
+    for l_p in (1, max(1, n_valid // 8), n_valid // 2):
+        want = set(O.select_essential(ref, l_p, 0).tolist())
+        idx, _, _ = spava.select_essential(spava_t(got, cuda), l_p, 0)
+        have = set(idx.cpu().numpy().tolist())
+        for j in want ^ have:  # every disagreement is a near-tie at the boundary
+            kth = np.sort(ref[fin])[::-1][l_p - 1]
+            assert abs(ref[j] - kth) <= 1e-3 * abs(kth), (j, ref[j], kth)
+
+
+def test_layer_fast_scoring_agrees(cuda):
+    """Layer with score_mode=1: passing indices agree with the exact layer (>= 99 %) and
+    the block outputs stay within the bf16 tolerance of the exact layer's."""
+    import torch
+
+    from paper_2601_21444_b200 import spava
+
+    n_v, n_t, l_a, l_p, hq, hkv = 8000, 128, 128, 512, 16, 2
+    outs, sels = [], []
+    g = torch.Generator(device=cuda).manual_seed(3)
+    for mode in (0, 1):
+        cfg = spava.LayerConfig.make(n_v, n_t, 1, l_a, l_p, hq, hkv, score_mode=mode)
+        fab = spava.Fabric(cfg, 0)
+        host_ = fab.host(0)
+        if mode == 0:
+            rows = host_.rows
+            ins = [torch.randn(rows, w * 128, device=cuda, generator=g).to(torch.bfloat16) for w in (hq, hkv, hkv)]
+        o = torch.zeros(rows, hq * 128, dtype=torch.bfloat16, device=cuda)
+        s = torch.zeros(2, l_p, dtype=torch.int32, device=cuda)
+        host_.layer(*ins, o, s)
+        torch.cuda.synchronize()
+        assert host_.status() == 0
+        outs.append(o.float().cpu().numpy())
+        sels.append(s.cpu().numpy())
+        host_.close()
+        fab.close()
+    agree = np.mean([len(set(sels[0][r]) & set(sels[1][r])) / l_p for r in range(2)])
+    assert agree >= 0.99, agree
+    assert max_abs(outs[0], outs[1]) < ATOL_BF16_OUT
+
+
 def spava_t(x, device):
     import torch
 
