@@ -215,6 +215,24 @@ int spava_sim_layer_timed(spava_fabric* fab, spava_host* const* hosts, const voi
  * merge row invalid everywhere).  Synchronises the given stream.            */
 int spava_host_status(spava_host* host, void* stream, int32_t* status_out);
 
+/* Schedule trace in the reference Event schema (simhost.hpp:17-46): while enabled, every
+ * layer call records run_host's events (score, pass1/pass2/qpartial issue / wait-start /
+ * completed, query_attn, stage1, stage2, merge begin/end; simhost.cpp:322-426) in program
+ * order with the device time of the stream position each one marks (microseconds from a
+ * per-fabric origin).  Tags are "<round>.L<layer>" as in the reference.  The caller
+ * assigns seq and Lamport clocks across hosts and can run seqpar::validate_trace
+ * (simhost.cpp:567-657) on the result (tests/test_gpu_trace.py).                   */
+typedef struct {
+  int kind;        /* 0 CommIssued, 1 CommWaitStart, 2 CommCompleted, 3 ComputeBegin, 4 ComputeEnd */
+  int layer;
+  char label[16];
+  char tag[24];    /* "" for compute events */
+  double t_us;
+} spava_trace_event;
+int spava_host_set_trace(spava_host* host, int enable);  /* resets the record and layer count */
+/* out == NULL: *n = number of records; else copies (synchronising on the events). */
+int spava_host_trace_read(spava_host* host, spava_trace_event* out, int cap, int* n);
+
 /* Device timing of this host's launches, by kernel class (0 attention, 1 score,
  * 2 select+pack, 3 merge): CUDA events on the launching stream around every
  * launch while enabled (enable = 2 additionally runs the scorer on the caller's stream

@@ -164,6 +164,7 @@ struct spava_fabric {
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;
   Exchange shared;  // local mode
+  cudaEvent_t trace_base = nullptr;  // common time origin of the hosts' traces
 };
 
 struct spava_host {
@@ -193,6 +194,18 @@ struct spava_host {
   // launching stream around every launch; classes 0 attention, 1 score, 2 select, 3 merge
   bool timing = false;
   bool serial = false;  // timing mode 2: scoring on the caller's stream (isolated kernels)
+  // schedule trace in the reference Event schema (simhost.hpp:17-40): program-order records
+  // with a device timestamp each (cudaEvent on the stream the step runs on)
+  struct TraceRec {
+    int kind, layer;
+    char label[16];
+    char tag[24];
+    cudaEvent_t ev;
+  };
+  bool trace = false;
+  int trace_layer = 0;
+  std::vector<TraceRec> trace_recs;
+  std::vector<cudaEvent_t> trace_pool;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<std::pair<size_t, size_t>> spans[4];
@@ -223,6 +236,27 @@ void span(spava_host* H, int cls, size_t a, cudaStream_t st) {
   if (!H || !H->timing || a == SIZE_MAX) return;
   const size_t b = mark(H, st);
   H->spans[cls].push_back({a, b});
+}
+
+// kinds follow seqpar::EventKind (simhost.hpp:17)
+enum TraceKind { kCommIssued = 0, kCommWaitStart = 1, kCommCompleted = 2, kComputeBegin = 3, kComputeEnd = 4 };
+
+void trace_ev(spava_host* H, cudaStream_t st, int kind, const char* label, bool comm) {
+  if (!H || !H->trace) return;
+  spava_host::TraceRec r{};
+  r.kind = kind;
+  r.layer = H->trace_layer;
+  std::snprintf(r.label, sizeof(r.label), "%s", label);
+  if (comm) std::snprintf(r.tag, sizeof(r.tag), "%s.L%d", label, H->trace_layer);
+  const size_t i = H->trace_recs.size();
+  if (i == H->trace_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    H->trace_pool.push_back(e);
+  }
+  r.ev = H->trace_pool[i];
+  cudaEventRecord(r.ev, st);
+  H->trace_recs.push_back(r);
 }
 
 // reference FLOP convention (attention.cpp:33-36): 4*nq*nk*dh visible, 2*nq*nk*dh causal
@@ -314,6 +348,7 @@ int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record)
   const long long dq = static_cast<long long>(c.hq) * c.dh, dk = static_cast<long long>(c.hkv) * c.dh;
   const long long qrow = p.l_a + 2LL * p.l_b;
   const int vs[2] = {H->v_lo, H->v_hi};
+  trace_ev(H, st, kComputeBegin, "score", false);
   // both blocks (lo, hi) scored in one launch of each scoring kernel
   {
     const void* ks[2] = {row_ptr(b.k, p.l_a, dk), row_ptr(b.k, p.l_a + static_cast<long long>(p.l_b), dk)};
@@ -352,6 +387,7 @@ int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record)
       CU_TRY(cudaMemcpyAsync(b.sel + r * p.l_p, idx_out, sizeof(int32_t) * p.l_p,
                              cudaMemcpyDeviceToDevice, st));
     if (record) CU_TRY(cudaEventRecord(H->ev[r], st));
+    if (r == 1) trace_ev(H, st, kComputeEnd, "score", false);
   }
   return SPAVA_OK;
 }
@@ -808,6 +844,7 @@ int spava_fabric_destroy(spava_fabric* F) {
   if (!F) return SPAVA_OK;
   if (F->comm) ncclCommDestroy(F->comm);
   if (F->comm_stream) cudaStreamDestroy(F->comm_stream);
+  if (F->trace_base) cudaEventDestroy(F->trace_base);
   F->shared.release();
   delete F;
   return SPAVA_OK;
@@ -887,6 +924,7 @@ int spava_host_destroy(spava_host* H) {
   for (auto& e : H->ev_out)
     if (e) cudaEventDestroy(e);
   for (auto& e : H->ev_pool) cudaEventDestroy(e);
+  for (auto& e : H->trace_pool) cudaEventDestroy(e);
   H->own.release();
   if (H->base) cudaFree(H->base);
   delete H;
@@ -921,6 +959,10 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
   auto done = [&](cudaStream_t s, int i) -> cudaError_t {
     return cp.on ? cudaEventRecord(H->ev_out[i], s) : cudaSuccess;
   };
+  // trace records follow run_host's overlapped program order (simhost.cpp:343-426)
+  auto T = [&](cudaStream_t s, int kind, const char* label, bool comm = false) {
+    trace_ev(H, s, kind, label, comm);
+  };
   // fork: scoring + selection on the side stream (its inputs are this step's q/k on st)
   CU_TRY(cudaEventRecord(H->ev_fork, st));
   CU_TRY(cudaStreamWaitEvent(ss, H->ev_fork, 0));
@@ -930,42 +972,84 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     // H = 1: block lo (v = 0) has no passing segment, so only stage 2 waits for selection
     ST_TRY(phase_select(H, b, ss, false));
     CU_TRY(cudaEventRecord(H->ev_sel, ss));
+    T(ss, kCommIssued, "pass1", true);
+    T(ss, kCommIssued, "pass2", true);
+    T(st, kComputeBegin, "query_attn");
     ST_TRY(phase_query(H, b, st, false));
+    T(st, kComputeEnd, "query_attn");
+    T(st, kCommIssued, "qpartial", true);
+    T(st, kCommWaitStart, "pass1", true);
+    T(st, kCommCompleted, "pass1", true);
     CU_TRY(need(st, 1));
+    T(st, kComputeBegin, "stage1");
     ST_TRY(phase_stage1(H, b, st));
+    T(st, kComputeEnd, "stage1");
     CU_TRY(done(st, 0));
+    T(st, kCommWaitStart, "pass2", true);
     CU_TRY(cudaStreamWaitEvent(st, H->ev_sel, 0));
+    T(st, kCommCompleted, "pass2", true);
     CU_TRY(need(st, 2));
+    T(st, kComputeBegin, "stage2");
     ST_TRY(phase_stage2(H, b, st));
+    T(st, kComputeEnd, "stage2");
     CU_TRY(done(st, 1));
+    T(st, kCommWaitStart, "qpartial", true);
+    T(st, kCommCompleted, "qpartial", true);
+    T(st, kComputeBegin, "merge");
     ST_TRY(phase_merge(H, b, st));
+    T(st, kComputeEnd, "merge");
+    if (H->trace) ++H->trace_layer;
     return done(st, 2) == cudaSuccess ? SPAVA_OK : fail(SPAVA_ECUDA, "event record");
   }
   cudaStream_t cs = F->comm_stream;
   ST_TRY(phase_select(H, b, ss, true));  // records pass1_ready, pass2_ready on ss
   CU_TRY(cudaEventRecord(H->ev_sel, ss));
   CU_TRY(cudaStreamWaitEvent(cs, H->ev[0], 0));
+  T(cs, kCommIssued, "pass1", true);
   ST_TRY(nccl_round(F, H->ex, 0));
   CU_TRY(cudaEventRecord(H->ev[3], cs));
   CU_TRY(cudaStreamWaitEvent(cs, H->ev[1], 0));
+  T(cs, kCommIssued, "pass2", true);
   ST_TRY(nccl_round(F, H->ex, 1));
   CU_TRY(cudaEventRecord(H->ev[4], cs));
+  T(st, kComputeBegin, "query_attn");
   ST_TRY(phase_query(H, b, st, true));  // overlaps scoring and the pass rounds
+  T(st, kComputeEnd, "query_attn");
   CU_TRY(cudaStreamWaitEvent(cs, H->ev[2], 0));
+  T(cs, kCommIssued, "qpartial", true);
   ST_TRY(nccl_qround(F, H->ex));
   CU_TRY(cudaEventRecord(H->ev[5], cs));
+  T(st, kCommWaitStart, "pass1", true);
   CU_TRY(cudaStreamWaitEvent(st, H->ev[3], 0));
-  if (!F->plan.zigzag) CU_TRY(cudaStreamWaitEvent(st, H->ev[4], 0));  // simhost.cpp:392-402
+  T(st, kCommCompleted, "pass1", true);
+  if (!F->plan.zigzag) {  // simhost.cpp:392-402
+    T(st, kCommWaitStart, "pass2", true);
+    CU_TRY(cudaStreamWaitEvent(st, H->ev[4], 0));
+    T(st, kCommCompleted, "pass2", true);
+  }
   CU_TRY(need(st, 1));
+  T(st, kComputeBegin, "stage1");
   ST_TRY(phase_stage1(H, b, st));
+  T(st, kComputeEnd, "stage1");
   CU_TRY(done(st, 0));
-  CU_TRY(cudaStreamWaitEvent(st, H->ev[4], 0));
+  if (F->plan.zigzag) {
+    T(st, kCommWaitStart, "pass2", true);
+    CU_TRY(cudaStreamWaitEvent(st, H->ev[4], 0));
+    T(st, kCommCompleted, "pass2", true);
+  }
   CU_TRY(cudaStreamWaitEvent(st, H->ev_sel, 0));  // join the side stream (sel copy-out)
   CU_TRY(need(st, 2));
+  T(st, kComputeBegin, "stage2");
   ST_TRY(phase_stage2(H, b, st));
+  T(st, kComputeEnd, "stage2");
   CU_TRY(done(st, 1));
+  T(st, kCommWaitStart, "qpartial", true);
   CU_TRY(cudaStreamWaitEvent(st, H->ev[5], 0));
+  T(st, kCommCompleted, "qpartial", true);
+  T(st, kComputeBegin, "merge");
   ST_TRY(phase_merge(H, b, st));
+  T(st, kComputeEnd, "merge");
+  if (H->trace) ++H->trace_layer;
   return done(st, 2) == cudaSuccess ? SPAVA_OK : fail(SPAVA_ECUDA, "event record");
 }
 
@@ -1051,15 +1135,42 @@ int spava_sim_layer(spava_fabric* F, spava_host* const* hosts, const void* const
                     static_cast<const uint8_t*>(v[h]), static_cast<uint8_t*>(out[h]),
                     sel ? sel[h] : nullptr};
   }
-  // phase 1 on every host fills the shared exchange (the GatherFabric rounds)
+  // phase 1 on every host fills the shared exchange (the GatherFabric rounds); trace
+  // records keep each host's run_host program order (simhost.cpp:343-426)
   for (int h = 0; h < H; ++h) {
-    ST_TRY(phase_select(hosts[h], b[h], st, false));
-    ST_TRY(phase_query(hosts[h], b[h], st, false));
+    spava_host* X = hosts[h];
+    ST_TRY(phase_select(X, b[h], st, false));
+    trace_ev(X, st, kCommIssued, "pass1", true);
+    trace_ev(X, st, kCommIssued, "pass2", true);
+    trace_ev(X, st, kComputeBegin, "query_attn", false);
+    ST_TRY(phase_query(X, b[h], st, false));
+    trace_ev(X, st, kComputeEnd, "query_attn", false);
+    trace_ev(X, st, kCommIssued, "qpartial", true);
   }
   for (int h = 0; h < H; ++h) {
-    ST_TRY(phase_stage1(hosts[h], b[h], st));
-    ST_TRY(phase_stage2(hosts[h], b[h], st));
-    ST_TRY(phase_merge(hosts[h], b[h], st));
+    spava_host* X = hosts[h];
+    trace_ev(X, st, kCommWaitStart, "pass1", true);
+    trace_ev(X, st, kCommCompleted, "pass1", true);
+    if (!F->plan.zigzag) {
+      trace_ev(X, st, kCommWaitStart, "pass2", true);
+      trace_ev(X, st, kCommCompleted, "pass2", true);
+    }
+    trace_ev(X, st, kComputeBegin, "stage1", false);
+    ST_TRY(phase_stage1(X, b[h], st));
+    trace_ev(X, st, kComputeEnd, "stage1", false);
+    if (F->plan.zigzag) {
+      trace_ev(X, st, kCommWaitStart, "pass2", true);
+      trace_ev(X, st, kCommCompleted, "pass2", true);
+    }
+    trace_ev(X, st, kComputeBegin, "stage2", false);
+    ST_TRY(phase_stage2(X, b[h], st));
+    trace_ev(X, st, kComputeEnd, "stage2", false);
+    trace_ev(X, st, kCommWaitStart, "qpartial", true);
+    trace_ev(X, st, kCommCompleted, "qpartial", true);
+    trace_ev(X, st, kComputeBegin, "merge", false);
+    ST_TRY(phase_merge(X, b[h], st));
+    trace_ev(X, st, kComputeEnd, "merge", false);
+    if (X->trace) ++X->trace_layer;
   }
   return SPAVA_OK;
 }
@@ -1106,6 +1217,39 @@ int spava_sim_layer_timed(spava_fabric* F, spava_host* const* hosts, const void*
   }
   for (auto& e : ev) cudaEventDestroy(e);
   return rc;
+}
+
+int spava_host_set_trace(spava_host* H, int enable) {
+  if (!H) return fail(SPAVA_EINVAL, "set_trace: null host");
+  CU_TRY(cudaSetDevice(H->fab->device));
+  H->trace = enable != 0;
+  H->trace_layer = 0;
+  H->trace_recs.clear();
+  if (enable && !H->fab->trace_base) {
+    CU_TRY(cudaEventCreate(&H->fab->trace_base));
+    CU_TRY(cudaEventRecord(H->fab->trace_base, 0));
+  }
+  return SPAVA_OK;
+}
+
+int spava_host_trace_read(spava_host* H, spava_trace_event* out, int cap, int* n) {
+  if (!H || !n) return fail(SPAVA_EINVAL, "trace_read: null argument");
+  CU_TRY(cudaSetDevice(H->fab->device));
+  *n = static_cast<int>(H->trace_recs.size());
+  if (!out) return SPAVA_OK;
+  if (cap < *n) return fail(SPAVA_EINVAL, "trace_read: capacity too small");
+  for (int i = 0; i < *n; ++i) {
+    const auto& r = H->trace_recs[i];
+    CU_TRY(cudaEventSynchronize(r.ev));
+    float ms = 0.f;
+    CU_TRY(cudaEventElapsedTime(&ms, H->fab->trace_base, r.ev));
+    out[i].kind = r.kind;
+    out[i].layer = r.layer;
+    std::memcpy(out[i].label, r.label, sizeof(out[i].label));
+    std::memcpy(out[i].tag, r.tag, sizeof(out[i].tag));
+    out[i].t_us = 1e3 * static_cast<double>(ms);
+  }
+  return SPAVA_OK;
 }
 
 int spava_host_set_timing(spava_host* H, int enable) {

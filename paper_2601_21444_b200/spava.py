@@ -37,7 +37,7 @@ EXPORTED_SYMBOLS = [
     "spava_fabric_create_local", "spava_nccl_unique_id", "spava_fabric_create_nccl",
     "spava_fabric_destroy", "spava_host_create", "spava_host_destroy", "spava_host_plan",
     "spava_host_rows", "spava_host_layer", "spava_host_layer_hostbuf", "spava_sim_layer",
-    "spava_sim_layer_timed",
+    "spava_sim_layer_timed", "spava_host_set_trace", "spava_host_trace_read",
     "spava_host_status",
     "spava_host_set_timing", "spava_host_timing", "spava_kernel_launches",
     "spava_debug_attn_prof",
@@ -61,6 +61,57 @@ class Plan(C.Structure):
 class _Segment(C.Structure):
     _fields_ = [("k", C.c_void_p), ("v", C.c_void_p), ("ld", C.c_int64), ("rows", C.c_int),
                 ("causal", C.c_int)]
+
+
+class TraceEvent(C.Structure):
+    _fields_ = [("kind", C.c_int), ("layer", C.c_int), ("label", C.c_char * 16), ("tag", C.c_char * 24),
+                ("t_us", C.c_double)]
+
+
+# seqpar::EventKind names as written to JSONL (simhost.cpp:19-37)
+EVENT_KINDS = ("comm_issued", "comm_wait_start", "comm_completed", "compute_begin", "compute_end")
+
+
+def trace_events(records_per_host):
+    """Reference EventTrace (simhost.hpp:28-40) from per-host program-order records:
+    per-host seq, Lamport clocks as HostRecorder::record (simhost.cpp:168-179) with a
+    completion merging the max issuing clock of all contributors (GatherFabric::wait),
+    global order by (clock, host, seq) (simhost.cpp:549-560).  Each event keeps the device
+    timestamp as an extra 't_us' field (ignored by the reference reader)."""
+    issue_clock = {}
+    per_host = []
+    for h, recs in enumerate(records_per_host):
+        clock, evs = 0, []
+        for seq, (kind, label, layer, tag, t_us) in enumerate(recs):
+            evs.append(dict(host=h, seq=seq, kind=EVENT_KINDS[kind], label=label, layer=layer,
+                            tag=tag, t_us=round(t_us, 3)))
+        per_host.append(evs)
+    # a completion's clock depends on the other hosts' issue clocks, which (across layers)
+    # depend on earlier completions: iterate the per-host sweeps to the fixpoint
+    while True:
+        changed = False
+        for evs in per_host:
+            clock = 0
+            for e in evs:
+                merge = issue_clock.get(e["tag"], 0) if e["kind"] == "comm_completed" else 0
+                clock = max(clock, merge) + 1
+                e["clock"] = clock
+                if e["kind"] == "comm_issued" and issue_clock.get(e["tag"], 0) < clock:
+                    issue_clock[e["tag"]] = clock
+                    changed = True
+        if not changed:
+            break
+    events = sorted((e for evs in per_host for e in evs), key=lambda e: (e["clock"], e["host"], e["seq"]))
+    for i, e in enumerate(events):
+        e["global_index"] = i
+    return events
+
+
+def trace_jsonl(events):
+    import json
+
+    keys = ("global_index", "host", "seq", "kind", "label", "layer", "tag", "clock", "t_us")
+    return "".join(json.dumps({k: e[k] for k in keys}) + "\n" for e in events)
 
 
 class LayerConfig(C.Structure):
@@ -114,6 +165,8 @@ def lib():
         L.spava_host_layer_hostbuf.argtypes = [C.c_void_p] * 12
         L.spava_sim_layer.argtypes = [C.c_void_p] * 8
         L.spava_sim_layer_timed.argtypes = [C.c_void_p] * 9
+        L.spava_host_set_trace.argtypes = [C.c_void_p, C.c_int]
+        L.spava_host_trace_read.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
         L.spava_host_create.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
         L.spava_host_destroy.argtypes = [C.c_void_p]
         L.spava_host_rows.argtypes = [C.c_void_p]
@@ -407,6 +460,18 @@ class Host:
             self._p, C.c_void_p(q_h.data_ptr()), C.c_void_p(k_h.data_ptr()), C.c_void_p(v_h.data_ptr()),
             C.c_void_p(out_h.data_ptr()), C.c_void_p(sel_h.data_ptr()) if sel_h is not None else None,
             _ptr(q_d), _ptr(k_d), _ptr(v_d), _ptr(out_d), _ptr(sel_d), _stream(stream)))
+
+    def set_trace(self, enable=True):
+        """Record run_host's schedule events (reference Event schema) on every layer call."""
+        _check(lib().spava_host_set_trace(self._p, int(enable)))
+
+    def trace_records(self):
+        """Program-order records: [(kind, label, layer, tag, t_us)] (kind per EVENT_KINDS)."""
+        n = C.c_int()
+        _check(lib().spava_host_trace_read(self._p, None, 0, C.byref(n)))
+        buf = (TraceEvent * max(n.value, 1))()
+        _check(lib().spava_host_trace_read(self._p, buf, n.value, C.byref(n)))
+        return [(e.kind, e.label.decode(), e.layer, e.tag.decode(), e.t_us) for e in buf[:n.value]]
 
     def set_timing(self, enable=True):
         _check(lib().spava_host_set_timing(self._p, int(enable)))
