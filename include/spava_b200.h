@@ -80,6 +80,18 @@ int spava_block_valid_rows(const spava_plan* plan, int v);
 int spava_passing_ranges(const spava_plan* plan, int v, int* r0_begin, int* r0_end,
                          int* r1_begin, int* r1_end);
 
+/* split_context on the device (partition.cpp:40-85): gather host h's local rows
+ * [anchor | block lo | block hi | query] from the global sequence [E_v (n_v) | E_Q (n_t)]
+ * (src, row stride ld_src_bytes), pad rows zero-filled.  Any row width (row_bytes, a
+ * multiple of 16), so one call per Q / K / V tensor.  Rows: l_a + 2*l_b + n_t.          */
+int spava_split_rows(const spava_plan* plan, int h, const void* src, int64_t ld_src_bytes,
+                     void* dst, int64_t ld_dst_bytes, int row_bytes, void* stream);
+/* Inverse of spava_split_rows for outputs: host h's block rows (non-pad) to their global
+ * positions; with write_shared also the anchor and query rows (identical on every host:
+ * anchor_attention is replicated and the merged query is the same after mha_merge).    */
+int spava_merge_rows(const spava_plan* plan, int h, const void* src, int64_t ld_src_bytes,
+                     void* dst, int64_t ld_dst_bytes, int row_bytes, int write_shared, void* stream);
+
 /* --------------------------------------------------------------- scoring
  * score_block (simhost.cpp:209-224) -> score_context (approx.cpp:15-69),
  * softmax or raw-logit aggregation, "exact" arithmetic.

@@ -642,6 +642,36 @@ int spava_pad_mask(const spava_plan* p, int v, uint8_t* mask) {
   return SPAVA_OK;
 }
 
+int spava_split_rows(const spava_plan* p, int h, const void* src, int64_t ld_src_bytes, void* dst,
+                     int64_t ld_dst_bytes, int row_bytes, void* stream) {
+  if (!p || !src || !dst) return fail(SPAVA_EINVAL, "split_rows: null argument");
+  if (h < 0 || h >= p->hosts) return fail(SPAVA_ERANGE, "split_rows: host index");
+  int lo, hi;
+  ST_TRY(spava_virtual_pair(p, h, &lo, &hi));
+  ST_TRY(require_device());
+  cudaError_t e = launch_split_rows(p->l_a, p->l_b, p->n_t, p->n_v, lo, hi, src, ld_src_bytes, dst,
+                                    ld_dst_bytes, row_bytes, false, false, as_stream(stream));
+  if (e != cudaSuccess) return fail(e == cudaErrorInvalidValue ? SPAVA_EINVAL : SPAVA_ECUDA,
+                                    "split_rows: rows and strides must be 16-byte multiples");
+  ++g_launches;
+  return SPAVA_OK;
+}
+
+int spava_merge_rows(const spava_plan* p, int h, const void* src, int64_t ld_src_bytes, void* dst,
+                     int64_t ld_dst_bytes, int row_bytes, int write_shared, void* stream) {
+  if (!p || !src || !dst) return fail(SPAVA_EINVAL, "merge_rows: null argument");
+  if (h < 0 || h >= p->hosts) return fail(SPAVA_ERANGE, "merge_rows: host index");
+  int lo, hi;
+  ST_TRY(spava_virtual_pair(p, h, &lo, &hi));
+  ST_TRY(require_device());
+  cudaError_t e = launch_split_rows(p->l_a, p->l_b, p->n_t, p->n_v, lo, hi, src, ld_src_bytes, dst,
+                                    ld_dst_bytes, row_bytes, true, write_shared != 0, as_stream(stream));
+  if (e != cudaSuccess) return fail(e == cudaErrorInvalidValue ? SPAVA_EINVAL : SPAVA_ECUDA,
+                                    "merge_rows: rows and strides must be 16-byte multiples");
+  ++g_launches;
+  return SPAVA_OK;
+}
+
 size_t spava_score_workspace(int n_t, int l_b, int hq) { return score_workspace_bytes(n_t, l_b, hq); }
 
 int spava_score_block(const void* q, int64_t ldq, int n_t, const void* k, int64_t ldk, int l_b,

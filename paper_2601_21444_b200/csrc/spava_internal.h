@@ -107,6 +107,11 @@ cudaError_t launch_select_pack(const float* scores, int l_b, int l_p, int global
                                void* k_out, void* v_out, long long ld_out, int32_t* count,
                                int32_t* status, cudaStream_t stream);
 
+// ---------------------------------------------------------------- split_context rows
+cudaError_t launch_split_rows(int l_a, int l_b, int n_t, int n_v, int lo, int hi, const void* src,
+                              long long ld_src, void* dst, long long ld_dst, int row_bytes,
+                              bool merge, bool shared, cudaStream_t stream);
+
 // ---------------------------------------------------------------- merge
 constexpr int kMaxMergeParts = 64;
 struct MergeParams {

@@ -30,7 +30,7 @@ EXPORTED_SYMBOLS = [
     "spava_last_error", "spava_version", "spava_device_ok", "spava_make_plan",
     "spava_default_plan", "spava_virtual_pair", "spava_physical_of", "spava_slice_anchor",
     "spava_block_offset", "spava_query_offset", "spava_pad_mask", "spava_block_valid_rows",
-    "spava_passing_ranges",
+    "spava_passing_ranges", "spava_split_rows", "spava_merge_rows",
     "spava_score_workspace", "spava_score_block", "spava_score_fast_workspace",
     "spava_score_block_fast", "spava_select_pack",
     "spava_attention_workspace", "spava_attention", "spava_mha_merge",
@@ -166,6 +166,10 @@ def lib():
         L.spava_sim_layer.argtypes = [C.c_void_p] * 8
         L.spava_sim_layer_timed.argtypes = [C.c_void_p] * 9
         L.spava_host_set_trace.argtypes = [C.c_void_p, C.c_int]
+        L.spava_split_rows.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                       C.c_int, C.c_void_p]
+        L.spava_merge_rows.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                       C.c_int, C.c_int, C.c_void_p]
         L.spava_host_trace_read.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
         L.spava_host_create.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
         L.spava_host_destroy.argtypes = [C.c_void_p]
@@ -295,6 +299,27 @@ def score_block(q, k, hq, hkv, dh=128, pad=None, n_valid=None, softmax=True, str
                                    l_b if n_valid is None else n_valid, hq, hkv, dh, int(softmax),
                                    _ptr(out), _ptr(ws), ws_bytes, _stream(stream)))
     return out
+
+
+def split_rows(plan, h, src, dst=None, stream=None):
+    """split_context for host h on the device: global [n_v + n_t, w] -> host-local rows."""
+    import torch
+
+    rows = plan.l_a + 2 * plan.l_b + plan.n_t
+    if dst is None:
+        dst = torch.empty((rows, src.shape[1]), dtype=src.dtype, device=src.device)
+    es = src.element_size()
+    _check(lib().spava_split_rows(C.byref(plan), h, _ptr(src), src.stride(0) * es, _ptr(dst),
+                                  dst.stride(0) * es, src.shape[1] * es, _stream(stream)))
+    return dst
+
+
+def merge_rows(plan, h, src, dst, write_shared, stream=None):
+    """Host h's output rows back to the global sequence positions (inverse of split_rows)."""
+    es = src.element_size()
+    _check(lib().spava_merge_rows(C.byref(plan), h, _ptr(src), src.stride(0) * es, _ptr(dst),
+                                  dst.stride(0) * es, src.shape[1] * es, int(write_shared), _stream(stream)))
+    return dst
 
 
 def score_block_fast(q, k, hq, hkv, dh=128, pad=None, n_valid=None, stream=None):
