@@ -294,3 +294,37 @@ def test_merge_matches_oracle(cuda):
                                     hq, 128, out_f32=True, want_lse=True)
     assert int(st.item()) == 0
     assert max_abs(host(got), ref) <= 2e-6 * max(1.0, float(np.abs(ref).max()))
+
+
+@pytest.mark.parametrize("fast", [False, True])
+def test_needle_keys_are_selected(cuda, fast):
+    """Selectivity (the needle of simhost.cpp:228-255 at the attention level): keys of one
+    'frame' planted along each kv-head's mean query direction, alternating sign, distinct
+    amplitudes, are all among the selected passing rows, and the selection equals the
+    oracle's (exact scorer)."""
+    import torch
+
+    from paper_2601_21444_b200 import spava
+
+    n_t, l_b, hq, hkv, frame, r0 = 64, 2000, 8, 2, 48, 900
+    rng = np.random.default_rng(17)
+    q = bf16(rng.standard_normal((n_t, hq * 128)).astype(np.float32))
+    k = bf16(rng.standard_normal((l_b, hkv * 128)).astype(np.float32))
+    g = hq // hkv
+    for hk in range(hkv):
+        d = q[:, hk * g * 128:(hk + 1) * g * 128].reshape(n_t, g, 128).sum(axis=(0, 1))
+        d /= np.linalg.norm(d)
+        for r in range(frame):
+            amp = 60.0 * (1 + r / frame) * (1 if r % 2 == 0 else -1)
+            k[r0 + r, hk * 128:(hk + 1) * 128] = amp * d
+    k = bf16(k)
+    l_p = 2 * frame
+    fn = spava.score_block_fast if fast else spava.score_block
+    s = fn(dev(q, cuda), dev(k, cuda), hq, hkv, 128)
+    idx, _, _ = spava.select_essential(s, l_p, 0)
+    idx = set(idx.cpu().numpy().tolist())
+    planted_pos = {r0 + r for r in range(0, frame, 2)}  # positive alignment
+    assert planted_pos <= idx
+    if not fast:
+        ref = O.score_block(q, k, hq, hkv, 128, None, True)
+        assert idx == set(O.select_essential(ref, l_p, 0).tolist())
