@@ -188,8 +188,13 @@ struct spava_host {
   cudaEvent_t ev_fork = nullptr, ev_sel = nullptr;
   // host-buffer layer (spava_host_layer_hostbuf): H2D / D2H copy streams and their edges
   cudaStream_t h2d = nullptr, d2h = nullptr;
-  cudaEvent_t ev_in[3] = {};   // k/v + query rows, anchor + lo rows of q, hi rows of q
-  cudaEvent_t ev_out[4] = {};  // stage1 done, stage2 done, merge done, d2h done
+  // row-chunk pipeline: q rows of block lo / hi arrive in kCopyChunks chunks each; the
+  // stage-1/2 attention runs per chunk and each chunk's output leaves as soon as it is final
+  static constexpr int kCopyChunks = 4;
+  cudaEvent_t ev_kvq = nullptr;                  // k, v and the query rows of q are on device
+  cudaEvent_t ev_qc[2 * kCopyChunks] = {};       // q rows of chunk c (chunk 0 of lo + anchor)
+  cudaEvent_t ev_oc[2 * kCopyChunks + 1] = {};   // output chunk c final (last: merged query)
+  cudaEvent_t ev_d2h = nullptr;
   // optional per-kernel-class device timing (bench roofline): CUDA events recorded on the
   // launching stream around every launch; classes 0 attention, 1 score, 2 select, 3 merge
   bool timing = false;
@@ -487,6 +492,27 @@ ProbView block_problem(spava_host* H, const HostBufs& b, int which) {
   return pv;
 }
 
+// rows [r0, r1) of block `which` as its own problem: the block's causal segment splits into
+// keys [0, r0) (visible to every row of the chunk) and a causal segment starting at r0
+ProbView block_chunk_problem(spava_host* H, const HostBufs& b, int which, int r0, int r1) {
+  ProbView pv = block_problem(H, b, which);
+  const spava_layer_cfg& c = H->fab->cfg;
+  const long long dq = static_cast<long long>(c.hq) * c.dh, dk = static_cast<long long>(c.hkv) * c.dh;
+  SegView own = pv.seg[pv.nseg - 1];  // the causal own segment, len = valid rows
+  --pv.nseg;
+  const int nv = own.len;
+  const int pre = std::min(r0, nv);
+  if (pre > 0) pv.seg[pv.nseg++] = SegView{own.k, own.v, own.ld, pre, 0};
+  const int clen = std::min(r1, nv) - r0;
+  if (clen > 0)
+    pv.seg[pv.nseg++] = SegView{row_ptr(static_cast<const uint8_t*>(own.k), r0, dk),
+                                row_ptr(static_cast<const uint8_t*>(own.v), r0, dk), own.ld, clen, 1};
+  pv.q = row_ptr(static_cast<const uint8_t*>(pv.q), r0, dq);
+  pv.nq = r1 - r0;
+  pv.out = static_cast<uint8_t*>(pv.out) + static_cast<long long>(r0) * dq * 2;
+  return pv;
+}
+
 ProbView anchor_problem(spava_host* H, const HostBufs& b) {
   const spava_layer_cfg& c = H->fab->cfg;
   const spava_plan& p = H->fab->plan;
@@ -736,7 +762,7 @@ size_t spava_attention_workspace(int nq, int hq, int dh, int splits) {
 int spava_attention(const void* q, int64_t ldq, int nq, const spava_segment* segs, int nseg,
                     int hq, int hkv, int dh, void* out, int64_t ldo, int out_f32, float* lse,
                     int splits, void* ws, size_t ws_bytes, void* stream) {
-  if (nseg < 0 || nseg > kMaxSegs) return fail(SPAVA_EINVAL, "attention: at most 4 key segments");
+  if (nseg < 0 || nseg > kMaxSegs) return fail(SPAVA_EINVAL, "attention: at most 5 key segments");
   if (splits < 1) splits = 1;
   if (splits > kMaxMergeParts) return fail(SPAVA_EINVAL, "attention: too many splits");
   for (int s = 0; s < nseg; ++s)
@@ -934,8 +960,10 @@ int spava_host_create(spava_fabric* F, int h, spava_host** out) {
   CU_TRY(cudaStreamCreateWithPriority(&H->side, cudaStreamNonBlocking, prio_hi));
   CU_TRY(cudaStreamCreateWithFlags(&H->h2d, cudaStreamNonBlocking));
   CU_TRY(cudaStreamCreateWithFlags(&H->d2h, cudaStreamNonBlocking));
-  for (auto& e : H->ev_in) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  for (auto& e : H->ev_out) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CU_TRY(cudaEventCreateWithFlags(&H->ev_kvq, cudaEventDisableTiming));
+  CU_TRY(cudaEventCreateWithFlags(&H->ev_d2h, cudaEventDisableTiming));
+  for (auto& e : H->ev_qc) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : H->ev_oc) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   *out = H;
   return SPAVA_OK;
 }
@@ -949,10 +977,12 @@ int spava_host_destroy(spava_host* H) {
   if (H->side) cudaStreamDestroy(H->side);
   if (H->h2d) cudaStreamDestroy(H->h2d);
   if (H->d2h) cudaStreamDestroy(H->d2h);
-  for (auto& e : H->ev_in)
+  for (auto& e : H->ev_qc)
     if (e) cudaEventDestroy(e);
-  for (auto& e : H->ev_out)
+  for (auto& e : H->ev_oc)
     if (e) cudaEventDestroy(e);
+  if (H->ev_kvq) cudaEventDestroy(H->ev_kvq);
+  if (H->ev_d2h) cudaEventDestroy(H->ev_d2h);
   for (auto& e : H->ev_pool) cudaEventDestroy(e);
   for (auto& e : H->trace_pool) cudaEventDestroy(e);
   H->own.release();
@@ -978,16 +1008,50 @@ namespace {
 // phases still run (ev_out).  Inputs arrive in the order the phases need them.
 struct CopyEdges {
   bool on = false;
+  int cb[spava_host::kCopyChunks + 1] = {};  // row bounds of the block chunks
 };
+
+CopyEdges copy_edges(const spava_plan& p) {
+  CopyEdges cp;
+  cp.on = true;
+  const int n = spava_host::kCopyChunks;
+  for (int c = 0; c <= n; ++c) {  // multiples of 256 rows (one ping-pong CTA unit)
+    const long long r = (static_cast<long long>(p.l_b) * c / n + 255) / 256 * 256;
+    cp.cb[c] = static_cast<int>(std::min<long long>(r, p.l_b));
+  }
+  cp.cb[n] = p.l_b;
+  return cp;
+}
+
+// stage 1 / stage 2 as row chunks (copy pipeline) or whole blocks
+int stage_chunks(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdges& cp, int which) {
+  if (!cp.on) return which == 0 ? phase_stage1(H, b, st) : phase_stage2(H, b, st);
+  const spava_layer_cfg& c = H->fab->cfg;
+  const int n = spava_host::kCopyChunks;
+  for (int k = 0; k < n; ++k) {
+    const int idx = which * n + k;
+    CU_TRY(cudaStreamWaitEvent(st, H->ev_qc[idx], 0));
+    if (cp.cb[k + 1] > cp.cb[k]) {
+      ProbView pv[2] = {block_chunk_problem(H, b, which, cp.cb[k], cp.cb[k + 1]), anchor_problem(H, b)};
+      const int np = (which == 0 && k == 0 && H->fab->plan.l_a > 0) ? 2 : 1;  // anchor with lo chunk 0
+      ST_TRY(attention_impl(pv, np, c.hq, c.hkv, c.dh, st, H));
+    } else if (which == 0 && k == 0 && H->fab->plan.l_a > 0) {
+      ProbView pa = anchor_problem(H, b);
+      ST_TRY(attention_impl(&pa, 1, c.hq, c.hkv, c.dh, st, H));
+    }
+    CU_TRY(cudaEventRecord(H->ev_oc[idx], st));
+  }
+  return SPAVA_OK;
+}
 
 int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdges& cp) {
   spava_fabric* F = H->fab;
   cudaStream_t ss = H->serial ? st : H->side;
-  auto need = [&](cudaStream_t s, int i) -> cudaError_t {
-    return cp.on ? cudaStreamWaitEvent(s, H->ev_in[i], 0) : cudaSuccess;
+  auto need_kvq = [&](cudaStream_t s) -> cudaError_t {
+    return cp.on ? cudaStreamWaitEvent(s, H->ev_kvq, 0) : cudaSuccess;
   };
-  auto done = [&](cudaStream_t s, int i) -> cudaError_t {
-    return cp.on ? cudaEventRecord(H->ev_out[i], s) : cudaSuccess;
+  auto merged = [&](cudaStream_t s) -> cudaError_t {
+    return cp.on ? cudaEventRecord(H->ev_oc[2 * spava_host::kCopyChunks], s) : cudaSuccess;
   };
   // trace records follow run_host's overlapped program order (simhost.cpp:343-426)
   auto T = [&](cudaStream_t s, int kind, const char* label, bool comm = false) {
@@ -996,8 +1060,8 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
   // fork: scoring + selection on the side stream (its inputs are this step's q/k on st)
   CU_TRY(cudaEventRecord(H->ev_fork, st));
   CU_TRY(cudaStreamWaitEvent(ss, H->ev_fork, 0));
-  CU_TRY(need(ss, 0));
-  CU_TRY(need(st, 0));
+  CU_TRY(need_kvq(ss));
+  CU_TRY(need_kvq(st));
   if (!F->nccl) {
     // H = 1: block lo (v = 0) has no passing segment, so only stage 2 waits for selection
     ST_TRY(phase_select(H, b, ss, false));
@@ -1010,26 +1074,22 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     T(st, kCommIssued, "qpartial", true);
     T(st, kCommWaitStart, "pass1", true);
     T(st, kCommCompleted, "pass1", true);
-    CU_TRY(need(st, 1));
     T(st, kComputeBegin, "stage1");
-    ST_TRY(phase_stage1(H, b, st));
+    ST_TRY(stage_chunks(H, b, st, cp, 0));
     T(st, kComputeEnd, "stage1");
-    CU_TRY(done(st, 0));
     T(st, kCommWaitStart, "pass2", true);
     CU_TRY(cudaStreamWaitEvent(st, H->ev_sel, 0));
     T(st, kCommCompleted, "pass2", true);
-    CU_TRY(need(st, 2));
     T(st, kComputeBegin, "stage2");
-    ST_TRY(phase_stage2(H, b, st));
+    ST_TRY(stage_chunks(H, b, st, cp, 1));
     T(st, kComputeEnd, "stage2");
-    CU_TRY(done(st, 1));
     T(st, kCommWaitStart, "qpartial", true);
     T(st, kCommCompleted, "qpartial", true);
     T(st, kComputeBegin, "merge");
     ST_TRY(phase_merge(H, b, st));
     T(st, kComputeEnd, "merge");
     if (H->trace) ++H->trace_layer;
-    return done(st, 2) == cudaSuccess ? SPAVA_OK : fail(SPAVA_ECUDA, "event record");
+    return merged(st) == cudaSuccess ? SPAVA_OK : fail(SPAVA_ECUDA, "event record");
   }
   cudaStream_t cs = F->comm_stream;
   ST_TRY(phase_select(H, b, ss, true));  // records pass1_ready, pass2_ready on ss
@@ -1057,22 +1117,18 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     CU_TRY(cudaStreamWaitEvent(st, H->ev[4], 0));
     T(st, kCommCompleted, "pass2", true);
   }
-  CU_TRY(need(st, 1));
   T(st, kComputeBegin, "stage1");
-  ST_TRY(phase_stage1(H, b, st));
+  ST_TRY(stage_chunks(H, b, st, cp, 0));
   T(st, kComputeEnd, "stage1");
-  CU_TRY(done(st, 0));
   if (F->plan.zigzag) {
     T(st, kCommWaitStart, "pass2", true);
     CU_TRY(cudaStreamWaitEvent(st, H->ev[4], 0));
     T(st, kCommCompleted, "pass2", true);
   }
   CU_TRY(cudaStreamWaitEvent(st, H->ev_sel, 0));  // join the side stream (sel copy-out)
-  CU_TRY(need(st, 2));
   T(st, kComputeBegin, "stage2");
-  ST_TRY(phase_stage2(H, b, st));
+  ST_TRY(stage_chunks(H, b, st, cp, 1));
   T(st, kComputeEnd, "stage2");
-  CU_TRY(done(st, 1));
   T(st, kCommWaitStart, "qpartial", true);
   CU_TRY(cudaStreamWaitEvent(st, H->ev[5], 0));
   T(st, kCommCompleted, "qpartial", true);
@@ -1080,7 +1136,7 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
   ST_TRY(phase_merge(H, b, st));
   T(st, kComputeEnd, "merge");
   if (H->trace) ++H->trace_layer;
-  return done(st, 2) == cudaSuccess ? SPAVA_OK : fail(SPAVA_ECUDA, "event record");
+  return merged(st) == cudaSuccess ? SPAVA_OK : fail(SPAVA_ECUDA, "event record");
 }
 
 }  // namespace
@@ -1118,35 +1174,46 @@ int spava_host_layer_hostbuf(spava_host* H, const void* q_h, const void* k_h, co
   cudaStream_t hs = H->h2d, ds = H->d2h;
   // inputs, in the order the phases consume them (the previous step's work on st is done
   // before the buffers are overwritten: h2d waits for the fork point of this step)
+  const CopyEdges cp = copy_edges(p);
+  const int nc = spava_host::kCopyChunks;
   CU_TRY(cudaEventRecord(H->ev_fork, st));
   CU_TRY(cudaStreamWaitEvent(hs, H->ev_fork, 0));
   CU_TRY(cudaMemcpyAsync(k_d, k_h, rows * rk, cudaMemcpyHostToDevice, hs));
   CU_TRY(cudaMemcpyAsync(v_d, v_h, rows * rk, cudaMemcpyHostToDevice, hs));
   CU_TRY(cudaMemcpyAsync(qd + qrow * rq, qh + qrow * rq, static_cast<size_t>(p.n_t) * rq, cudaMemcpyHostToDevice, hs));
-  CU_TRY(cudaEventRecord(H->ev_in[0], hs));
-  CU_TRY(cudaMemcpyAsync(qd, qh, lo_end * rq, cudaMemcpyHostToDevice, hs));
-  CU_TRY(cudaEventRecord(H->ev_in[1], hs));
-  CU_TRY(cudaMemcpyAsync(qd + lo_end * rq, qh + lo_end * rq, static_cast<size_t>(p.l_b) * rq,
-                         cudaMemcpyHostToDevice, hs));
-  CU_TRY(cudaEventRecord(H->ev_in[2], hs));
+  CU_TRY(cudaEventRecord(H->ev_kvq, hs));
+  // q chunk rows (chunk 0 of block lo also carries the anchor rows)
+  auto chunk_rows = [&](int idx, size_t* r0, size_t* r1) {
+    const int which = idx / nc, k = idx % nc;
+    const size_t base = static_cast<size_t>(p.l_a) + static_cast<size_t>(which) * p.l_b;
+    *r0 = (which == 0 && k == 0) ? 0 : base + cp.cb[k];
+    *r1 = base + cp.cb[k + 1];
+  };
+  for (int idx = 0; idx < 2 * nc; ++idx) {
+    size_t r0, r1;
+    chunk_rows(idx, &r0, &r1);
+    if (r1 > r0)
+      CU_TRY(cudaMemcpyAsync(qd + r0 * rq, qh + r0 * rq, (r1 - r0) * rq, cudaMemcpyHostToDevice, hs));
+    CU_TRY(cudaEventRecord(H->ev_qc[idx], hs));
+  }
   HostBufs b{static_cast<const uint8_t*>(q_d), static_cast<const uint8_t*>(k_d),
              static_cast<const uint8_t*>(v_d), od, sel_d};
-  CopyEdges cp;
-  cp.on = true;
   ST_TRY(layer_impl(H, b, st, cp));
-  // outputs as soon as each row range is final
-  CU_TRY(cudaStreamWaitEvent(ds, H->ev_out[0], 0));
-  CU_TRY(cudaMemcpyAsync(oh, od, lo_end * rq, cudaMemcpyDeviceToHost, ds));
-  CU_TRY(cudaStreamWaitEvent(ds, H->ev_out[1], 0));
-  CU_TRY(cudaMemcpyAsync(oh + lo_end * rq, od + lo_end * rq, static_cast<size_t>(p.l_b) * rq,
-                         cudaMemcpyDeviceToHost, ds));
-  CU_TRY(cudaStreamWaitEvent(ds, H->ev_out[2], 0));
+  // outputs as soon as each row chunk is final
+  for (int idx = 0; idx < 2 * nc; ++idx) {
+    size_t r0, r1;
+    chunk_rows(idx, &r0, &r1);
+    CU_TRY(cudaStreamWaitEvent(ds, H->ev_oc[idx], 0));
+    if (r1 > r0)
+      CU_TRY(cudaMemcpyAsync(oh + r0 * rq, od + r0 * rq, (r1 - r0) * rq, cudaMemcpyDeviceToHost, ds));
+  }
+  CU_TRY(cudaStreamWaitEvent(ds, H->ev_oc[2 * nc], 0));
   CU_TRY(cudaMemcpyAsync(oh + qrow * rq, od + qrow * rq, static_cast<size_t>(p.n_t) * rq,
                          cudaMemcpyDeviceToHost, ds));
   if (sel_h && sel_d && p.l_p > 0)
     CU_TRY(cudaMemcpyAsync(sel_h, sel_d, 2ull * p.l_p * sizeof(int32_t), cudaMemcpyDeviceToHost, ds));
-  CU_TRY(cudaEventRecord(H->ev_out[3], ds));
-  CU_TRY(cudaStreamWaitEvent(st, H->ev_out[3], 0));  // the caller's stream covers the copies
+  CU_TRY(cudaEventRecord(H->ev_d2h, ds));
+  CU_TRY(cudaStreamWaitEvent(st, H->ev_d2h, 0));  // the caller's stream covers the copies
   return SPAVA_OK;
 }
 

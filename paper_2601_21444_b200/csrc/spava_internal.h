@@ -14,7 +14,8 @@ constexpr int kHeadDim = 128;       // dh (Qwen2.5-VL 3B/7B)
 constexpr int kBlockM = 128;        // query rows per Q tile (TMEM lanes)
 constexpr int kBlockN = 128;        // keys per KV tile
 constexpr int kTilesPerCta = 2;     // two Q tiles share every K/V tile (ping-pong softmax)
-constexpr int kMaxSegs = 4;         // [anchor | passing lo-round | passing hi-round | own]
+constexpr int kMaxSegs = 5;         // [anchor | passing lo-round | passing hi-round | own]
+                                     // (+1: a row chunk splits own into visible prefix + causal)
 constexpr int kMaxProbs = 3;        // attention problems fused into one launch
 
 struct AttnSeg {
