@@ -14,6 +14,29 @@ host_list = [int(x) for x in sys.argv[2:]] or [1, 2, 4, 8]
 cfg = bench.CONFIGS[cfg_name]
 dev = torch.device("cuda:0")
 hq, hkv = cfg["hq"], cfg["hkv"]
+
+# dense exact causal attention over the whole sequence on ONE GPU (our kernel), the
+# comparator of BASELINE.json's configs
+n = cfg["n"]
+gen = torch.Generator(device=dev).manual_seed(3)
+qd = torch.randn(n, hq * 128, device=dev, generator=gen).to(torch.bfloat16)
+kd = torch.randn(n, hkv * 128, device=dev, generator=gen).to(torch.bfloat16)
+vd = torch.randn(n, hkv * 128, device=dev, generator=gen).to(torch.bfloat16)
+for _ in range(2):
+    spava.attention(qd, [dict(k=kd, v=vd, causal=True)], hq, hkv)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(3):
+    spava.attention(qd, [dict(k=kd, v=vd, causal=True)], hq, hkv)
+e1.record()
+torch.cuda.synchronize()
+dense_ms = e0.elapsed_time(e1) / 3
+dense_fl = 2.0 * n * n * hq * 128
+print(json.dumps({"config": cfg_name, "n": n, "dense_exact_1gpu_ms": round(dense_ms, 3),
+                  "dense_tflops": round(dense_fl / (dense_ms / 1e3) / 1e12, 1),
+                  "dense_tokens_per_s": round(n / (dense_ms / 1e3))}), flush=True)
+del qd, kd, vd
+torch.cuda.empty_cache()
 for H in host_list:
     for zz in ((True, False) if H > 1 else (True,)):
         g = bench.geometry(cfg, H, zz)
@@ -37,6 +60,7 @@ for H in host_list:
                           "max_over_min": round(mx / min(ms), 3),
                           "flops_max_over_min": round(max(fl) / min(fl), 3),
                           "projected_tokens_per_s_excl_comm": round(g["n"] / (mx / 1e3)),
+                          "speedup_vs_dense_1gpu": round(dense_ms / mx, 2),
                           "attn_tflops_per_s_on_max_host": round(fl[ms.index(mx)] / (mx / 1e3) / 1e12, 1)}),
               flush=True)
         for h in hosts:
