@@ -276,7 +276,7 @@ def run_reference_arm(args):
         "n_gpus": max(world, args.gpus), "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": g["n"] / value * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic N(0,1)",
-        "config": {"workload": f"{args.config}: {cfg['desc']}", "model": cfg["model"], "n": g["n"],
+        "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g["n"],
                    "n_t": g["n_t"], "l_a": g["l_a"], "l_b": g["l_b"], "l_p": g["l_p"],
                    "hosts": g["hosts"], "parallelism": f"sp{g['hosts']} (simulated hosts on CPU)"},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": kind,
@@ -541,7 +541,7 @@ def run_spava_arm(args):
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic N(0,1) bf16 activations",
-        "config": {"workload": f"{args.config}: {cfg['desc']}", "model": cfg["model"], "n": g["n"],
+        "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g["n"],
                    "n_t": g["n_t"], "l_a": g["l_a"], "l_b": g["l_b"], "l_p": g["l_p"],
                    "hosts": H, "heads": f"{hq}q/{hkv}kv", "dh": DH, "layers_per_step": 1,
                    "parallelism": f"sp{H} (Spava zigzag virtual hosts, one per GPU)",

@@ -43,7 +43,9 @@ BODY(k_ddiv, double, threadIdx.x * 1e-3 + i + 1.0, a[i] = 1.0 / a[i] + 0.5,
      (unsigned long long)__double_as_longlong(a[i]))
 
 typedef void (*K)(unsigned long long*, int);
+int main2();
 int main() {
+  main2();
   unsigned long long* o;
   cudaMalloc(&o, 148 * 4 * 1024 * 8);
   cudaEvent_t e0, e1;
@@ -67,5 +69,25 @@ int main() {
     double ops = (double)blocks * thr * iters * 8 * k.per;
     printf("%-28s %8.1f /clk/SM (at 1.965 GHz)\n", k.n, ops / (ms * 1e-3) / 148 / 1.965e9);
   }
+  return 0;
+}
+// (appended) f16x2 ex2: one MUFU op for two halves?
+BODY(k_ex2f16x2, unsigned, 0x3c003c00u + threadIdx.x + i,
+     asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(a[i])), a[i])
+int main2() {
+  unsigned long long* o;
+  cudaMalloc(&o, 148 * 4 * 1024 * 8);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int blocks = 148 * 4, thr = 256, iters = 2048;
+  float ms;
+  k_ex2f16x2<<<blocks, thr>>>(o, 8);
+  cudaEventRecord(e0);
+  k_ex2f16x2<<<blocks, thr>>>(o, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("ex2.approx.f16x2 (exps)        %8.1f /clk/SM\n", (double)blocks * thr * iters * 16 / (ms * 1e-3) / 148 / 1.965e9);
   return 0;
 }
