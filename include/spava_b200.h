@@ -260,6 +260,9 @@ int spava_host_timing(spava_host* host, double* ms_by_class4, double* attn_flops
 /* Development: read-and-reset the cycle counters of the instrumented attention
  * variant (SPAVA_ATTN_VARIANT=5): 16 uint64 (see attention.cu).            */
 int spava_debug_attn_prof(uint64_t* out16);
+/* Development: force an attention kernel variant for this process (-1 = default or the
+ * SPAVA_ATTN_VARIANT environment variable); lets the tests cover every variant.        */
+int spava_debug_attn_variant(int variant);
 
 /* Number of kernels the library launched since process start (for bench's
  * gpu_launches claim). */

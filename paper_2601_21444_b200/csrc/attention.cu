@@ -27,6 +27,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -1424,6 +1425,8 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, long long rows, long long 
   return make_tmap(m, base, rows, cols, ld, err, box_rows);
 }
 
+std::atomic<int> g_attn_variant{-1};  // -1: SPAVA_ATTN_VARIANT / default
+
 cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, int dh,
                              cudaStream_t stream, std::string* err) {
   if (dh != kHeadDim) {
@@ -1458,11 +1461,13 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
       {attn_fwd2_kernel<2>, Smem2::bytes, kThreads, 2},                   // 8 7 + 25% FMA exp2
       {attn_fwd2_kernel<1>, Smem2::bytes, kThreads, 2}};                  // 9 7 + 12.5% FMA exp2
   constexpr int kNumVar = sizeof(variants) / sizeof(variants[0]);
-  static int vsel = [] {
+  static const int env_sel = [] {
     const char* e = getenv("SPAVA_ATTN_VARIANT");
     const int v = e ? atoi(e) : 0;
     return (v >= 0 && v < kNumVar) ? v : 0;
   }();
+  const int forced = g_attn_variant.load();
+  const int vsel = (forced >= 0 && forced < kNumVar) ? forced : env_sel;
   const Var& var = variants[vsel];
   const int rows_per_cta = var.family == 1 ? kBlockM : kTilesPerCta * kBlockM;
   int work = 0;
@@ -1530,6 +1535,12 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
            std::to_string(fa.localSizeBytes) + ", params " + std::to_string(sizeof(AttnParams)) + ")";
   }
   return e;
+}
+
+int attn_set_variant(int v) {
+  if (v < -1 || v > 9) return -1;
+  g_attn_variant.store(v);
+  return 0;
 }
 
 // dev: read and reset the cycle counters of the profiling variant

@@ -610,6 +610,11 @@ int spava_debug_attn_prof(uint64_t* out16) {
   return SPAVA_OK;
 }
 
+int spava_debug_attn_variant(int variant) {
+  if (attn_set_variant(variant) != 0) return fail(SPAVA_EINVAL, "attn_variant: -1 or 0..9");
+  return SPAVA_OK;
+}
+
 int spava_make_plan(int n_v, int n_t, int hosts, int l_a, int l_p, int zigzag, spava_plan* out) {
   return plan_impl(n_v, n_t, hosts, l_a, l_p, zigzag, out);
 }

@@ -73,7 +73,8 @@ struct ProbView {
   long long split_stride_out;
   long long split_stride_lse;
 };
-void attn_prof_read(unsigned long long* out16);  // dev: cycle counters of variant 5
+void attn_prof_read(unsigned long long* out16);  // dev: cycle counters of variant 2
+int attn_set_variant(int v);                     // dev: -1 = env/default, else variant id
 cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, int dh,
                              cudaStream_t stream, std::string* err);
 

@@ -40,7 +40,7 @@ EXPORTED_SYMBOLS = [
     "spava_sim_layer_timed", "spava_host_set_trace", "spava_host_trace_read",
     "spava_host_status",
     "spava_host_set_timing", "spava_host_timing", "spava_kernel_launches",
-    "spava_debug_attn_prof",
+    "spava_debug_attn_prof", "spava_debug_attn_variant",
 ]
 
 
@@ -166,6 +166,7 @@ def lib():
         L.spava_sim_layer.argtypes = [C.c_void_p] * 8
         L.spava_sim_layer_timed.argtypes = [C.c_void_p] * 9
         L.spava_host_set_trace.argtypes = [C.c_void_p, C.c_int]
+        L.spava_debug_attn_variant.argtypes = [C.c_int]
         L.spava_split_rows.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                                        C.c_int, C.c_void_p]
         L.spava_merge_rows.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,

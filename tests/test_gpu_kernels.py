@@ -215,6 +215,27 @@ def _segs_np(segs):
     (64, [(5, False, 5)], 2, 2, 1),                     # tiny
 ])
 def test_attention_matches_oracle(cuda, case):
+    _check_attention_case(cuda, case)
+
+
+@pytest.mark.parametrize("variant", [1, 3, 7, 8])
+def test_attention_variants_match_oracle(cuda, variant):
+    """The measured alternative kernel families (single Q tile with double-buffered S, 64-key
+    tiles with double-buffered S, with/without FMA-pipe exp2) meet the same bar."""
+    from paper_2601_21444_b200 import spava
+
+    cases = [(300, [(300, True, 300)], 4, 2, 1),
+             (517, [(64, False, 64), (96, False, 96), (517, True, 509)], 4, 1, 1),
+             (128, [(33, False, 33), (700, False, 690), (700, False, 700), (128, True, 128)], 8, 2, 5)]
+    spava._check(spava.lib().spava_debug_attn_variant(variant))
+    try:
+        for case in cases:
+            _check_attention_case(cuda, case)
+    finally:
+        spava._check(spava.lib().spava_debug_attn_variant(-1))
+
+
+def _check_attention_case(cuda, case):
     from paper_2601_21444_b200 import spava
 
     nq, seginfo, hq, hkv, splits = case
