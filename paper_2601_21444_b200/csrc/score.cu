@@ -342,13 +342,28 @@ __device__ __forceinline__ float prob_fast(double e, double rinv, bool& redo) {
 // CTA = 32 keys x all heads: warp w owns heads w, w+16, ...; lane owns key j.  Per head the
 // column sum runs over query rows i ascending (8-row batches keep 8 loads and 8
 // independent exps in flight per lane), then the ordered sum over heads through smem.
+// kSmemStats: the per-row statistics (mx, 1/sum, lthr) of every (head, row) are staged in
+// shared memory once per CTA (warp-uniform broadcast reads) instead of three global loads
+// per element; used whenever hq * n_t rows fit (the C1..C4 shapes).
 constexpr int kColWarps = 16;
+constexpr int kColStatBytes = 20;  // double mx, double 1/sum, float lthr
+template <bool kSmemStats>
 __global__ void __launch_bounds__(kColWarps * 32) colsum_kernel(const __grid_constant__ ScoreArgs a) {
   __shared__ float part[32][33];
   __shared__ double tab[16];
+  extern __shared__ __align__(16) uint8_t col_smem[];
+  double2* sstat = reinterpret_cast<double2*>(col_smem);                       // [hq*n_t] (mx, rinv)
+  float* slthr = reinterpret_cast<float*>(col_smem + 16ull * a.hq * a.n_t);    // [hq*n_t]
   load_exp_table(tab);
-  __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, blk = blockIdx.y;
+  if (kSmemStats && a.softmax) {
+    const double* stb = a.stats + static_cast<long long>(blk) * a.hq * a.n_t * kStat;
+    for (int r = threadIdx.x; r < a.hq * a.n_t; r += kColWarps * 32) {
+      sstat[r] = make_double2(stb[r * kStat], stb[r * kStat + 2]);
+      slthr[r] = lthr_of(stb + r * kStat);
+    }
+  }
+  __syncthreads();
   const int j = blockIdx.x * 32 + lane;
   const bool inb = j < a.l_b;  // j < ldL always (ldL is a multiple of 128)
   const double sc = static_cast<double>(a.scale);
@@ -356,6 +371,9 @@ __global__ void __launch_bounds__(kColWarps * 32) colsum_kernel(const __grid_con
     const long long hb = (static_cast<long long>(blk) * a.hq + h) * a.n_t;
     const float* L = a.L + hb * a.ldL + j;
     const double* st = a.stats + hb * kStat;
+    auto mx_of = [&](int i) { return kSmemStats ? sstat[h * a.n_t + i].x : st[i * kStat]; };
+    auto rinv_of = [&](int i) { return kSmemStats ? sstat[h * a.n_t + i].y : st[i * kStat + 2]; };
+    auto thr_of = [&](int i) { return kSmemStats ? slthr[h * a.n_t + i] : lthr_of(st + i * kStat); };
     float acc = 0.f;
     if (a.softmax) {
       int i = 0;
@@ -375,12 +393,11 @@ __global__ void __launch_bounds__(kColWarps * 32) colsum_kernel(const __grid_con
         bool redo = false;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          p[u] = prob_fast(exp_neg(xrel(l[u], lthr_of(st + (i + u) * kStat), sc, st[(i + u) * kStat]), tab),
-                           st[(i + u) * kStat + 2], redo);
+          p[u] = prob_fast(exp_neg(xrel(l[u], thr_of(i + u), sc, mx_of(i + u)), tab), rinv_of(i + u), redo);
         if (redo) {
 #pragma unroll 1
           for (int u = 0; u < 8; ++u) {
-            const double e = exp_neg(xrel(l[u], lthr_of(st + (i + u) * kStat), sc, st[(i + u) * kStat]), tab);
+            const double e = exp_neg(xrel(l[u], thr_of(i + u), sc, mx_of(i + u)), tab);
             p[u] = __double2float_rn(__ddiv_rn(e, st[(i + u) * kStat + 1]));
           }
         }
@@ -388,7 +405,7 @@ __global__ void __launch_bounds__(kColWarps * 32) colsum_kernel(const __grid_con
         for (int u = 0; u < 8; ++u) acc = __fadd_rn(acc, p[u]);
       }
       for (; i < a.n_t; ++i) {
-        const double e = exp_neg(xrel(L[static_cast<long long>(i) * a.ldL], lthr_of(st + i * kStat), sc, st[i * kStat]), tab);
+        const double e = exp_neg(xrel(L[static_cast<long long>(i) * a.ldL], thr_of(i), sc, mx_of(i)), tab);
         acc = __fadd_rn(acc, __double2float_rn(__ddiv_rn(e, st[i * kStat + 1])));
       }
     } else {
@@ -461,7 +478,19 @@ cudaError_t launch_score_exact2(int nblk, const void* q, long long ldq, int n_t,
     else
       rowstats_kernel<false><<<grid, 256, 0, stream>>>(a);
   }
-  colsum_kernel<<<dim3((l_b + 31) / 32, nblk), kColWarps * 32, 0, stream>>>(a);
+  const size_t stat_smem = static_cast<size_t>(kColStatBytes) * hq * n_t;
+  if (softmax && stat_smem <= 96 * 1024) {
+    static size_t attr = 0;
+    if (stat_smem > attr) {
+      cudaError_t e = cudaFuncSetAttribute(colsum_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(96 * 1024));
+      if (e != cudaSuccess) return e;
+      attr = 96 * 1024;
+    }
+    colsum_kernel<true><<<dim3((l_b + 31) / 32, nblk), kColWarps * 32, stat_smem, stream>>>(a);
+  } else {
+    colsum_kernel<false><<<dim3((l_b + 31) / 32, nblk), kColWarps * 32, 0, stream>>>(a);
+  }
   return cudaGetLastError();
 }
 
