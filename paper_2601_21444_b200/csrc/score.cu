@@ -238,7 +238,10 @@ __global__ void __launch_bounds__(kThr, 2) logits_kernel(const __grid_constant__
 // of the exact products, monotone), sum = sum_j exp(x_j - mx) over non-pad keys (fp64,
 // thread-strided, then butterfly + 8-warp tree).  kPad: an explicit pad mask (the
 // partition's pads are a tail, passed as n_valid, so the production path reads no mask).
-template <bool kPad>
+// kRegF4 > 0: the thread's share of the row (<= kRegF4 float4, l_b <= kRegF4 * 1024) is
+// loaded once, all loads in flight together, and kept in registers for the sum pass;
+// kRegF4 == 0 streams the row twice (long blocks, e.g. C4 at H = 1).
+template <bool kPad, int kRegF4>
 __global__ void __launch_bounds__(256) rowstats_kernel(const __grid_constant__ ScoreArgs a) {
   __shared__ double tab[16];
   __shared__ float redf[8];
@@ -251,8 +254,8 @@ __global__ void __launch_bounds__(256) rowstats_kernel(const __grid_constant__ S
   const uint8_t* pad = a.pad[blk];
   const int nv = min(a.n_valid[blk], a.l_b);
   auto vis = [&](int j) { return j < nv && !(kPad && pad[j]); };
-  // 4 float4 loads in flight per thread per pass step (the row is 4*l_b bytes)
-  constexpr int kU = 4;
+  constexpr int kU = kRegF4 > 0 ? kRegF4 : 4;  // float4 loads in flight per thread
+  float4 keep[kRegF4 > 0 ? kRegF4 : 1];
   float mxf = -INFINITY;
   for (int j0 = tid * 4; j0 < nv; j0 += kU * 1024) {
     float4 v[kU];
@@ -262,6 +265,7 @@ __global__ void __launch_bounds__(256) rowstats_kernel(const __grid_constant__ S
                                 : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
+      if (kRegF4 > 0) keep[u] = v[u];
       const int j = j0 + u * 1024;
       if (j + 4 <= nv && !kPad) {
         mxf = fmaxf(fmaxf(mxf, fmaxf(v[u].x, v[u].y)), fmaxf(v[u].z, v[u].w));
@@ -272,6 +276,7 @@ __global__ void __launch_bounds__(256) rowstats_kernel(const __grid_constant__ S
         if (vis(j + 3)) mxf = fmaxf(mxf, v[u].w);
       }
     }
+    if (kRegF4 > 0) break;  // the whole share is in registers (l_b <= kRegF4 * 1024)
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
@@ -284,28 +289,39 @@ __global__ void __launch_bounds__(256) rowstats_kernel(const __grid_constant__ S
   const double mx = static_cast<double>(mxf) * sc;
   const float lthr = static_cast<float>((mx - 110.0) / sc);
   double s0 = 0.0, s1 = 0.0;
+  auto add4 = [&](const float4& v, int j) {
+    double e0 = exp_neg(xrel(v.x, lthr, sc, mx), tab);
+    double e1 = exp_neg(xrel(v.y, lthr, sc, mx), tab);
+    double e2 = exp_neg(xrel(v.z, lthr, sc, mx), tab);
+    double e3 = exp_neg(xrel(v.w, lthr, sc, mx), tab);
+    if (kPad || j + 4 > nv) {
+      e0 = vis(j) ? e0 : 0.0;
+      e1 = vis(j + 1) ? e1 : 0.0;
+      e2 = vis(j + 2) ? e2 : 0.0;
+      e3 = vis(j + 3) ? e3 : 0.0;
+    }
+    s0 += e0 + e1;
+    s1 += e2 + e3;
+  };
   if (mxf != -INFINITY) {
-    for (int j0 = tid * 4; j0 < nv; j0 += kU * 1024) {
-      float4 v[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u)
-        v[u] = j0 + u * 1024 < nv ? *reinterpret_cast<const float4*>(L + j0 + u * 1024)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (kRegF4 > 0) {
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const int j = j0 + u * 1024;
-        double e0 = exp_neg(xrel(v[u].x, lthr, sc, mx), tab);
-        double e1 = exp_neg(xrel(v[u].y, lthr, sc, mx), tab);
-        double e2 = exp_neg(xrel(v[u].z, lthr, sc, mx), tab);
-        double e3 = exp_neg(xrel(v[u].w, lthr, sc, mx), tab);
-        if (kPad || j + 4 > nv) {
-          e0 = vis(j) ? e0 : 0.0;
-          e1 = vis(j + 1) ? e1 : 0.0;
-          e2 = vis(j + 2) ? e2 : 0.0;
-          e3 = vis(j + 3) ? e3 : 0.0;
+        const int j = tid * 4 + u * 1024;
+        if (j < nv) add4(keep[u], j);
+      }
+    } else {
+      for (int j0 = tid * 4; j0 < nv; j0 += kU * 1024) {
+        float4 v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          v[u] = j0 + u * 1024 < nv ? *reinterpret_cast<const float4*>(L + j0 + u * 1024)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int j = j0 + u * 1024;
+          if (j < nv) add4(v[u], j);
         }
-        s0 += e0 + e1;
-        s1 += e2 + e3;
       }
     }
   }
@@ -474,9 +490,13 @@ cudaError_t launch_score_exact2(int nblk, const void* q, long long ldq, int n_t,
     bool any_pad = false;
     for (int b = 0; b < nblk; ++b) any_pad |= a.pad[b] != nullptr;
     if (any_pad)
-      rowstats_kernel<true><<<grid, 256, 0, stream>>>(a);
+      rowstats_kernel<true, 0><<<grid, 256, 0, stream>>>(a);
+    else if (l_b <= 8 * 1024)
+      rowstats_kernel<false, 8><<<grid, 256, 0, stream>>>(a);
+    else if (l_b <= 16 * 1024)
+      rowstats_kernel<false, 16><<<grid, 256, 0, stream>>>(a);
     else
-      rowstats_kernel<false><<<grid, 256, 0, stream>>>(a);
+      rowstats_kernel<false, 0><<<grid, 256, 0, stream>>>(a);
   }
   const size_t stat_smem = static_cast<size_t>(kColStatBytes) * hq * n_t;
   if (softmax && stat_smem <= 96 * 1024) {
