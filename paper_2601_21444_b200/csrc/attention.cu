@@ -946,6 +946,371 @@ __global__ void __launch_bounds__(kThreads1, 1) attn_fwd1_kernel(const __grid_co
   if (warp == 5) tmem_dealloc(tmem, kTmemCols);
 }
 
+// ============================================================================ variant family 3
+// Family 1 (one Q tile per CTA, S double-buffered: S_0 | S_1 | O) with the softmax split by
+// COLUMNS over two warpgroups: warps 0-3 take keys 0-63 of every tile, warps 4-7 keys
+// 64-127 of the same rows (a warp and its partner share TMEM lanes).  Each SMSP then holds
+// two softmax warps working on the same tile with half the exps each, so one warp's MUFU
+// stream fills the other's issue gaps, and the double-buffered S keeps the next tile's QK
+// off the critical path.  The halves agree on the running max through a per-tile exchange
+// in shared memory (named barrier of the 256 softmax threads); the row sum is combined in
+// the epilogue.
+constexpr int kThreads3 = 320;  // warps 0-7 softmax (2 column halves), 8 TMA, 9 MMA
+struct Smem3 {
+  static constexpr uint32_t q = 0;
+  static constexpr uint32_t k = q + kTileBytes;
+  static constexpr uint32_t v = k + kKS1 * kTileBytes;
+  static constexpr uint32_t xch = v + kVS1 * kTileBytes;        // [2 buf][2 half][128] f32
+  static constexpr uint32_t bar = xch + 2 * 2 * 128 * 4;
+  static constexpr uint32_t total = bar + 256;
+  static constexpr uint32_t bytes = total + 1024;
+};
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+template <int kEmu>
+__global__ void __launch_bounds__(kThreads3, 1) attn_fwd3_kernel(const __grid_constant__ AttnParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem3::bar);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;           // [kKS1]
+  uint64_t* k_empty = k_full + kKS1;     // [kKS1]
+  uint64_t* v_full = k_empty + kKS1;     // [kVS1]
+  uint64_t* v_empty = v_full + kVS1;     // [kVS1]
+  uint64_t* s_full = v_empty + kVS1;     // [2]
+  uint64_t* p_full = s_full + 2;         // [2] both halves' P written (256 arrivals)
+  uint64_t* o_full = p_full + 2;         // PV complete
+  uint64_t* o_done = o_full + 1;         // every MMA complete (epilogue)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+  float* xch = reinterpret_cast<float*>(smem + Smem3::xch);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+
+  int pi = 0;
+  while (pi + 1 < P.nprob && static_cast<int>(blockIdx.x) >= P.prob[pi + 1].work_begin) ++pi;
+  const AttnProb& prob = P.prob[pi];
+  int local = static_cast<int>(blockIdx.x) - prob.work_begin;
+  const int split = local % prob.splits;
+  local /= prob.splits;
+  const int head = local % P.hq;
+  local /= P.hq;
+  const int unit = prob.units - 1 - local;
+  const int i0 = unit * kBlockM;
+  const int nq = prob.nq;
+  const int imax = min(i0 + kBlockM, nq);
+  const int hk = head / (P.hq / P.hkv);
+
+  int T = 0;
+  for (int s = 0; s < prob.nseg; ++s) T += seg_tiles(prob.seg[s], imax);
+  const int t_begin = static_cast<int>(static_cast<long long>(T) * split / prob.splits);
+  const int t_end = static_cast<int>(static_cast<long long>(T) * (split + 1) / prob.splits);
+  const int ntiles = t_end - t_begin;
+  const CUtensorMap* tm = P.tmap[pi];
+
+  if (warp == 8 && elect_one()) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < kKS1; ++s) {
+      mbar_init(k_full + s, 1);
+      mbar_init(k_empty + s, 1);
+    }
+    for (int s = 0; s < kVS1; ++s) {
+      mbar_init(v_full + s, 1);
+      mbar_init(v_empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(s_full + b, 1);
+      mbar_init(p_full + b, 256);
+    }
+    mbar_init(o_full, 1);
+    mbar_init(o_done, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&tm[0]);
+    for (int s = 0; s < prob.nseg; ++s) {
+      tma_prefetch_desc(&tm[1 + 2 * s]);
+      tma_prefetch_desc(&tm[2 + 2 * s]);
+    }
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    // ======================================================== TMA producer
+    if (elect_one()) {
+      mbar_expect_tx(q_full, kTileBytes);
+      for (int c = 0; c < 2; ++c)
+        tma_load_2d(smem + Smem3::q + c * kBoxBytes, &tm[0], q_full, head * kHeadDim + c * 64, i0);
+      Cursor cur = cursor_at(prob, imax, t_begin);
+      for (int it = 0; it < ntiles; ++it) {
+        const CUtensorMap* km = &tm[1 + 2 * cur.seg];
+        const CUtensorMap* vm = &tm[2 + 2 * cur.seg];
+        const int ks = it % kKS1, vs = it % kVS1;
+        if (it >= kKS1) mbar_wait(k_empty + ks, ((it / kKS1) - 1) & 1);
+        mbar_expect_tx(k_full + ks, kTileBytes);
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d(smem + Smem3::k + ks * kTileBytes + c * kBoxBytes, km, k_full + ks,
+                      hk * kHeadDim + c * 64, cur.kt * kBlockN);
+        if (it >= kVS1) mbar_wait(v_empty + vs, ((it / kVS1) - 1) & 1);
+        mbar_expect_tx(v_full + vs, kTileBytes);
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d(smem + Smem3::v + vs * kTileBytes + c * kBoxBytes, vm, v_full + vs,
+                      hk * kHeadDim + c * 64, cur.kt * kBlockN);
+        cursor_next(prob, imax, cur);
+      }
+    }
+  } else if (warp == 9) {
+    // ======================================================== MMA issuer (as family 1)
+    if (elect_one()) {
+      const uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
+      const uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
+      const uint32_t sq = smem_u32(smem + Smem3::q);
+      const uint32_t sk = smem_u32(smem + Smem3::k);
+      const uint32_t sv = smem_u32(smem + Smem3::v);
+      auto issue_qk = [&](int b, int it) {
+        const int ks = it % kKS1;
+        mbar_wait(k_full + ks, (it / kKS1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + b * 128;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t koff = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
+          mma_ss(d, sdesc_sw128(sq + koff, 16, 1024), sdesc_sw128(sk + ks * kTileBytes + koff, 16, 1024),
+                 idesc_qk, kk > 0 ? 1u : 0u);
+        }
+        tc_commit(s_full + b);
+        tc_commit(k_empty + ks);
+      };
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      if (ntiles > 0) issue_qk(0, 0);
+      if (ntiles > 1) issue_qk(1, 1);
+      for (int it = 0; it < ntiles; ++it) {
+        const int b = it & 1, vs = it % kVS1;
+        mbar_wait(v_full + vs, (it / kVS1) & 1);
+        mbar_wait(p_full + b, (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + 256;
+        const uint32_t a = tmem + b * 128;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(d, a + kk * 8, sdesc_sw128(sv + vs * kTileBytes + kk * 2048, kBoxBytes, 1024), idesc_pv,
+                 (it > 0 || kk > 0) ? 1u : 0u);
+        tc_commit(o_full);
+        tc_commit(v_empty + vs);
+        if (it + 2 < ntiles) issue_qk(b, it + 2);
+      }
+      tc_commit(o_done);
+    }
+  } else {
+    // ======================================================== softmax: 2 column halves
+    const int half = warp >> 2;   // 0: keys 0-63 of each tile, 1: keys 64-127
+    const int quad = warp & 3;
+    const int rloc = quad * 32 + lane;
+    const int row = i0 + rloc;
+    const uint32_t t_lane = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t tO = tmem + t_lane + 256 + half * 64;  // this half rescales/stores O cols
+    const float sl2 = P.scale_log2;
+    const float2 sl2v = make_float2(sl2, sl2);
+    float m_ref = -INFINITY;
+    float l = 0.f;
+    int xc = 0;  // exchange counter (identical in both halves: same decisions)
+    // max of this half's 64 scores, combined with the partner half through smem
+    auto exchange_max = [&](float mine) {
+      float* buf = xch + (xc & 1) * 256;
+      buf[half * 128 + rloc] = mine;
+      named_bar_sync(1, 256);
+      const float other = buf[(half ^ 1) * 128 + rloc];
+      ++xc;
+      return fmaxf(mine, other);
+    };
+    Cursor cur = cursor_at(prob, imax, t_begin);
+    uint32_t sr[2][32];
+    uint32_t pk[2][16];
+    for (int it = 0; it < ntiles; ++it, cursor_next(prob, imax, cur)) {
+      const int b = it & 1;
+      const uint32_t tS = tmem + t_lane + b * 128;
+      const AttnSeg sg = prob.seg[cur.seg];
+      const int mode = tile_mode(sg, cur.kt, i0, nq);
+      mbar_wait(s_full + b, (it >> 1) & 1);
+      tc_fence_after();
+      auto load_s = [&]() {
+        tmem_ld32(tS + half * 64, sr[0]);
+        tmem_ld32(tS + half * 64 + 32, sr[1]);
+        tmem_wait_ld();
+      };
+      auto chunk_max = [&](int c, float (&mxp)[8]) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const int t = (j / 2) & 7;
+          mxp[t] = fmaxf(mxp[t], fmaxf(__uint_as_float(sr[c][j]), __uint_as_float(sr[c][j + 1])));
+        }
+      };
+      auto chunk_exp = [&](int c, float2 negm, bool emu) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 x2 = __ffma2_rn(
+              make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1])), sl2v, negm);
+          float2 p2;
+          if (kEmu > 0 && emu && (j % (16 / kEmu)) == (16 / kEmu) - 1)
+            p2 = exp2_poly2(x2);
+          else
+            p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));
+          sr[c][2 * j] = __float_as_uint(p2.x);
+          sr[c][2 * j + 1] = __float_as_uint(p2.y);
+        }
+      };
+      auto chunk_pack = [&](int c, float2 (&sacc)[4]) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 p2 = make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1]));
+          sacc[j & 3] = __fadd2_rn(sacc[j & 3], p2);
+          __nv_bfloat162 bb = __floats2bfloat162_rn(p2.x, p2.y);
+          pk[c][j] = *reinterpret_cast<uint32_t*>(&bb);
+        }
+      };
+      auto exp_pack_all = [&](float2 negm, bool emu, float2 (&sacc)[4]) {
+        chunk_exp(0, negm, emu);
+        chunk_exp(1, negm, emu);
+        chunk_pack(0, sacc);
+        chunk_pack(1, sacc);
+      };
+      auto max8 = [](const float (&m)[8]) {
+        return fmaxf(fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3])), fmaxf(fmaxf(m[4], m[5]), fmaxf(m[6], m[7])));
+      };
+      float alpha = 1.f;
+      bool rescale = false;
+      float mxp[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
+      float2 sacc[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
+      bool done = false;
+      load_s();
+      if (mode == kFull && m_ref != -INFINITY) {
+        const float2 negm = make_float2(-m_ref, -m_ref);
+        chunk_max(0, mxp);
+        chunk_max(1, mxp);
+        exp_pack_all(negm, true, sacc);
+        const float mx = exchange_max(max8(mxp));
+        done = !(mx * sl2 > m_ref + 8.f);
+        if (!done) {
+#pragma unroll
+          for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
+          load_s();
+        }
+      } else if (mode == kPart) {
+        const int k0 = cur.kt * kBlockN + half * 64;
+        int lim = sg.len - k0;
+        if (sg.causal) lim = min(lim, row - k0 + 1);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c * 32 + j >= lim) sr[c][j] = __float_as_uint(-INFINITY);
+      }
+      if (!done) {
+        chunk_max(0, mxp);
+        chunk_max(1, mxp);
+        const float mx = exchange_max(max8(mxp));
+        const float m_new = fmaxf(m_ref, mx * sl2);
+        if (m_new > m_ref + 8.f) {
+          alpha = exp2f(m_ref - m_new);
+          m_ref = m_new;
+          rescale = true;
+        }
+        const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+        exp_pack_all(make_float2(-m_use, -m_use), mode == kFull, sacc);
+      }
+      tmem_st16(tS + half * 32, pk[0]);
+      tmem_st16(tS + half * 32 + 16, pk[1]);
+      const float2 sum2 = __fadd2_rn(__fadd2_rn(sacc[0], sacc[1]), __fadd2_rn(sacc[2], sacc[3]));
+      l = l * alpha + (sum2.x + sum2.y);  // this half's share of the row sum
+      if (rescale && it > 0) {
+        mbar_wait(o_full, (it - 1) & 1);  // PV(it-1) has landed in O
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t o[32];
+          tmem_ld32(tO + 32 * c, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
+          tmem_st32(tO + 32 * c, o);
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_full + b);
+    }
+    // ---- epilogue: the row sum of both halves, O / l (this half's 64 columns), lse
+    {
+      float* buf = xch + (xc & 1) * 256;
+      buf[half * 128 + rloc] = l;
+      named_bar_sync(1, 256);
+      l += buf[(half ^ 1) * 128 + rloc];
+    }
+    mbar_wait(o_done, 0);
+    tc_fence_after();
+    const bool valid_row = row < nq;
+    const float inv = (l > 0.f) ? 1.f / l : 0.f;
+    const long long obase = static_cast<long long>(split) * prob.split_stride_out +
+                            static_cast<long long>(row) * prob.ldo + head * kHeadDim + half * 64;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uint32_t o[32];
+      if (ntiles > 0) {
+        tmem_ld32(tO + 32 * c, o);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o[j] = 0u;
+      }
+      if (valid_row) {
+        if (prob.out_f32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(prob.out) + obase + 32 * c);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(__uint_as_float(o[4 * j]) * inv, __uint_as_float(o[4 * j + 1]) * inv,
+                                 __uint_as_float(o[4 * j + 2]) * inv, __uint_as_float(o[4 * j + 3]) * inv);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(prob.out) + obase + 32 * c);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 bb = __floats2bfloat162_rn(__uint_as_float(o[8 * j + 2 * e]) * inv,
+                                                        __uint_as_float(o[8 * j + 2 * e + 1]) * inv);
+              w[e] = *reinterpret_cast<uint32_t*>(&bb);
+            }
+            dst[j] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+    }
+    if (valid_row && prob.lse && half == 0) {
+      const float lse = (l > 0.f) ? (m_ref + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+      prob.lse[static_cast<long long>(split) * prob.split_stride_lse +
+               static_cast<long long>(row) * prob.ld_lse + head] = lse;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 9) tmem_dealloc(tmem, kTmemCols);
+}
+
 // ============================================================================ variant family 2
 // Two Q tiles (256 rows, or two q-heads of one GQA group) per CTA as in the ping-pong
 // family, but with 64-key KV tiles so each Q tile's score accumulator fits TMEM twice:
@@ -1459,7 +1824,9 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
                                                                           //   one-chunk-behind pack
       {attn_fwd2_kernel<0>, Smem2::bytes, kThreads, 2},                   // 7 64-key tiles, S x2
       {attn_fwd2_kernel<2>, Smem2::bytes, kThreads, 2},                   // 8 7 + 25% FMA exp2
-      {attn_fwd2_kernel<1>, Smem2::bytes, kThreads, 2}};                  // 9 7 + 12.5% FMA exp2
+      {attn_fwd2_kernel<1>, Smem2::bytes, kThreads, 2},                   // 9 7 + 12.5% FMA exp2
+      {attn_fwd3_kernel<0>, Smem3::bytes, kThreads3, 1},                  // 10 1 + column-split softmax
+      {attn_fwd3_kernel<4>, Smem3::bytes, kThreads3, 1}};                 // 11 10 + 25% FMA exp2
   constexpr int kNumVar = sizeof(variants) / sizeof(variants[0]);
   static const int env_sel = [] {
     const char* e = getenv("SPAVA_ATTN_VARIANT");
@@ -1538,7 +1905,7 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
 }
 
 int attn_set_variant(int v) {
-  if (v < -1 || v > 9) return -1;
+  if (v < -1 || v > 11) return -1;
   g_attn_variant.store(v);
   return 0;
 }
