@@ -589,6 +589,399 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 #undef TILE_HEAD
 }
 
+// ============================================================================ variant family 4
+// Ping-pong family with the score tile split across time: P is stored in the UPPER half of
+// the S columns (64..127) and QK(j+1) is issued as two N=64 halves.  Half A (keys 0-63 ->
+// S columns 0-63) is issued as soon as the softmax has pulled S(j) into registers (after
+// its row max), i.e. while tile j's exps still run; P(j) is committed in two halves so
+// PV(j) starts on keys 0-63 while the softmax is still on keys 64-127; half B of QK(j+1)
+// (columns 64-127) follows PV(j) in the in-order tensor pipe.  The softmax of tile j+1
+// then waits only for PV(j)_B + QK(j+1)_B after its last commit instead of a full PV+QK.
+// The MMA warp is a small scheduler polling both Q tiles' barriers (no head-of-line
+// blocking between the two softmax warpgroups).
+template <int kEmu>
+__global__ void __launch_bounds__(kThreads, 1) attn_fwd4_kernel(const __grid_constant__ AttnParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  using SL = Smem<2>;
+  constexpr int KS = 2;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SL::bar);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;        // [2]
+  uint64_t* k_empty = k_full + 2;     // [2]
+  uint64_t* v_full = k_empty + 2;     // [2]
+  uint64_t* v_empty = v_full + 2;     // [2]
+  uint64_t* sA = v_empty + 2;         // [2 Q tiles] QK half A (S cols 0-63) landed
+  uint64_t* sB = sA + 2;              // [2] QK half B (S cols 64-127) landed
+  uint64_t* sfree = sB + 2;           // [2] softmax holds S(j) in registers (128 arrivals)
+  uint64_t* pA = sfree + 2;           // [2] P keys 0-63 stored (and O corrected)
+  uint64_t* pB = pA + 2;              // [2] P keys 64-127 stored
+  uint64_t* o_full = pB + 2;          // [2] PV half B of the tile complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+
+  int pi = 0;
+  while (pi + 1 < P.nprob && static_cast<int>(blockIdx.x) >= P.prob[pi + 1].work_begin) ++pi;
+  const AttnProb& prob = P.prob[pi];
+  int local = static_cast<int>(blockIdx.x) - prob.work_begin;
+  const int split = local % prob.splits;
+  local /= prob.splits;
+  const int pair = prob.head_pair;
+  const int nheads = pair ? P.hq / 2 : P.hq;
+  const int head = pair ? 2 * (local % nheads) : local % nheads;
+  local /= nheads;
+  const int unit = prob.units - 1 - local;
+  const int i0 = pair ? 0 : unit * (kTilesPerCta * kBlockM);
+  const int nq = prob.nq;
+  const int imax = min(i0 + (pair ? kBlockM : kTilesPerCta * kBlockM), nq);
+  const int hk = head / (P.hq / P.hkv);
+#define TILE_R0(t) (pair ? 0 : i0 + (t) * kBlockM)
+#define TILE_HEAD(t) (head + pair * (t))
+
+  int T = 0;
+  for (int s = 0; s < prob.nseg; ++s) T += seg_tiles(prob.seg[s], imax);
+  const int t_begin = static_cast<int>(static_cast<long long>(T) * split / prob.splits);
+  const int t_end = static_cast<int>(static_cast<long long>(T) * (split + 1) / prob.splits);
+  const int ntiles = t_end - t_begin;
+  const CUtensorMap* tm = P.tmap[pi];
+  // Q tile t processes a prefix of the KV tiles (causal skips only trail the own segment)
+  int nt[2] = {0, 0};
+  {
+    Cursor c = cursor_at(prob, imax, t_begin);
+    for (int it = 0; it < ntiles; ++it, cursor_next(prob, imax, c))
+      for (int qt = 0; qt < 2; ++qt)
+        if (tile_mode(prob.seg[c.seg], c.kt, TILE_R0(qt), nq) != kSkip) nt[qt] = it + 1;
+  }
+
+  if (warp == kProducerWarp && elect_one()) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < KS; ++s) {
+      mbar_init(k_full + s, 1);
+      mbar_init(k_empty + s, 1);
+      mbar_init(v_full + s, 1);
+      mbar_init(v_empty + s, 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(sA + t, 1);
+      mbar_init(sB + t, 1);
+      mbar_init(sfree + t, 128);
+      mbar_init(pA + t, 128);
+      mbar_init(pB + t, 128);
+      mbar_init(o_full + t, 1);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tm[0]);
+    for (int s = 0; s < prob.nseg; ++s) {
+      tma_prefetch_desc(&tm[1 + 2 * s]);
+      tma_prefetch_desc(&tm[2 + 2 * s]);
+    }
+  }
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kProducerWarp) {
+    // ======================================================== TMA producer (as family 0)
+    if (elect_one()) {
+      const bool has1 = TILE_R0(1) < nq;
+      mbar_expect_tx(q_full, (has1 ? 2u : 1u) * kTileBytes);
+      for (int qt = 0; qt < (has1 ? 2 : 1); ++qt)
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d(smem + SL::q + qt * kTileBytes + c * kBoxBytes, &tm[0], q_full,
+                      TILE_HEAD(qt) * kHeadDim + c * 64, TILE_R0(qt));
+      Cursor cur = cursor_at(prob, imax, t_begin);
+      for (int it = 0; it < ntiles; ++it) {
+        const CUtensorMap* km = &tm[1 + 2 * cur.seg];
+        const CUtensorMap* vm = &tm[2 + 2 * cur.seg];
+        const int ks = it % KS, vs = it % kVStages;
+        if (it >= KS) mbar_wait(k_empty + ks, ((it / KS) - 1) & 1);
+        mbar_expect_tx(k_full + ks, kTileBytes);
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d(smem + SL::k + ks * kTileBytes + c * kBoxBytes, km, k_full + ks,
+                      hk * kHeadDim + c * 64, cur.kt * kBlockN);
+        if (it >= kVStages) mbar_wait(v_empty + vs, ((it / kVStages) - 1) & 1);
+        mbar_expect_tx(v_full + vs, kTileBytes);
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d(smem + SL::v + vs * kTileBytes + c * kBoxBytes, vm, v_full + vs,
+                      hk * kHeadDim + c * 64, cur.kt * kBlockN);
+        cursor_next(prob, imax, cur);
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ======================================================== MMA scheduler
+    if (elect_one()) {
+      const uint32_t idesc_h = idesc_bf16_f32(128, 64, 0, 0);    // QK half: N = 64 keys
+      const uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);  // P (TMEM), V MN-major
+      const uint32_t sq = smem_u32(smem + SL::q);
+      const uint32_t sk = smem_u32(smem + SL::k);
+      const uint32_t sv = smem_u32(smem + SL::v);
+      // QK(j) half h of Q tile qt: S cols [64h, 64h+64) <- Q_qt x K(j) rows [64h, 64h+64)
+      auto issue_qk_half = [&](int qt, int j, int h) {
+        const int ks = j % KS;
+        const uint32_t d = tmem + qt * 128 + h * 64;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t koff = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
+          mma_ss(d, sdesc_sw128(sq + qt * kTileBytes + koff, 16, 1024),
+                 sdesc_sw128(sk + ks * kTileBytes + koff + h * 64 * 128, 16, 1024), idesc_h,
+                 kk > 0 ? 1u : 0u);
+        }
+      };
+      // PV(j) half h: O_qt += P[keys 64h..64h+63] x V(j) rows [64h, 64h+64)
+      auto issue_pv_half = [&](int qt, int j, int h) {
+        const int vs = j % kVStages;
+        const uint32_t d = tmem + 256 + qt * 128;
+        const uint32_t a = tmem + qt * 128 + 64;
+#pragma unroll
+        for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
+          mma_ts(d, a + kk * 8, sdesc_sw128(sv + vs * kTileBytes + kk * 2048, kBoxBytes, 1024), idesc_pv,
+                 (j > 0 || kk > 0) ? 1u : 0u);
+      };
+      // K(j) / V(j) are released once every Q tile that uses tile j has issued its last MMA on it
+      auto users = [&](int j) { return (nt[0] > j ? 1 : 0) + (nt[1] > j ? 1 : 0); };
+      int k_done[KS] = {0, 0}, v_done[kVStages] = {0, 0};
+      auto k_release = [&](int j) {
+        if (++k_done[j % KS] == users(j)) {
+          tc_commit(k_empty + j % KS);
+          k_done[j % KS] = 0;
+        }
+      };
+      auto v_release = [&](int j) {
+        if (++v_done[j % kVStages] == users(j)) {
+          tc_commit(v_empty + j % kVStages);
+          v_done[j % kVStages] = 0;
+        }
+      };
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      if (ntiles > 0) {
+        mbar_wait(k_full, 0);
+        tc_fence_after();
+        for (int qt = 0; qt < 2; ++qt)
+          if (nt[qt] > 0) {
+            issue_qk_half(qt, 0, 0);
+            tc_commit(sA + qt);
+            issue_qk_half(qt, 0, 1);
+            tc_commit(sB + qt);
+            k_release(0);
+          }
+      }
+      // per Q tile: current tile j and phase (0: QK_A(j+1) after sfree(j), 1: PV_A(j) after
+      // pA(j), 2: PV_B(j) + QK_B(j+1) after pB(j))
+      int j[2] = {0, 0}, ph[2] = {0, 0};
+      bool a_issued[2] = {false, false};  // QK_A(j+1) issued for the current j
+      auto finished = [&](int qt) { return j[qt] >= nt[qt]; };
+      while (!(finished(0) && finished(1))) {
+        for (int qt = 0; qt < 2; ++qt) {
+          if (finished(qt)) continue;
+          const int jj = j[qt];
+          const bool next = jj + 1 < nt[qt];
+          if (ph[qt] == 0) {
+            if (!next) {
+              ph[qt] = 1;
+            } else if (mbar_try(sfree + qt, jj & 1) && mbar_try(k_full + (jj + 1) % KS, ((jj + 1) / KS) & 1)) {
+              tc_fence_after();
+              issue_qk_half(qt, jj + 1, 0);
+              tc_commit(sA + qt);
+              a_issued[qt] = true;
+              ph[qt] = 1;
+            }
+          }
+          if (ph[qt] == 1) {
+            if (mbar_try(pA + qt, jj & 1) && mbar_try(v_full + jj % kVStages, (jj / kVStages) & 1)) {
+              tc_fence_after();
+              issue_pv_half(qt, jj, 0);
+              ph[qt] = 2;
+            }
+          }
+          if (ph[qt] == 2) {
+            if (mbar_try(pB + qt, jj & 1)) {
+              tc_fence_after();
+              issue_pv_half(qt, jj, 1);
+              tc_commit(o_full + qt);
+              v_release(jj);
+              if (next) {
+                issue_qk_half(qt, jj + 1, 1);
+                tc_commit(sB + qt);
+                k_release(jj + 1);
+              }
+              a_issued[qt] = false;
+              ph[qt] = 0;
+              ++j[qt];
+            }
+          }
+        }
+      }
+    }
+  } else if (warp < kProducerWarp) {
+    // ======================================================== softmax warpgroups
+    const int qt = warp >> 2;
+    const int quad = warp & 3;
+    const int row = TILE_R0(qt) + quad * 32 + lane;
+    const int qhead = TILE_HEAD(qt);
+    const uint32_t t_lane = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t tS = tmem + t_lane + qt * 128;
+    const uint32_t tO = tmem + t_lane + 256 + qt * 128;
+    const float sl2 = P.scale_log2;
+    const float2 sl2v = make_float2(sl2, sl2);
+    float m_ref = -INFINITY;
+    float l = 0.f;
+    Cursor cur = cursor_at(prob, imax, t_begin);
+    uint32_t sr[4][32];
+    uint32_t pk[2][16];
+    for (int it = 0; it < nt[qt]; ++it, cursor_next(prob, imax, cur)) {
+      const AttnSeg sg = prob.seg[cur.seg];
+      const int mode = tile_mode(sg, cur.kt, TILE_R0(qt), nq);
+      mbar_wait(sA + qt, it & 1);
+      mbar_wait(sB + qt, it & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tS + 32 * c, sr[c]);
+      tmem_wait_ld();
+      if (mode == kPart) {
+        const int k0 = cur.kt * kBlockN;
+        int lim = sg.len - k0;
+        if (sg.causal) lim = min(lim, row - k0 + 1);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int jv = 0; jv < 32; ++jv)
+            if (c * 32 + jv >= lim) sr[c][jv] = __float_as_uint(-INFINITY);
+      }
+      float mxp[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int jv = 0; jv < 32; jv += 2) {
+          const int t = (jv / 2) & 7;
+          mxp[t] = fmaxf(mxp[t], fmaxf(__uint_as_float(sr[c][jv]), __uint_as_float(sr[c][jv + 1])));
+        }
+      // S is in registers: the next tile's QK half A may overwrite S columns 0-63 now
+      tc_fence_before();
+      mbar_arrive(sfree + qt);
+      const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                             fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+      float alpha = 1.f;
+      bool rescale = false;
+      const float m_new = fmaxf(m_ref, mx * sl2);
+      if (m_new > m_ref + 8.f) {  // lazy rescale (P <= 2^8 otherwise)
+        alpha = exp2f(m_ref - m_new);
+        m_ref = m_new;
+        rescale = true;
+      }
+      const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+      const float2 negm = make_float2(-m_use, -m_use);
+      float2 sacc[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c = 2 * h + cc;
+#pragma unroll
+          for (int jv = 0; jv < 16; ++jv) {
+            const float2 x2 = __ffma2_rn(make_float2(__uint_as_float(sr[c][2 * jv]),
+                                                     __uint_as_float(sr[c][2 * jv + 1])), sl2v, negm);
+            float2 p2;
+            if (kEmu > 0 && mode == kFull && (jv % (16 / kEmu)) == (16 / kEmu) - 1)
+              p2 = exp2_poly2(x2);
+            else
+              p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));
+            sacc[jv & 3] = __fadd2_rn(sacc[jv & 3], p2);
+            __nv_bfloat162 bb = __floats2bfloat162_rn(p2.x, p2.y);
+            pk[cc][jv] = *reinterpret_cast<uint32_t*>(&bb);
+          }
+        }
+        // P keys [64h, 64h+64) -> S columns 64 + 32h .. (packed bf16 pairs)
+        tmem_st16(tS + 64 + 32 * h, pk[0]);
+        tmem_st16(tS + 64 + 32 * h + 16, pk[1]);
+        if (h == 0 && rescale && it > 0) {
+          // PV(it-1) is complete: S(it) half B only landed after it in the tensor pipe
+          mbar_wait(o_full + qt, (it - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tO + 32 * c, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int jv = 0; jv < 32; ++jv) o[jv] = __float_as_uint(__uint_as_float(o[jv]) * alpha);
+            tmem_st32(tO + 32 * c, o);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(h == 0 ? pA + qt : pB + qt);
+      }
+      const float2 sum2 = __fadd2_rn(__fadd2_rn(sacc[0], sacc[1]), __fadd2_rn(sacc[2], sacc[3]));
+      l = l * alpha + (sum2.x + sum2.y);
+    }
+    // ---- epilogue: O / l, lse
+    const int cnt = nt[qt];
+    if (cnt > 0) {
+      mbar_wait(o_full + qt, (cnt - 1) & 1);  // only PV(cnt-1) can still be in flight
+      tc_fence_after();
+    }
+    const bool valid_row = row < nq;
+    const float inv = (l > 0.f) ? 1.f / l : 0.f;
+    const long long obase = static_cast<long long>(split) * prob.split_stride_out +
+                            static_cast<long long>(row) * prob.ldo + qhead * kHeadDim;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t o[32];
+      if (cnt > 0) {
+        tmem_ld32(tO + 32 * c, o);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int jv = 0; jv < 32; ++jv) o[jv] = 0u;
+      }
+      if (valid_row) {
+        if (prob.out_f32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(prob.out) + obase + 32 * c);
+#pragma unroll
+          for (int jv = 0; jv < 8; ++jv)
+            dst[jv] = make_float4(__uint_as_float(o[4 * jv]) * inv, __uint_as_float(o[4 * jv + 1]) * inv,
+                                  __uint_as_float(o[4 * jv + 2]) * inv, __uint_as_float(o[4 * jv + 3]) * inv);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(prob.out) + obase + 32 * c);
+#pragma unroll
+          for (int jv = 0; jv < 4; ++jv) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 bb = __floats2bfloat162_rn(__uint_as_float(o[8 * jv + 2 * e]) * inv,
+                                                        __uint_as_float(o[8 * jv + 2 * e + 1]) * inv);
+              w[e] = *reinterpret_cast<uint32_t*>(&bb);
+            }
+            dst[jv] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+    }
+    if (valid_row && prob.lse) {
+      const float lse = (l > 0.f) ? (m_ref + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+      prob.lse[static_cast<long long>(split) * prob.split_stride_lse +
+               static_cast<long long>(row) * prob.ld_lse + qhead] = lse;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == kMmaWarp) tmem_dealloc(tmem, kTmemCols);
+#undef TILE_R0
+#undef TILE_HEAD
+}
+
 // ============================================================================ variant family 1
 // One Q tile (128 rows of one q-head) per CTA with the score accumulator double-buffered
 // in TMEM: S_0 | S_1 | O (384 of 512 columns).  The MMA warp issues QK(j+2) into the buffer
@@ -1826,7 +2219,9 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
       {attn_fwd2_kernel<2>, Smem2::bytes, kThreads, 2},                   // 8 7 + 25% FMA exp2
       {attn_fwd2_kernel<1>, Smem2::bytes, kThreads, 2},                   // 9 7 + 12.5% FMA exp2
       {attn_fwd3_kernel<0>, Smem3::bytes, kThreads3, 1},                  // 10 1 + column-split softmax
-      {attn_fwd3_kernel<4>, Smem3::bytes, kThreads3, 1}};                 // 11 10 + 25% FMA exp2
+      {attn_fwd3_kernel<4>, Smem3::bytes, kThreads3, 1},                  // 11 10 + 25% FMA exp2
+      {attn_fwd4_kernel<0>, Smem<2>::bytes, kThreads, 0},                 // 12 0 + split QK / P halves
+      {attn_fwd4_kernel<4>, Smem<2>::bytes, kThreads, 0}};                // 13 12 + 25% FMA exp2
   constexpr int kNumVar = sizeof(variants) / sizeof(variants[0]);
   static const int env_sel = [] {
     const char* e = getenv("SPAVA_ATTN_VARIANT");
@@ -1905,7 +2300,7 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
 }
 
 int attn_set_variant(int v) {
-  if (v < -1 || v > 11) return -1;
+  if (v < -1 || v > 13) return -1;
   g_attn_variant.store(v);
   return 0;
 }

@@ -611,7 +611,7 @@ int spava_debug_attn_prof(uint64_t* out16) {
 }
 
 int spava_debug_attn_variant(int variant) {
-  if (attn_set_variant(variant) != 0) return fail(SPAVA_EINVAL, "attn_variant: -1 or 0..11");
+  if (attn_set_variant(variant) != 0) return fail(SPAVA_EINVAL, "attn_variant: -1 or 0..13");
   return SPAVA_OK;
 }
 

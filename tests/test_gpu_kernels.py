@@ -218,7 +218,7 @@ def test_attention_matches_oracle(cuda, case):
     _check_attention_case(cuda, case)
 
 
-@pytest.mark.parametrize("variant", [1, 3, 7, 8, 10])
+@pytest.mark.parametrize("variant", [1, 3, 7, 8, 10, 12])
 def test_attention_variants_match_oracle(cuda, variant):
     """The measured alternative kernel families (single Q tile with double-buffered S, 64-key
     tiles with double-buffered S, with/without FMA-pipe exp2) meet the same bar."""
