@@ -896,7 +896,11 @@ int spava_fabric_create_nccl(const spava_layer_cfg* cfg, int device, const void*
     delete F;
     return fail(SPAVA_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
   }
-  CU_TRY(cudaStreamCreateWithFlags(&F->comm_stream, cudaStreamNonBlocking));
+  const cudaError_t e = cudaStreamCreateWithFlags(&F->comm_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    spava_fabric_destroy(F);
+    return fail(SPAVA_ECUDA, std::string("nccl fabric: comm stream: ") + cudaGetErrorString(e));
+  }
   *out = F;
   return SPAVA_OK;
 }
@@ -910,6 +914,24 @@ int spava_fabric_destroy(spava_fabric* F) {
   delete F;
   return SPAVA_OK;
 }
+
+namespace {
+int host_init_streams(spava_host* H) {
+  for (auto& e : H->ev) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CU_TRY(cudaEventCreateWithFlags(&H->ev_fork, cudaEventDisableTiming));
+  CU_TRY(cudaEventCreateWithFlags(&H->ev_sel, cudaEventDisableTiming));
+  int prio_lo = 0, prio_hi = 0;
+  CU_TRY(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CU_TRY(cudaStreamCreateWithPriority(&H->side, cudaStreamNonBlocking, prio_hi));
+  CU_TRY(cudaStreamCreateWithFlags(&H->h2d, cudaStreamNonBlocking));
+  CU_TRY(cudaStreamCreateWithFlags(&H->d2h, cudaStreamNonBlocking));
+  CU_TRY(cudaEventCreateWithFlags(&H->ev_kvq, cudaEventDisableTiming));
+  CU_TRY(cudaEventCreateWithFlags(&H->ev_d2h, cudaEventDisableTiming));
+  for (auto& e : H->ev_qc) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : H->ev_oc) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return SPAVA_OK;
+}
+}  // namespace
 
 int spava_host_create(spava_fabric* F, int h, spava_host** out) {
   if (!F) return fail(SPAVA_EINVAL, "host_create: null fabric");
@@ -957,18 +979,11 @@ int spava_host_create(spava_fabric* F, int h, spava_host** out) {
   H->qsplit_out = reinterpret_cast<float*>(b); b += qo;
   H->qsplit_lse = reinterpret_cast<float*>(b); b += ql;
   H->status = reinterpret_cast<int32_t*>(b);
-  for (auto& e : H->ev) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  CU_TRY(cudaEventCreateWithFlags(&H->ev_fork, cudaEventDisableTiming));
-  CU_TRY(cudaEventCreateWithFlags(&H->ev_sel, cudaEventDisableTiming));
-  int prio_lo = 0, prio_hi = 0;
-  CU_TRY(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-  CU_TRY(cudaStreamCreateWithPriority(&H->side, cudaStreamNonBlocking, prio_hi));
-  CU_TRY(cudaStreamCreateWithFlags(&H->h2d, cudaStreamNonBlocking));
-  CU_TRY(cudaStreamCreateWithFlags(&H->d2h, cudaStreamNonBlocking));
-  CU_TRY(cudaEventCreateWithFlags(&H->ev_kvq, cudaEventDisableTiming));
-  CU_TRY(cudaEventCreateWithFlags(&H->ev_d2h, cudaEventDisableTiming));
-  for (auto& e : H->ev_qc) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  for (auto& e : H->ev_oc) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  const int rc = host_init_streams(H);
+  if (rc != SPAVA_OK) {
+    spava_host_destroy(H);  // releases whatever was created before the failure
+    return rc;
+  }
   *out = H;
   return SPAVA_OK;
 }
