@@ -171,3 +171,20 @@ def test_host_buffer_layer_matches_device_layer(cuda, nccl):
         assert torch.equal(o_h, o_ref.cpu()), it
     host.close()
     fab.close()
+
+
+@pytest.mark.parametrize("hosts,n_t", [(2, 37), (8, 128)])
+def test_layer_7b_heads(cuda, hosts, n_t):
+    """Qwen2.5-VL-7B head shape (28 q / 4 kv heads, GQA group 7 -> no head pairing) with a
+    ragged query block and, at 8 hosts, a padded tail, against the C oracle layer."""
+    from paper_2601_21444_b200 import spava
+
+    n_v, hq, hkv = 3001, 28, 4
+    l_a, l_p = 40, 96
+    plan = spava.make_plan(n_v, n_t, hosts, l_a, l_p, True)
+    n_pad = l_a + 2 * hosts * plan.l_b + n_t
+    rng = np.random.default_rng(700 + hosts)
+    Q, K, V = randn(rng, n_pad, hq * 128), randn(rng, n_pad, hkv * 128), randn(rng, n_pad, hkv * 128)
+    want = O.spava_layer(Q, K, V, n_v, n_t, hosts, l_a, l_p, hq, hkv, 128)
+    res = run_layer(cuda, Q, K, V, n_v, n_t, hosts, l_a, l_p, hq, hkv)
+    check_layer(res, want, n_t, hosts, l_a, True)
