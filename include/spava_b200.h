@@ -213,6 +213,14 @@ int spava_host_layer(spava_host* host, const void* q, const void* k, const void*
 int spava_host_layer_hostbuf(spava_host* host, const void* q_h, const void* k_h, const void* v_h,
                              void* out_h, int32_t* sel_h, void* q_d, void* k_d, void* v_d,
                              void* out_d, int32_t* sel_d, void* stream);
+/* One spava_host_layer captured as a CUDA graph (caller, side and comm streams, NCCL
+ * rounds included) on `stream` (not the legacy default stream), then replayed with one
+ * launch per layer: the buffers are those of the capture (fill them before each replay).
+ * Timing and trace must be off while capturing.                                       */
+int spava_host_capture_layer(spava_host* host, const void* q, const void* k, const void* v,
+                             void* out, int32_t* sel, void* stream);
+int spava_host_replay_layer(spava_host* host, void* stream);
+
 int spava_sim_layer(spava_fabric* fab, spava_host* const* hosts, const void* const* q,
                     const void* const* k, const void* const* v, void* const* out,
                     int32_t* const* sel, void* stream);

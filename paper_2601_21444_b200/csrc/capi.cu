@@ -209,6 +209,10 @@ struct spava_host {
   };
   bool trace = false;
   int trace_layer = 0;
+  // one captured layer (CUDA graph over the caller's, side and comm streams)
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  uint64_t graph_kernels = 0;
   std::vector<TraceRec> trace_recs;
   std::vector<cudaEvent_t> trace_pool;
   std::vector<cudaEvent_t> ev_pool;
@@ -994,6 +998,8 @@ int spava_host_destroy(spava_host* H) {
     if (e) cudaEventDestroy(e);
   if (H->ev_fork) cudaEventDestroy(H->ev_fork);
   if (H->ev_sel) cudaEventDestroy(H->ev_sel);
+  if (H->graph_exec) cudaGraphExecDestroy(H->graph_exec);
+  if (H->graph) cudaGraphDestroy(H->graph);
   if (H->side) cudaStreamDestroy(H->side);
   if (H->h2d) cudaStreamDestroy(H->h2d);
   if (H->d2h) cudaStreamDestroy(H->d2h);
@@ -1393,6 +1399,46 @@ int spava_host_timing(spava_host* H, double* ms_by_class, double* attn_flops,
   }
   if (attn_flops) *attn_flops = H->attn_flops;
   if (attn_launches) *attn_launches = H->attn_launches;
+  return SPAVA_OK;
+}
+
+int spava_host_capture_layer(spava_host* H, const void* q, const void* k, const void* v, void* out,
+                             int32_t* sel, void* stream) {
+  spava_fabric* F = H->fab;
+  if (!F->nccl && F->plan.hosts != 1)
+    return fail(SPAVA_EINVAL, "capture_layer: local fabric with H > 1 must be driven by spava_sim_layer");
+  if (H->timing || H->trace) return fail(SPAVA_EINVAL, "capture_layer: disable timing and trace first");
+  if (!stream) return fail(SPAVA_EINVAL, "capture_layer: needs a non-default stream");
+  CU_TRY(cudaSetDevice(F->device));
+  cudaStream_t st = as_stream(stream);
+  if (H->graph_exec) cudaGraphExecDestroy(H->graph_exec);
+  if (H->graph) cudaGraphDestroy(H->graph);
+  H->graph_exec = nullptr;
+  H->graph = nullptr;
+  HostBufs b{static_cast<const uint8_t*>(q), static_cast<const uint8_t*>(k),
+             static_cast<const uint8_t*>(v), static_cast<uint8_t*>(out), sel};
+  const uint64_t k0 = g_launches.load();
+  CU_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  const int rc = layer_impl(H, b, st, CopyEdges{});
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(st, &g);
+  if (rc != SPAVA_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  CU_TRY(e);
+  H->graph = g;
+  CU_TRY(cudaGraphInstantiate(&H->graph_exec, g, 0));
+  H->graph_kernels = g_launches.load() - k0;
+  g_launches -= H->graph_kernels;  // captured, not launched
+  return SPAVA_OK;
+}
+
+int spava_host_replay_layer(spava_host* H, void* stream) {
+  if (!H || !H->graph_exec) return fail(SPAVA_EINVAL, "replay_layer: nothing captured");
+  CU_TRY(cudaSetDevice(H->fab->device));
+  CU_TRY(cudaGraphLaunch(H->graph_exec, as_stream(stream)));
+  g_launches += H->graph_kernels;
   return SPAVA_OK;
 }
 

@@ -188,3 +188,39 @@ def test_layer_7b_heads(cuda, hosts, n_t):
     want = O.spava_layer(Q, K, V, n_v, n_t, hosts, l_a, l_p, hq, hkv, 128)
     res = run_layer(cuda, Q, K, V, n_v, n_t, hosts, l_a, l_p, hq, hkv)
     check_layer(res, want, n_t, hosts, l_a, True)
+
+
+@pytest.mark.parametrize("nccl", [False, True])
+def test_graph_replay_matches_layer(cuda, nccl):
+    """A layer captured as a CUDA graph (side / comm streams and NCCL rounds included)
+    replays bit-identically to spava_host_layer, also after the inputs are refilled."""
+    import torch
+
+    from paper_2601_21444_b200 import spava
+
+    n_v, n_t, l_a, l_p, hq, hkv = 3000, 64, 32, 128, 4, 2
+    cfg = spava.LayerConfig.make(n_v, n_t, 1, l_a, l_p, hq, hkv)
+    fab = (spava.Fabric(cfg, 0, unique_id=spava.nccl_unique_id(), world=1, rank=0) if nccl
+           else spava.Fabric(cfg, 0))
+    host = fab.host(0)
+    rows = host.rows
+    g = torch.Generator(device=cuda).manual_seed(23)
+    q, k, v = [torch.randn(rows, w * 128, device=cuda, generator=g).to(torch.bfloat16) for w in (hq, hkv, hkv)]
+    out = torch.zeros(rows, hq * 128, dtype=torch.bfloat16, device=cuda)
+    sel = torch.zeros(2, l_p, dtype=torch.int32, device=cuda)
+    s = torch.cuda.Stream()
+    host.capture_layer(q, k, v, out, sel, stream=s)
+    for it in range(2):
+        if it:
+            for x in (q, k, v):
+                x.copy_(torch.randn(x.shape, device=cuda, generator=g).to(torch.bfloat16))
+        o_ref = torch.zeros_like(out)
+        s_ref = torch.zeros_like(sel)
+        host.layer(q, k, v, o_ref, s_ref)
+        torch.cuda.synchronize()
+        host.replay_layer(s)
+        s.synchronize()
+        assert torch.equal(sel, s_ref), it
+        assert torch.equal(out, o_ref), it
+    host.close()
+    fab.close()
