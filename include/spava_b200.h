@@ -235,6 +235,12 @@ int spava_sim_layer_timed(spava_fabric* fab, spava_host* const* hosts, const voi
  * merge row invalid everywhere).  Synchronises the given stream.            */
 int spava_host_status(spava_host* host, void* stream, int32_t* status_out);
 
+/* DelayInjection analogue (simhost.hpp:51-55): spin `ns` nanoseconds on a stream before
+ * a phase of every layer -- 0: scoring/selection (side stream), 1: exchange rounds (comm
+ * stream), 2: query attention (caller stream), 3: stage 1.  Results must not change
+ * (tests/test_gpu_layer.py, acceptance.cpp:221-268 criterion 5).                     */
+int spava_host_set_delay(spava_host* host, int which, uint64_t ns);
+
 /* Schedule trace in the reference Event schema (simhost.hpp:17-46): while enabled, every
  * layer call records run_host's events (score, pass1/pass2/qpartial issue / wait-start /
  * completed, query_attn, stage1, stage2, merge begin/end; simhost.cpp:322-426) in program

@@ -209,6 +209,9 @@ struct spava_host {
   };
   bool trace = false;
   int trace_layer = 0;
+  // DelayInjection analogue: ns of spin before a phase on its stream (0 score/select on the
+  // side stream, 1 exchange rounds on the comm stream, 2 query attention, 3 stage 1)
+  unsigned long long delay_ns[4] = {0, 0, 0, 0};
   // one captured layer (CUDA graph over the caller's, side and comm streams)
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
@@ -1088,6 +1091,8 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
   CU_TRY(cudaStreamWaitEvent(ss, H->ev_fork, 0));
   CU_TRY(need_kvq(ss));
   CU_TRY(need_kvq(st));
+  CU_TRY(launch_delay(H->delay_ns[0], ss));
+  CU_TRY(launch_delay(H->delay_ns[2], st));
   if (!F->nccl) {
     // H = 1: block lo (v = 0) has no passing segment, so only stage 2 waits for selection
     ST_TRY(phase_select(H, b, ss, false));
@@ -1100,6 +1105,7 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     T(st, kCommIssued, "qpartial", true);
     T(st, kCommWaitStart, "pass1", true);
     T(st, kCommCompleted, "pass1", true);
+    CU_TRY(launch_delay(H->delay_ns[3], st));
     T(st, kComputeBegin, "stage1");
     ST_TRY(stage_chunks(H, b, st, cp, 0));
     T(st, kComputeEnd, "stage1");
@@ -1121,6 +1127,7 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
   ST_TRY(phase_select(H, b, ss, true));  // records pass1_ready, pass2_ready on ss
   CU_TRY(cudaEventRecord(H->ev_sel, ss));
   CU_TRY(cudaStreamWaitEvent(cs, H->ev[0], 0));
+  CU_TRY(launch_delay(H->delay_ns[1], cs));
   T(cs, kCommIssued, "pass1", true);
   ST_TRY(nccl_round(F, H->ex, 0));
   CU_TRY(cudaEventRecord(H->ev[3], cs));
@@ -1143,6 +1150,7 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     CU_TRY(cudaStreamWaitEvent(st, H->ev[4], 0));
     T(st, kCommCompleted, "pass2", true);
   }
+  CU_TRY(launch_delay(H->delay_ns[3], st));
   T(st, kComputeBegin, "stage1");
   ST_TRY(stage_chunks(H, b, st, cp, 0));
   T(st, kComputeEnd, "stage1");
@@ -1340,6 +1348,13 @@ int spava_sim_layer_timed(spava_fabric* F, spava_host* const* hosts, const void*
   }
   for (auto& e : ev) cudaEventDestroy(e);
   return rc;
+}
+
+int spava_host_set_delay(spava_host* H, int which, uint64_t ns) {
+  if (!H) return fail(SPAVA_EINVAL, "set_delay: null host");
+  if (which < 0 || which > 3) return fail(SPAVA_ERANGE, "set_delay: which is 0..3");
+  H->delay_ns[which] = ns;
+  return SPAVA_OK;
 }
 
 int spava_host_set_trace(spava_host* H, int enable) {

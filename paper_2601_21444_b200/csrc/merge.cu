@@ -81,4 +81,20 @@ cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// DelayInjection analogue (simhost.hpp:51-55, simhost.cpp:139-147): one thread spins on
+// %globaltimer so a stream reaches its next operation late (schedule-independence tests).
+__global__ void delay_kernel(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+cudaError_t launch_delay(unsigned long long ns, cudaStream_t stream) {
+  if (ns == 0) return cudaSuccess;
+  delay_kernel<<<1, 1, 0, stream>>>(ns);
+  return cudaGetLastError();
+}
+
 }  // namespace spava

@@ -130,5 +130,6 @@ struct MergeParams {
   int32_t* status; // nullable; set to 1 if a row is invalid in every part
 };
 cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream);
+cudaError_t launch_delay(unsigned long long ns, cudaStream_t stream);  // test: stream delay
 
 }  // namespace spava

@@ -38,7 +38,7 @@ EXPORTED_SYMBOLS = [
     "spava_fabric_destroy", "spava_host_create", "spava_host_destroy", "spava_host_plan",
     "spava_host_rows", "spava_host_layer", "spava_host_layer_hostbuf", "spava_sim_layer",
     "spava_sim_layer_timed", "spava_host_set_trace", "spava_host_trace_read",
-    "spava_host_capture_layer", "spava_host_replay_layer",
+    "spava_host_capture_layer", "spava_host_replay_layer", "spava_host_set_delay",
     "spava_host_status",
     "spava_host_set_timing", "spava_host_timing", "spava_kernel_launches",
     "spava_debug_attn_prof", "spava_debug_attn_variant",
@@ -169,6 +169,7 @@ def lib():
         L.spava_host_set_trace.argtypes = [C.c_void_p, C.c_int]
         L.spava_host_capture_layer.argtypes = [C.c_void_p] * 7
         L.spava_host_replay_layer.argtypes = [C.c_void_p, C.c_void_p]
+        L.spava_host_set_delay.argtypes = [C.c_void_p, C.c_int, C.c_uint64]
         L.spava_debug_attn_variant.argtypes = [C.c_int]
         L.spava_split_rows.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                                        C.c_int, C.c_void_p]
@@ -489,6 +490,10 @@ class Host:
             self._p, C.c_void_p(q_h.data_ptr()), C.c_void_p(k_h.data_ptr()), C.c_void_p(v_h.data_ptr()),
             C.c_void_p(out_h.data_ptr()), C.c_void_p(sel_h.data_ptr()) if sel_h is not None else None,
             _ptr(q_d), _ptr(k_d), _ptr(v_d), _ptr(out_d), _ptr(sel_d), _stream(stream)))
+
+    def set_delay(self, which, ns):
+        """Spin `ns` ns before phase `which` (0 score, 1 exchange, 2 query, 3 stage 1)."""
+        _check(lib().spava_host_set_delay(self._p, int(which), int(ns)))
 
     def capture_layer(self, q, k, v, out, sel=None, stream=None):
         """Capture one layer on these buffers as a CUDA graph (replay_layer launches it)."""
