@@ -264,3 +264,58 @@ def test_schedule_and_delay_independence(cuda, nccl):
         assert torch.equal(o, o_ref) and torch.equal(s, s_ref), which
     host.close()
     fab.close()
+
+
+def test_instrumented_flops_match_formula(cuda):
+    """acceptance.cpp:130-182 (criterion 3) on the GPU runtime: the attention FLOPs the
+    runtime counts at launch (reference convention, attention.cpp:33-36) equal bench.py's
+    per-host formula exactly; minus the block->anchor and query terms they equal the
+    reference's attn_flops_per_host (metrics.cpp:11-15); zigzag balances them, naive does
+    not."""
+    import random
+
+    import torch
+
+    import bench
+    from paper_2601_21444_b200 import spava
+
+    rnd = random.Random(3)
+    for _ in range(6):
+        hosts = rnd.randint(1, 4)
+        l_b, l_a, n_t = rnd.randint(2, 5) * 64, rnd.choice([0, 64, 128]), rnd.choice([16, 64])
+        l_p = rnd.randint(0, l_b // 64) * 32
+        n_v = l_a + 2 * hosts * l_b  # no pad rows
+        hq, hkv = 4, 2
+        subsets = {}
+        for zz in (True, False):
+            cfg = spava.LayerConfig.make(n_v, n_t, hosts, l_a, l_p, hq, hkv, zigzag=zz)
+            fab = spava.Fabric(cfg, 0)
+            hs = [fab.host(h) for h in range(hosts)]
+            rows = hs[0].rows
+            ins = [[torch.randn(rows, w * 128, device=cuda).to(torch.bfloat16) for w in (hq, hkv, hkv)]
+                   for _ in range(hosts)]
+            outs = [torch.empty(rows, hq * 128, dtype=torch.bfloat16, device=cuda) for _ in range(hosts)]
+            for h in hs:
+                h.set_timing(True)
+            fab.sim_layer(hs, [x[0] for x in ins], [x[1] for x in ins], [x[2] for x in ins], outs)
+            torch.cuda.synchronize()
+            g = dict(hosts=hosts, l_a=l_a, l_b=l_b, l_p=l_p, n_t=n_t)
+            d = hq * 128
+            sub = []
+            for h, X in enumerate(hs):
+                got = X.timing()["attention_flops"]
+                assert got == bench.attn_flops_host(g, hq, h, zz), (hosts, zz, h)
+                a0, a1 = spava.slice_anchor(l_a, hosts, h)
+                extra = (8 * l_a * l_b + 4 * n_t * ((a1 - a0) + 2 * l_b) +
+                         (2 * n_t * n_t if h == hosts - 1 else 0)) * d
+                sub.append(got - extra)
+                X.set_timing(False)
+            if zz:
+                b2 = 2 * l_a * l_a * d + 4 * l_b * l_b * d + 4 * (2 * hosts - 1) * l_p * l_b * d
+                assert all(x == b2 for x in sub), (sub, b2)
+            subsets[zz] = sub
+            for X in hs:
+                X.close()
+            fab.close()
+        if hosts >= 2 and l_p >= 1:
+            assert max(subsets[False]) / min(subsets[False]) > 1.0
