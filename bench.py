@@ -531,6 +531,41 @@ def run_spava_arm(args):
             fabf.close()
         except Exception as e:  # pragma: no cover
             extra["fast_scoring"] = {"error": str(e)[:200]}
+        # the decoder layer around the path (f2): layer_norm, [Wq|Wk|Wv], Spava attention, Wo +
+        # residual, layer_norm, ReLU MLP + residual (simhost.cpp:196-207, 431-436) at
+        # Qwen2.5-VL-3B widths (d_model 2048, ffn 11008), cuBLASLt bf16 GEMMs
+        try:
+            D, FF = 2048, 11008
+            gw = torch.Generator(device=dev).manual_seed(77)
+            bfw = lambda *sh, sc: (torch.randn(*sh, generator=gw, device=dev) * sc).to(torch.bfloat16)
+            xw = bfw(rows, D, sc=1.0)
+            w_qkv = bfw(D, (hq + 2 * hkv) * DH, sc=D ** -0.5)
+            w_o = bfw(hq * DH, D, sc=(hq * DH) ** -0.5)
+            w_1 = bfw(D, FF, sc=D ** -0.5)
+            w_2 = bfw(FF, D, sc=FF ** -0.5)
+            g1 = torch.ones(D, device=dev)
+            g2 = torch.ones(D, device=dev)
+            wsd = host.decoder_layer(xw, w_qkv, w_o, w_1, w_2, g1, g2, stream)
+            for _ in range(2):
+                host.decoder_layer(xw, w_qkv, w_o, w_1, w_2, g1, g2, stream, wsd)
+            torch.cuda.synchronize()
+            nd = max(3, min(args.steps, 10))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(nd):
+                host.decoder_layer(xw, w_qkv, w_o, w_1, w_2, g1, g2, stream, wsd)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            dms = e0.elapsed_time(e1) / nd
+            gemm_fl = 2.0 * rows * D * ((hq + 2 * hkv) * DH + hq * DH / D * D + 2 * FF)
+            extra["decoder_layer"] = {
+                "tokens_per_s": g["n"] / (dms / 1e3), "ms": round(dms, 3),
+                "gemm_tflop": round(gemm_fl / 1e12, 3),
+                "note": "x += Spava-attention decoder layer (layer_norm, QKV, Spava, Wo, layer_norm, "
+                        "ReLU MLP) at d_model 2048 / ffn 11008; GEMMs are cuBLASLt bf16"}
+            del xw, w_qkv, w_o, w_1, w_2, wsd
+        except Exception as e:  # pragma: no cover
+            extra["decoder_layer"] = {"error": str(e)[:200]}
         if not args.no_cpu:
             threads = os.cpu_count() or 1
             tps, layer_s, rate, desc, kind = reference_tokens_per_s(g, hq, hkv, threads, args.cpu_budget)

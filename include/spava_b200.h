@@ -221,6 +221,26 @@ int spava_host_capture_layer(spava_host* host, const void* q, const void* k, con
                              void* out, int32_t* sel, void* stream);
 int spava_host_replay_layer(spava_host* host, void* stream);
 
+/* The decoder layer around the path (simhost.cpp:196-207, 431-436):
+ *   xn = norm ? layer_norm(x, g_1) : x;  q, k, v = xn [Wq | Wk | Wv];  a = spava layer;
+ *   x += a Wo;  f = norm ? layer_norm(x, g_2) : x;  x += relu(f W1) W2.
+ * x: host-local rows [anchor | lo | hi | query] x d_model, bf16, updated in place.  All
+ * matrices are row-major bf16 on the device (w_qkv: d_model x (hq+2*hkv)*128, w_o:
+ * hq*128 x d_model, w_1: d_model x ffn, w_2: ffn x d_model); gains fp32 [d_model].
+ * GEMMs are cuBLASLt bf16 library GEMMs with fp32 accumulation.                       */
+typedef struct {
+  const void* w_qkv;
+  const void* w_o;
+  const void* w_1;
+  const void* w_2;
+  const float* g_1;
+  const float* g_2;
+  int d_model, ffn, norm;
+} spava_decoder_weights;
+size_t spava_decoder_workspace(const spava_host* host, const spava_decoder_weights* w);
+int spava_host_decoder_layer(spava_host* host, const spava_decoder_weights* w, void* x, int64_t ldx,
+                             void* ws, size_t ws_bytes, void* stream);
+
 int spava_sim_layer(spava_fabric* fab, spava_host* const* hosts, const void* const* q,
                     const void* const* k, const void* const* v, void* const* out,
                     int32_t* const* sel, void* stream);

@@ -212,6 +212,7 @@ struct spava_host {
   // DelayInjection analogue: ns of spin before a phase on its stream (0 score/select on the
   // side stream, 1 exchange rounds on the comm stream, 2 query attention, 3 stage 1)
   unsigned long long delay_ns[4] = {0, 0, 0, 0};
+  void* gemm = nullptr;  // cuBLASLt handle of the decoder-layer GEMMs (lazy)
   // one captured layer (CUDA graph over the caller's, side and comm streams)
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
@@ -1003,6 +1004,7 @@ int spava_host_destroy(spava_host* H) {
   if (H->ev_sel) cudaEventDestroy(H->ev_sel);
   if (H->graph_exec) cudaGraphExecDestroy(H->graph_exec);
   if (H->graph) cudaGraphDestroy(H->graph);
+  gemm_handle_destroy(H->gemm);
   if (H->side) cudaStreamDestroy(H->side);
   if (H->h2d) cudaStreamDestroy(H->h2d);
   if (H->d2h) cudaStreamDestroy(H->d2h);
@@ -1414,6 +1416,99 @@ int spava_host_timing(spava_host* H, double* ms_by_class, double* attn_flops,
   }
   if (attn_flops) *attn_flops = H->attn_flops;
   if (attn_launches) *attn_launches = H->attn_launches;
+  return SPAVA_OK;
+}
+
+namespace {
+constexpr size_t kGemmWs = 32ull << 20;
+struct DecoderWs {
+  size_t xn, q, k, v, a, h, gemm, total;
+};
+DecoderWs decoder_ws(const spava_host* H, const spava_decoder_weights* w) {
+  const spava_layer_cfg& c = H->fab->cfg;
+  const spava_plan& p = H->fab->plan;
+  const size_t rows = static_cast<size_t>(p.l_a) + 2ull * p.l_b + p.n_t;
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  DecoderWs d{};
+  size_t o = 0;
+  d.xn = o; o += al(rows * w->d_model * 2);
+  d.q = o; o += al(rows * c.hq * c.dh * 2);
+  d.k = o; o += al(rows * c.hkv * c.dh * 2);
+  d.v = o; o += al(rows * c.hkv * c.dh * 2);
+  d.a = o; o += al(rows * c.hq * c.dh * 2);
+  d.h = o; o += al(rows * static_cast<size_t>(w->ffn) * 2);
+  d.gemm = o; o += kGemmWs;
+  d.total = o;
+  return d;
+}
+}  // namespace
+
+size_t spava_decoder_workspace(const spava_host* H, const spava_decoder_weights* w) {
+  return (H && w) ? decoder_ws(H, w).total : 0;
+}
+
+int spava_host_decoder_layer(spava_host* H, const spava_decoder_weights* w, void* x, int64_t ldx,
+                             void* ws, size_t ws_bytes, void* stream) {
+  if (!H || !w || !x || !ws) return fail(SPAVA_EINVAL, "decoder_layer: null argument");
+  spava_fabric* F = H->fab;
+  if (!F->nccl && F->plan.hosts != 1)
+    return fail(SPAVA_EINVAL, "decoder_layer: local fabric with H > 1 must be driven by the simulator");
+  if (!w->w_qkv || !w->w_o || !w->w_1 || !w->w_2 || w->d_model <= 0 || w->d_model % 8 || w->ffn <= 0 ||
+      w->ffn % 8 || ldx < w->d_model || ldx % 8)
+    return fail(SPAVA_EINVAL, "decoder_layer: weights / d_model / ffn / ldx");
+  if (w->norm && (!w->g_1 || !w->g_2)) return fail(SPAVA_EINVAL, "decoder_layer: norm needs g_1, g_2");
+  const DecoderWs d = decoder_ws(H, w);
+  if (ws_bytes < d.total) return fail(SPAVA_EINVAL, "decoder_layer: workspace too small");
+  CU_TRY(cudaSetDevice(F->device));
+  if (!H->gemm && !(H->gemm = gemm_handle_create())) return fail(SPAVA_ECUDA, "decoder_layer: cublasLtCreate");
+  const spava_layer_cfg& c = F->cfg;
+  const spava_plan& p = F->plan;
+  const int rows = p.l_a + 2 * p.l_b + p.n_t;
+  const int D = w->d_model, dq = c.hq * c.dh, dk = c.hkv * c.dh, wqkv = dq + 2 * dk;
+  cudaStream_t st = as_stream(stream);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  void* xn = base + d.xn;
+  void* q = base + d.q;
+  void* k = base + d.k;
+  void* v = base + d.v;
+  void* a = base + d.a;
+  void* hbuf = base + d.h;
+  void* gws = base + d.gemm;
+  std::string err;
+  auto G = [&](int M, int N, int K, const void* A, long long lda, const void* B, long long ldb, void* Cm,
+               long long ldc, float beta, bool relu) -> int {
+    const cudaError_t e = gemm_bf16_rm(H->gemm, M, N, K, A, lda, B, ldb, Cm, ldc, beta, relu, gws, kGemmWs, st, &err);
+    if (e != cudaSuccess) return fail(SPAVA_ECUDA, "decoder_layer: " + (err.empty() ? std::string(cudaGetErrorString(e)) : err));
+    return SPAVA_OK;
+  };
+  const uint8_t* wq = static_cast<const uint8_t*>(w->w_qkv);
+  // project (simhost.cpp:196-199): xn = layer_norm(x, g1); q, k, v = xn [Wq | Wk | Wv]
+  const void* xin = x;
+  long long ldin = ldx;
+  if (w->norm) {
+    CU_TRY(launch_layer_norm(x, ldx, w->g_1, D, xn, D, rows, st));
+    xin = xn;
+    ldin = D;
+  }
+  ST_TRY(G(rows, dq, D, xin, ldin, wq, wqkv, q, dq, 0.f, false));
+  ST_TRY(G(rows, dk, D, xin, ldin, wq + dq * 2, wqkv, k, dk, 0.f, false));
+  ST_TRY(G(rows, dk, D, xin, ldin, wq + (dq + dk) * 2, wqkv, v, dk, 0.f, false));
+  // Spava attention (the hot path)
+  HostBufs b{static_cast<const uint8_t*>(q), static_cast<const uint8_t*>(k), static_cast<const uint8_t*>(v),
+             static_cast<uint8_t*>(a), nullptr};
+  ST_TRY(layer_impl(H, b, st, CopyEdges{}));
+  // finish_group (simhost.cpp:202-207): x += a Wo; f = layer_norm(x, g2); x += relu(f W1) W2
+  ST_TRY(G(rows, D, dq, a, dq, w->w_o, D, x, ldx, 1.f, false));
+  const void* fin = x;
+  long long ldf = ldx;
+  if (w->norm) {
+    CU_TRY(launch_layer_norm(x, ldx, w->g_2, D, xn, D, rows, st));
+    fin = xn;
+    ldf = D;
+  }
+  ST_TRY(G(rows, w->ffn, D, fin, ldf, w->w_1, w->ffn, hbuf, w->ffn, 0.f, true));
+  ST_TRY(G(rows, D, w->ffn, hbuf, w->ffn, w->w_2, D, x, ldx, 1.f, false));
+  g_launches += 6 + (w->norm ? 2 : 0);
   return SPAVA_OK;
 }
 

@@ -114,6 +114,15 @@ cudaError_t launch_split_rows(int l_a, int l_b, int n_t, int n_v, int lo, int hi
                               long long ld_src, void* dst, long long ld_dst, int row_bytes,
                               bool merge, bool shared, cudaStream_t stream);
 
+// ---------------------------------------------------------------- decoder layer (f2)
+cudaError_t launch_layer_norm(const void* x, long long ldx, const float* g, int d, void* y,
+                              long long ldy, int rows, cudaStream_t stream);
+cudaError_t gemm_bf16_rm(void* lt, int M, int N, int K, const void* A, long long lda, const void* B,
+                         long long ldb, void* C, long long ldc, float beta, bool relu, void* ws,
+                         size_t ws_bytes, cudaStream_t stream, std::string* err);
+void* gemm_handle_create();
+void gemm_handle_destroy(void* h);
+
 // ---------------------------------------------------------------- merge
 constexpr int kMaxMergeParts = 64;
 struct MergeParams {

@@ -39,6 +39,7 @@ EXPORTED_SYMBOLS = [
     "spava_host_rows", "spava_host_layer", "spava_host_layer_hostbuf", "spava_sim_layer",
     "spava_sim_layer_timed", "spava_host_set_trace", "spava_host_trace_read",
     "spava_host_capture_layer", "spava_host_replay_layer", "spava_host_set_delay",
+    "spava_decoder_workspace", "spava_host_decoder_layer",
     "spava_host_status",
     "spava_host_set_timing", "spava_host_timing", "spava_kernel_launches",
     "spava_debug_attn_prof", "spava_debug_attn_variant",
@@ -115,6 +116,13 @@ def trace_jsonl(events):
     return "".join(json.dumps({k: e[k] for k in keys}) + "\n" for e in events)
 
 
+class DecoderWeights(C.Structure):
+    """spava_decoder_weights: device pointers of the decoder layer around the path."""
+    _fields_ = [("w_qkv", C.c_void_p), ("w_o", C.c_void_p), ("w_1", C.c_void_p), ("w_2", C.c_void_p),
+                ("g_1", C.c_void_p), ("g_2", C.c_void_p), ("d_model", C.c_int), ("ffn", C.c_int),
+                ("norm", C.c_int)]
+
+
 class LayerConfig(C.Structure):
     _fields_ = [(n, C.c_int) for n in (
         "n_v", "n_t", "hosts", "l_a", "l_p", "zigzag", "designated", "query_self_all",
@@ -170,6 +178,10 @@ def lib():
         L.spava_host_capture_layer.argtypes = [C.c_void_p] * 7
         L.spava_host_replay_layer.argtypes = [C.c_void_p, C.c_void_p]
         L.spava_host_set_delay.argtypes = [C.c_void_p, C.c_int, C.c_uint64]
+        L.spava_decoder_workspace.restype = C.c_size_t
+        L.spava_decoder_workspace.argtypes = [C.c_void_p, C.c_void_p]
+        L.spava_host_decoder_layer.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                               C.c_size_t, C.c_void_p]
         L.spava_debug_attn_variant.argtypes = [C.c_int]
         L.spava_split_rows.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                                        C.c_int, C.c_void_p]
@@ -490,6 +502,22 @@ class Host:
             self._p, C.c_void_p(q_h.data_ptr()), C.c_void_p(k_h.data_ptr()), C.c_void_p(v_h.data_ptr()),
             C.c_void_p(out_h.data_ptr()), C.c_void_p(sel_h.data_ptr()) if sel_h is not None else None,
             _ptr(q_d), _ptr(k_d), _ptr(v_d), _ptr(out_d), _ptr(sel_d), _stream(stream)))
+
+    def decoder_layer(self, x, w_qkv, w_o, w_1, w_2, g_1=None, g_2=None, stream=None, ws=None):
+        """x += Spava-attention decoder layer (in place); weights are torch CUDA tensors
+        (bf16 row-major, gains fp32).  Returns the workspace for reuse."""
+        import torch
+
+        dw = DecoderWeights(w_qkv.data_ptr(), w_o.data_ptr(), w_1.data_ptr(), w_2.data_ptr(),
+                            g_1.data_ptr() if g_1 is not None else None,
+                            g_2.data_ptr() if g_2 is not None else None,
+                            x.shape[1], w_1.shape[1], int(g_1 is not None))
+        need = lib().spava_decoder_workspace(self._p, C.byref(dw))
+        if ws is None or ws.numel() < need:
+            ws = torch.empty(need, dtype=torch.uint8, device=x.device)
+        _check(lib().spava_host_decoder_layer(self._p, C.byref(dw), _ptr(x), x.stride(0), _ptr(ws),
+                                              ws.numel(), _stream(stream)))
+        return ws
 
     def set_delay(self, which, ns):
         """Spin `ns` ns before phase `which` (0 score, 1 exchange, 2 query, 3 stage 1)."""

@@ -319,3 +319,54 @@ def test_instrumented_flops_match_formula(cuda):
             fab.close()
         if hosts >= 2 and l_p >= 1:
             assert max(subsets[False]) / min(subsets[False]) > 1.0
+
+
+@pytest.mark.parametrize("norm", [True, False])
+def test_decoder_layer_matches_reference_math(cuda, norm):
+    """f2: the decoder layer around the path (simhost.cpp:196-207, 431-436) against an fp32
+    restatement of the same math whose attention is the C oracle's Spava layer on the
+    same (bf16-rounded) q, k, v."""
+    import torch
+
+    from paper_2601_21444_b200 import spava
+
+    n_v, n_t, l_a, l_p, hq, hkv, D, ffn = 1500, 32, 32, 96, 4, 2, 512, 1024
+    plan = spava.make_plan(n_v, n_t, 1, l_a, l_p)
+    cfg = spava.LayerConfig.make(n_v, n_t, 1, l_a, l_p, hq, hkv)
+    fab = spava.Fabric(cfg, 0)
+    host = fab.host(0)
+    rows = host.rows
+    g = torch.Generator(device=cuda).manual_seed(41)
+    bf = lambda *s, sc=1.0: (torch.randn(*s, device=cuda, generator=g) * sc).to(torch.bfloat16)
+    x = bf(rows, D)
+    w_qkv = bf(D, (hq + 2 * hkv) * 128, sc=D ** -0.5)
+    w_o = bf(hq * 128, D, sc=(hq * 128) ** -0.5)
+    w_1 = bf(D, ffn, sc=D ** -0.5)
+    w_2 = bf(ffn, D, sc=ffn ** -0.5)
+    g_1 = (1 + 0.1 * torch.randn(D, device=cuda, generator=g)) if norm else None
+    g_2 = (1 + 0.1 * torch.randn(D, device=cuda, generator=g)) if norm else None
+    x0 = x.float().clone()
+    host.decoder_layer(x, w_qkv, w_o, w_1, w_2, g_1, g_2)
+    torch.cuda.synchronize()
+    assert host.status() == 0
+
+    def ln(t, gain):
+        if gain is None:
+            return t
+        return torch.nn.functional.layer_norm(t, (D,), eps=1e-5) * gain
+
+    xn = ln(x0, g_1).to(torch.bfloat16).float()
+    qkv = (xn @ w_qkv.float()).to(torch.bfloat16).float()
+    q, k, v = qkv[:, :hq * 128], qkv[:, hq * 128:(hq + hkv) * 128], qkv[:, (hq + hkv) * 128:]
+    want = O.spava_layer(q.cpu().numpy(), k.cpu().numpy(), v.cpu().numpy(), n_v, n_t, 1, l_a, l_p, hq, hkv, 128)
+    att = np.concatenate([want["anchor"], want["blocks"][0], want["blocks"][1], want["query"]])
+    a = torch.from_numpy(att).to(cuda).to(torch.bfloat16).float()
+    xr = x0 + a @ w_o.float()
+    f = ln(xr, g_2).to(torch.bfloat16).float()
+    h = torch.relu(f @ w_1.float()).to(torch.bfloat16).float()
+    xr = xr + h @ w_2.float()
+    got = x.float()
+    rl2 = ((got - xr).norm() / xr.norm()).item()
+    assert rl2 < 1.5e-2, rl2
+    host.close()
+    fab.close()
