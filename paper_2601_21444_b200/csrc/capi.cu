@@ -619,7 +619,7 @@ int spava_debug_attn_prof(uint64_t* out16) {
 }
 
 int spava_debug_attn_variant(int variant) {
-  if (attn_set_variant(variant) != 0) return fail(SPAVA_EINVAL, "attn_variant: -1 or 0..13");
+  if (attn_set_variant(variant) != 0) return fail(SPAVA_EINVAL, "attn_variant: -1 or 0..14");
   return SPAVA_OK;
 }
 
