@@ -3,10 +3,12 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C1] [--impl spava|reference]
 
-N>1 is launched by the driver under torch.distributed.run (one rank per GPU, NCCL).
+N>1 is launched by the driver under torch.distributed.run (one rank per GPU).
 Rank h is physical host h of the reference's partition (zigzag virtual pair (h, 2H-1-h));
-the three exchange rounds (pass1, pass2, qpartial) are in-place ncclAllGathers inside
-the C-ABI layer call.  A "step" is one Spava attention layer of the whole job:
+the three exchange rounds (pass1, pass2, qpartial) run inside the C-ABI layer call: by
+default as NVLink stores from the select-gather / query-merge kernels into the peers'
+IPC-mapped exchange buffers with epoch flags (`--fabric peer`), or as in-place
+ncclAllGathers on a comm stream (`--fabric nccl`).  A "step" is one Spava attention layer of the whole job:
 score -> select+pack -> exchange -> query / anchor / block attention -> lse merge
 (run_host's per-layer body, simhost.cpp:321-426, minus projections/FFN).
 
@@ -251,8 +253,10 @@ def reference_tokens_per_s(g, hq, hkv, threads, budget_s, seed=0):
 
 # --------------------------------------------------------------------- arms
 def dist_env():
-    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
-            int(os.environ.get("LOCAL_RANK", 0)))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if os.environ.get("SPAVA_BENCH_ONE_GPU") == "1":  # test aid: every rank on cuda:0 (gloo)
+        local = 0
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), local
 
 
 def run_reference_arm(args):
@@ -304,10 +308,23 @@ def run_spava_arm(args):
     hq, hkv = cfg["hq"], cfg["hkv"]
     lc = spava.LayerConfig.make(g["n_v"], g["n_t"], H, g["l_a"], g["l_p"], hq, hkv, DH)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        obj = [spava.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        fab = spava.Fabric(lc, local, unique_id=obj[0], world=world, rank=rank)
+        if os.environ.get("SPAVA_BENCH_ONE_GPU") == "1":
+            if args.fabric != "peer":
+                raise SystemExit("SPAVA_BENCH_ONE_GPU needs --fabric peer (NCCL refuses shared GPUs)")
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+        if args.fabric == "peer":
+            # exchange rounds as NVLink stores from the producing kernels (IPC-mapped peer
+            # exchange buffers) + epoch flags; torch.distributed only ships the handles
+            fab = spava.Fabric.create_peer(lc, local, world, rank)
+            handles = [None] * world
+            dist.all_gather_object(handles, fab.peer_handle())
+            fab.peer_open(handles)
+        else:
+            obj = [spava.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            fab = spava.Fabric(lc, local, unique_id=obj[0], world=world, rank=rank)
     else:
         fab = spava.Fabric(lc, local)
     host = fab.host(rank)
@@ -409,6 +426,9 @@ def run_spava_arm(args):
 
     if rank != 0:
         if world > 1:
+            torch.cuda.synchronize()
+            dist.barrier()  # peers store into this rank's exchange buffer until their last layer
+            dist.barrier()
             dist.destroy_process_group()
         return
 
@@ -580,6 +600,9 @@ def run_spava_arm(args):
                    "n_t": g["n_t"], "l_a": g["l_a"], "l_b": g["l_b"], "l_p": g["l_p"],
                    "hosts": H, "heads": f"{hq}q/{hkv}kv", "dh": DH, "layers_per_step": 1,
                    "parallelism": f"sp{H} (Spava zigzag virtual hosts, one per GPU)",
+                   "exchange": ("local" if world == 1 else
+                                "peer (NVLink stores from the select / merge kernels + epoch flags)"
+                                if args.fabric == "peer" else "nccl allgather"),
                    "l2": "flushed (256 MiB write) between timed steps, outside the events",
                    "scoring": "exact (bit-faithful to the reference)"},
         "e2e": {"value": tokens / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
@@ -593,9 +616,13 @@ def run_spava_arm(args):
     }
     line.update(extra)
     print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()
     host.close()
     fab.close()
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 
@@ -606,6 +633,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C1", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="spava", choices=["spava", "reference"])
+    ap.add_argument("--fabric", default="peer", choices=["peer", "nccl"],
+                    help="N>1 exchange: NVLink peer stores + flags (default) or NCCL allgathers")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds for the CPU baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true")

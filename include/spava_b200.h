@@ -167,7 +167,11 @@ int spava_mha_merge(int nparts, const float* const* outs, const float* const* ls
  *  - local: H simulated hosts on ONE device, exchange buffers shared in place
  *    (the reference's in-process mailbox); drive with spava_sim_layer.
  *  - nccl: one process per GPU; pass1/pass2/qpartial are in-place
- *    ncclAllGather on a dedicated comm stream, overlapped per Algorithm 1.  */
+ *    ncclAllGather on a dedicated comm stream, overlapped per Algorithm 1.
+ *  - peer: one process per GPU (<= 8, one node); no collective library -- the
+ *    select gather and the query split-merge kernels store their slot straight
+ *    into every peer GPU's exchange buffer over NVLink (IPC-mapped), and 32-bit
+ *    epoch flags written / waited by stream memory operations order the rounds. */
 typedef struct {
   int n_v, n_t, hosts, l_a, l_p;
   int zigzag;         /* HostTopology pairing                                 */
@@ -189,6 +193,20 @@ int spava_fabric_create_local(const spava_layer_cfg* cfg, int device, spava_fabr
 int spava_nccl_unique_id(void* unique_id_128);
 int spava_fabric_create_nccl(const spava_layer_cfg* cfg, int device, const void* unique_id_128,
                              int world, int rank, spava_fabric** out);
+/* Peer fabric (replaces GatherFabric::issue/wait, simhost.cpp:73-124).  Setup:
+ * create on every rank, exchange the 64-byte handles (any host channel, e.g.
+ * torch.distributed all_gather_object), then spava_fabric_peer_open with the
+ * world x 64-byte array in rank order.  All ranks must run the same number of
+ * layers.  Destroy only after every rank has synchronised its last layer (a
+ * barrier), since peers store into this rank's buffer.                        */
+#define SPAVA_PEER_HANDLE_BYTES 64
+int spava_fabric_create_peer(const spava_layer_cfg* cfg, int device, int world, int rank,
+                             spava_fabric** out);
+int spava_fabric_peer_handle(spava_fabric* fab, void* handle_64);
+int spava_fabric_peer_open(spava_fabric* fab, const void* handles_world_x_64);
+/* In-process variant (tests, one device): fabrics[r] = the peer fabric of rank r;
+ * each rank's layer must then run on its own stream (the flag waits are in-stream). */
+int spava_fabric_peer_attach(spava_fabric* const* fabrics, int world);
 int spava_fabric_destroy(spava_fabric* fab);
 
 int spava_host_create(spava_fabric* fab, int h, spava_host** out);

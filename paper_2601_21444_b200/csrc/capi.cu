@@ -124,6 +124,12 @@ struct Exchange {
   int32_t* passCnt[2] = {nullptr, nullptr};  // [H]
   float* qOut = nullptr;                     // [H x n_t x hq*dh]
   float* qLse = nullptr;                     // [H x n_t x hq]
+  // peer fabric flags (epochs): arrive[round][q] = last epoch whose round-`round` slot from
+  // host q has landed here (rounds 0 pass1, 1 pass2, 2 qpartial); done[q] = last epoch host
+  // q has finished reading its own exchange buffer (so this host may overwrite its slot there)
+  static constexpr size_t kFlagBytes = 4096;
+  static constexpr int kArrive = 0, kDone = 3 * 256;
+  uint32_t* flags = nullptr;
   void* base = nullptr;
 
   int alloc(const spava_layer_cfg& c, const spava_plan& p) {
@@ -135,7 +141,7 @@ struct Exchange {
     const size_t qo = H * std::max(p.n_t, 1) * dq * 4;
     const size_t ql = H * std::max(p.n_t, 1) * c.hq * 4;
     auto al = [](size_t x) { return (x + 255) / 256 * 256; };
-    const size_t total = 2 * (2 * al(kv) + al(idx) + al(cnt)) + al(qo) + al(ql);
+    const size_t total = 2 * (2 * al(kv) + al(idx) + al(cnt)) + al(qo) + al(ql) + kFlagBytes;
     CU_TRY(cudaMalloc(&base, total));
     CU_TRY(cudaMemset(base, 0, total));
     uint8_t* b = static_cast<uint8_t*>(base);
@@ -146,7 +152,8 @@ struct Exchange {
       passCnt[r] = reinterpret_cast<int32_t*>(b); b += al(cnt);
     }
     qOut = reinterpret_cast<float*>(b); b += al(qo);
-    qLse = reinterpret_cast<float*>(b);
+    qLse = reinterpret_cast<float*>(b); b += al(ql);
+    flags = reinterpret_cast<uint32_t*>(b);
     return SPAVA_OK;
   }
   void release() {
@@ -163,8 +170,20 @@ struct spava_fabric {
   int world = 1, rank = 0;
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;
-  Exchange shared;  // local mode
+  Exchange shared;  // local mode; the rank's own exchange buffer in peer mode
   cudaEvent_t trace_base = nullptr;  // common time origin of the hosts' traces
+  // peer (NVLink P2P) mode: every rank's exchange buffer mapped here (IPC or same process)
+  bool peer = false;
+  bool peer_ready = false;
+  uint32_t epoch = 0;                        // layers run on this fabric
+  uint8_t* peer_base[kMaxMergeParts] = {};   // [world]; own base at [rank]
+  bool peer_ipc[kMaxMergeParts] = {};        // opened through cudaIpcOpenMemHandle
+  // pointer p into the own exchange buffer, translated into peer q's copy (same layout)
+  template <typename T>
+  T* at_peer(int q, T* p) const {
+    const auto off = reinterpret_cast<const uint8_t*>(p) - static_cast<const uint8_t*>(shared.base);
+    return reinterpret_cast<T*>(peer_base[q] + off);
+  }
 };
 
 struct spava_host {
@@ -354,6 +373,40 @@ inline const void* row_ptr(const uint8_t* base, long long row, long long ld) {
 }
 
 // score + select + pack (lo then hi) into this host's exchange slots
+// ---- peer fabric: arrival / release flags (peer.cu) and the peers' copies of a slot
+uint32_t* arrive_flag(uint32_t* flags, int round, int q) { return flags + Exchange::kArrive + round * 256 + q; }
+uint32_t* done_flag(uint32_t* flags, int q) { return flags + Exchange::kDone + q; }
+
+// this rank's round-`round` slot has been stored into every peer: raise arrive[round][me]
+int peer_signal(spava_fabric* F, cudaStream_t s, int round) {
+  for (int q = 0; q < F->world; ++q)
+    if (q != F->rank) CU_TRY(stream_write_u32(s, arrive_flag(F->at_peer(q, F->shared.flags), round, F->rank), F->epoch));
+  return SPAVA_OK;
+}
+
+// the stream waits until every peer's round-`round` slot of this epoch is here
+int peer_wait_arrive(spava_fabric* F, cudaStream_t s, int round) {
+  for (int q = 0; q < F->world; ++q)
+    if (q != F->rank) CU_TRY(stream_wait_geq_u32(s, arrive_flag(F->shared.flags, round, q), F->epoch));
+  return SPAVA_OK;
+}
+
+// the stream waits until every peer has finished reading the previous epoch's exchange, so
+// this rank may overwrite its slots in their buffers
+int peer_wait_done(spava_fabric* F, cudaStream_t s) {
+  if (F->epoch <= 1) return SPAVA_OK;
+  for (int q = 0; q < F->world; ++q)
+    if (q != F->rank) CU_TRY(stream_wait_geq_u32(s, done_flag(F->shared.flags, q), F->epoch - 1));
+  return SPAVA_OK;
+}
+
+// this rank has finished reading its exchange buffer for the epoch: tell every peer
+int peer_release(spava_fabric* F, cudaStream_t s) {
+  for (int q = 0; q < F->world; ++q)
+    if (q != F->rank) CU_TRY(stream_write_u32(s, done_flag(F->at_peer(q, F->shared.flags), F->rank), F->epoch));
+  return SPAVA_OK;
+}
+
 int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record) {
   const spava_fabric& F = *H->fab;
   const spava_layer_cfg& c = F.cfg;
@@ -387,13 +440,25 @@ int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record)
     const long long krow = p.l_a + static_cast<long long>(r) * p.l_b;
     const long long slot = static_cast<long long>(H->h) * p.l_p;
     int32_t* idx_out = H->ex->passIdx[r] + slot;
+    uint8_t* k_out = static_cast<uint8_t*>(H->ex->passK[r]) + slot * dk * 2;
+    uint8_t* v_out = static_cast<uint8_t*>(H->ex->passV[r]) + slot * dk * 2;
+    int32_t* cnt_out = H->ex->passCnt[r] + H->h;
+    PeerSlots peers{};
+    if (F.peer && p.l_p > 0)  // the gather also stores the slot into every peer's buffer
+      for (int q = 0; q < F.world; ++q)
+        if (q != F.rank) {
+          peers.k[peers.n] = F.at_peer(q, k_out);
+          peers.v[peers.n] = F.at_peer(q, v_out);
+          peers.idx[peers.n] = F.at_peer(q, idx_out);
+          peers.cnt[peers.n] = F.at_peer(q, cnt_out);
+          ++peers.n;
+        }
     const size_t t0 = mark(H, st);
     cudaError_t e = launch_select_pack(H->scores[r], p.l_b, p.l_p, p.l_a + vs[r] * p.l_b, row_ptr(b.k, krow, dk),
-                           row_ptr(b.v, krow, dk), dk, static_cast<int>(dk), idx_out,
-                           static_cast<uint8_t*>(H->ex->passK[r]) + slot * dk * 2,
-                           static_cast<uint8_t*>(H->ex->passV[r]) + slot * dk * 2, dk,
-                           H->ex->passCnt[r] + H->h, H->status, st);
+                           row_ptr(b.v, krow, dk), dk, static_cast<int>(dk), idx_out, k_out, v_out, dk,
+                           cnt_out, H->status, st, &peers);
     if (e != cudaSuccess) return fail(SPAVA_ECUDA, std::string("select: ") + cudaGetErrorString(e));
+    if (F.peer) ST_TRY(peer_signal(H->fab, st, r));
     g_launches += p.l_p > 0 ? 2 : 1;
     span(H, 2, t0, st);
     if (b.sel && p.l_p > 0)
@@ -429,7 +494,9 @@ int phase_query(spava_host* H, const HostBufs& b, cudaStream_t st, bool record) 
   pv.nseg = n;
   float* dst_out = H->ex->qOut + static_cast<long long>(H->h) * p.n_t * dq;
   float* dst_lse = H->ex->qLse + static_cast<long long>(H->h) * p.n_t * c.hq;
-  if (H->splits <= 1) {
+  // peer fabric: the split merge always runs (one part = exact copy) and stores the host's
+  // partial into every peer's qpartial slot as well
+  if (H->splits <= 1 && !F.peer) {
     pv.out = dst_out;
     pv.ldo = dq;
     pv.out_f32 = 1;
@@ -463,7 +530,15 @@ int phase_query(spava_host* H, const HostBufs& b, cudaStream_t st, bool record) 
     mp.dst_f32 = 1;
     mp.dst_lse = dst_lse;
     mp.status = nullptr;  // query partials may legitimately be empty rows
+    if (F.peer)
+      for (int q = 0; q < F.world; ++q)
+        if (q != F.rank) {
+          mp.peer_dst[mp.npeer] = F.at_peer(q, dst_out);
+          mp.peer_lse[mp.npeer] = F.at_peer(q, dst_lse);
+          ++mp.npeer;
+        }
     ST_TRY(merge_impl(mp, st, H));
+    if (F.peer) ST_TRY(peer_signal(H->fab, st, 2));
   }
   if (record) CU_TRY(cudaEventRecord(H->ev[2], st));
   return SPAVA_OK;
@@ -932,8 +1007,82 @@ int spava_fabric_create_nccl(const spava_layer_cfg* cfg, int device, const void*
   return SPAVA_OK;
 }
 
+int spava_fabric_create_peer(const spava_layer_cfg* cfg, int device, int world, int rank,
+                             spava_fabric** out) {
+  spava_plan plan;
+  ST_TRY(cfg_check(cfg, &plan));
+  if (world != cfg->hosts) return fail(SPAVA_EINVAL, "peer fabric: world size must equal hosts");
+  if (world > kMaxPeers + 1) return fail(SPAVA_EINVAL, "peer fabric: at most 8 GPUs");
+  if (rank < 0 || rank >= world) return fail(SPAVA_ERANGE, "peer fabric: rank");
+  CU_TRY(cudaSetDevice(device));
+  ST_TRY(require_device());
+  auto* F = new spava_fabric();
+  F->cfg = *cfg;
+  F->plan = plan;
+  F->device = device;
+  F->peer = true;
+  F->world = world;
+  F->rank = rank;
+  const int s = F->shared.alloc(*cfg, plan);
+  if (s != SPAVA_OK) {
+    delete F;
+    return s;
+  }
+  F->peer_base[rank] = static_cast<uint8_t*>(F->shared.base);
+  F->peer_ready = world == 1;
+  *out = F;
+  return SPAVA_OK;
+}
+
+int spava_fabric_peer_handle(spava_fabric* F, void* handle) {
+  if (!F || !F->peer) return fail(SPAVA_EINVAL, "peer_handle: not a peer fabric");
+  if (!handle) return fail(SPAVA_EINVAL, "peer_handle: null handle buffer");
+  static_assert(sizeof(cudaIpcMemHandle_t) == SPAVA_PEER_HANDLE_BYTES, "IPC handle size");
+  CU_TRY(cudaSetDevice(F->device));
+  cudaIpcMemHandle_t h;
+  CU_TRY(cudaIpcGetMemHandle(&h, F->shared.base));
+  std::memcpy(handle, &h, sizeof(h));
+  return SPAVA_OK;
+}
+
+int spava_fabric_peer_open(spava_fabric* F, const void* handles) {
+  if (!F || !F->peer) return fail(SPAVA_EINVAL, "peer_open: not a peer fabric");
+  if (F->peer_ready) return fail(SPAVA_EINVAL, "peer_open: peers already open");
+  if (!handles) return fail(SPAVA_EINVAL, "peer_open: null handles");
+  CU_TRY(cudaSetDevice(F->device));
+  const auto* hb = static_cast<const uint8_t*>(handles);
+  for (int q = 0; q < F->world; ++q) {
+    if (q == F->rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, hb + static_cast<size_t>(q) * SPAVA_PEER_HANDLE_BYTES, sizeof(h));
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(SPAVA_ECUDA, std::string("peer_open: rank ") + std::to_string(q) + ": " + cudaGetErrorString(e));
+    F->peer_base[q] = static_cast<uint8_t*>(p);
+    F->peer_ipc[q] = true;
+  }
+  F->peer_ready = true;
+  return SPAVA_OK;
+}
+
+int spava_fabric_peer_attach(spava_fabric* const* fabrics, int world) {
+  if (!fabrics || world < 1) return fail(SPAVA_EINVAL, "peer_attach: no fabrics");
+  for (int r = 0; r < world; ++r) {
+    const spava_fabric* F = fabrics[r];
+    if (!F || !F->peer || F->world != world || F->rank != r || F->peer_ready != (world == 1))
+      return fail(SPAVA_EINVAL, "peer_attach: fabrics[r] must be a fresh peer fabric of rank r");
+    if (F->device != fabrics[0]->device) return fail(SPAVA_EINVAL, "peer_attach: one device only");
+  }
+  for (int r = 0; r < world; ++r)
+    for (int q = 0; q < world; ++q) fabrics[r]->peer_base[q] = static_cast<uint8_t*>(fabrics[q]->shared.base);
+  for (int r = 0; r < world; ++r) fabrics[r]->peer_ready = true;
+  return SPAVA_OK;
+}
+
 int spava_fabric_destroy(spava_fabric* F) {
   if (!F) return SPAVA_OK;
+  for (int q = 0; q < kMaxMergeParts; ++q)
+    if (F->peer_ipc[q]) cudaIpcCloseMemHandle(F->peer_base[q]);
   if (F->comm) ncclCommDestroy(F->comm);
   if (F->comm_stream) cudaStreamDestroy(F->comm_stream);
   if (F->trace_base) cudaEventDestroy(F->trace_base);
@@ -965,7 +1114,7 @@ int spava_host_create(spava_fabric* F, int h, spava_host** out) {
   const spava_plan& p = F->plan;
   const spava_layer_cfg& c = F->cfg;
   if (h < 0 || h >= p.hosts) return fail(SPAVA_ERANGE, "host_create: host index");
-  if (F->nccl && h != F->rank) return fail(SPAVA_EINVAL, "host_create: nccl host must equal rank");
+  if ((F->nccl || F->peer) && h != F->rank) return fail(SPAVA_EINVAL, "host_create: nccl/peer host must equal rank");
   CU_TRY(cudaSetDevice(F->device));
   auto* H = new spava_host();
   H->fab = F;
@@ -1114,7 +1263,7 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
   CU_TRY(need_kvq(st));
   CU_TRY(launch_delay(H->delay_ns[0], ss));
   CU_TRY(launch_delay(H->delay_ns[2], st));
-  if (!F->nccl) {
+  if (!F->nccl && !F->peer) {
     // H = 1: block lo (v = 0) has no passing segment, so only stage 2 waits for selection
     ST_TRY(phase_select(H, b, ss, false));
     CU_TRY(cudaEventRecord(H->ev_sel, ss));
@@ -1144,38 +1293,65 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     if (H->trace) ++H->trace_layer;
     return merged(st) == cudaSuccess ? SPAVA_OK : fail(SPAVA_ECUDA, "event record");
   }
+  // exchange rounds: NCCL in-place allgathers on the comm stream, or (peer fabric) stores
+  // by the producing kernels into every peer's slot + epoch flags (no comm stream)
   cudaStream_t cs = F->comm_stream;
+  if (F->peer) {
+    if (!F->peer_ready) return fail(SPAVA_EINVAL, "peer fabric: peers not opened");
+    ++F->epoch;
+    ST_TRY(peer_wait_done(F, ss));  // peers have released the previous epoch's slots
+    ST_TRY(peer_wait_done(F, st));
+  }
   ST_TRY(phase_select(H, b, ss, true));  // records pass1_ready, pass2_ready on ss
   CU_TRY(cudaEventRecord(H->ev_sel, ss));
-  CU_TRY(cudaStreamWaitEvent(cs, H->ev[0], 0));
-  CU_TRY(launch_delay(H->delay_ns[1], cs));
-  T(cs, kCommIssued, "pass1", true);
-  ST_TRY(nccl_round(F, H->ex, 0));
-  CU_TRY(cudaEventRecord(H->ev[3], cs));
-  CU_TRY(cudaStreamWaitEvent(cs, H->ev[1], 0));
-  T(cs, kCommIssued, "pass2", true);
-  ST_TRY(nccl_round(F, H->ex, 1));
-  CU_TRY(cudaEventRecord(H->ev[4], cs));
+  if (F->peer) {
+    T(ss, kCommIssued, "pass1", true);
+    T(ss, kCommIssued, "pass2", true);
+  } else {
+    CU_TRY(cudaStreamWaitEvent(cs, H->ev[0], 0));
+    CU_TRY(launch_delay(H->delay_ns[1], cs));
+    T(cs, kCommIssued, "pass1", true);
+    ST_TRY(nccl_round(F, H->ex, 0));
+    CU_TRY(cudaEventRecord(H->ev[3], cs));
+    CU_TRY(cudaStreamWaitEvent(cs, H->ev[1], 0));
+    T(cs, kCommIssued, "pass2", true);
+    ST_TRY(nccl_round(F, H->ex, 1));
+    CU_TRY(cudaEventRecord(H->ev[4], cs));
+  }
   T(st, kComputeBegin, "query_attn");
   ST_TRY(phase_query(H, b, st, true));  // overlaps scoring and the pass rounds
   T(st, kComputeEnd, "query_attn");
-  CU_TRY(cudaStreamWaitEvent(cs, H->ev[2], 0));
-  T(cs, kCommIssued, "qpartial", true);
-  ST_TRY(nccl_qround(F, H->ex));
-  CU_TRY(cudaEventRecord(H->ev[5], cs));
+  if (F->peer) {
+    T(st, kCommIssued, "qpartial", true);
+  } else {
+    CU_TRY(cudaStreamWaitEvent(cs, H->ev[2], 0));
+    T(cs, kCommIssued, "qpartial", true);
+    ST_TRY(nccl_qround(F, H->ex));
+    CU_TRY(cudaEventRecord(H->ev[5], cs));
+  }
+  // st waits for round k (0 pass1, 1 pass2, 2 qpartial) of every host
+  auto wait_round = [&](int k) -> int {
+    if (!F->peer) {
+      CU_TRY(cudaStreamWaitEvent(st, H->ev[3 + k], 0));
+      return SPAVA_OK;
+    }
+    ST_TRY(peer_wait_arrive(F, st, k));
+    if (k < 2) CU_TRY(cudaStreamWaitEvent(st, H->ev[k], 0));  // own slot, written on ss
+    return SPAVA_OK;
+  };
   T(st, kCommWaitStart, "pass1", true);
-  CU_TRY(cudaStreamWaitEvent(st, H->ev[3], 0));
+  ST_TRY(wait_round(0));
   T(st, kCommCompleted, "pass1", true);
   if (!F->plan.zigzag) {  // simhost.cpp:392-402
     T(st, kCommWaitStart, "pass2", true);
-    CU_TRY(cudaStreamWaitEvent(st, H->ev[4], 0));
+    ST_TRY(wait_round(1));
     T(st, kCommCompleted, "pass2", true);
   }
   CU_TRY(launch_delay(H->delay_ns[3], st));
   if (!cp.on && merged_stages()) {  // both rounds in, then one launch for both blocks
     if (F->plan.zigzag) {
       T(st, kCommWaitStart, "pass2", true);
-      CU_TRY(cudaStreamWaitEvent(st, H->ev[4], 0));
+      ST_TRY(wait_round(1));
       T(st, kCommCompleted, "pass2", true);
     }
     CU_TRY(cudaStreamWaitEvent(st, H->ev_sel, 0));
@@ -1190,7 +1366,7 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     T(st, kComputeEnd, "stage1");
     if (F->plan.zigzag) {
       T(st, kCommWaitStart, "pass2", true);
-      CU_TRY(cudaStreamWaitEvent(st, H->ev[4], 0));
+      ST_TRY(wait_round(1));
       T(st, kCommCompleted, "pass2", true);
     }
     CU_TRY(cudaStreamWaitEvent(st, H->ev_sel, 0));  // join the side stream (sel copy-out)
@@ -1199,11 +1375,12 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     T(st, kComputeEnd, "stage2");
   }
   T(st, kCommWaitStart, "qpartial", true);
-  CU_TRY(cudaStreamWaitEvent(st, H->ev[5], 0));
+  ST_TRY(wait_round(2));
   T(st, kCommCompleted, "qpartial", true);
   T(st, kComputeBegin, "merge");
   ST_TRY(phase_merge(H, b, st));
   T(st, kComputeEnd, "merge");
+  if (F->peer) ST_TRY(peer_release(F, st));  // the exchange buffer of this epoch is read
   if (H->trace) ++H->trace_layer;
   return merged(st) == cudaSuccess ? SPAVA_OK : fail(SPAVA_ECUDA, "event record");
 }
@@ -1213,7 +1390,7 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
 int spava_host_layer(spava_host* H, const void* q, const void* k, const void* v, void* out,
                      int32_t* sel, void* stream) {
   spava_fabric* F = H->fab;
-  if (!F->nccl && F->plan.hosts != 1)
+  if (!F->nccl && !F->peer && F->plan.hosts != 1)
     return fail(SPAVA_EINVAL, "host_layer: local fabric with H > 1 must be driven by spava_sim_layer");
   CU_TRY(cudaSetDevice(F->device));
   HostBufs b{static_cast<const uint8_t*>(q), static_cast<const uint8_t*>(k),
@@ -1225,7 +1402,7 @@ int spava_host_layer_hostbuf(spava_host* H, const void* q_h, const void* k_h, co
                              void* out_h, int32_t* sel_h, void* q_d, void* k_d, void* v_d,
                              void* out_d, int32_t* sel_d, void* stream) {
   spava_fabric* F = H->fab;
-  if (!F->nccl && F->plan.hosts != 1)
+  if (!F->nccl && !F->peer && F->plan.hosts != 1)
     return fail(SPAVA_EINVAL, "host_layer_hostbuf: local fabric with H > 1 must be driven by spava_sim_layer");
   if (!q_h || !k_h || !v_h || !out_h || !q_d || !k_d || !v_d || !out_d)
     return fail(SPAVA_EINVAL, "host_layer_hostbuf: null buffer");
@@ -1289,7 +1466,7 @@ int spava_host_layer_hostbuf(spava_host* H, const void* q_h, const void* k_h, co
 int spava_sim_layer(spava_fabric* F, spava_host* const* hosts, const void* const* q,
                     const void* const* k, const void* const* v, void* const* out,
                     int32_t* const* sel, void* stream) {
-  if (!F || F->nccl) return fail(SPAVA_EINVAL, "sim_layer: needs a local fabric");
+  if (!F || F->nccl || F->peer) return fail(SPAVA_EINVAL, "sim_layer: needs a local fabric");
   CU_TRY(cudaSetDevice(F->device));
   cudaStream_t st = as_stream(stream);
   const int H = F->plan.hosts;
@@ -1566,6 +1743,7 @@ int spava_host_capture_layer(spava_host* H, const void* q, const void* k, const 
   spava_fabric* F = H->fab;
   if (!F->nccl && F->plan.hosts != 1)
     return fail(SPAVA_EINVAL, "capture_layer: local fabric with H > 1 must be driven by spava_sim_layer");
+  if (F->peer) return fail(SPAVA_EINVAL, "capture_layer: the peer fabric's epoch flags change every layer");
   if (H->timing || H->trace) return fail(SPAVA_EINVAL, "capture_layer: disable timing and trace first");
   if (!stream) return fail(SPAVA_EINVAL, "capture_layer: needs a non-default stream");
   CU_TRY(cudaSetDevice(F->device));

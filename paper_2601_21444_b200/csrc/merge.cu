@@ -70,12 +70,20 @@ __global__ void merge_kernel(const __grid_constant__ MergeParams p) {
   else
     static_cast<__nv_bfloat16*>(p.dst)[d] = __float2bfloat16_rn(acc);
   if (p.dst_lse && c == 0) p.dst_lse[static_cast<long long>(i) * p.hq + h] = lse_sh;
+  // peer fabric: the qpartial round is this kernel's epilogue (NVLink stores into every
+  // peer's slot); only the f32 slot layout is ever published
+  for (int q = 0; q < p.npeer; ++q) {
+    static_cast<float*>(p.peer_dst[q])[d] = acc;
+    if (c == 0) p.peer_lse[q][static_cast<long long>(i) * p.hq + h] = lse_sh;
+  }
 }
 
 }  // namespace
 
 cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream) {
   if (p.nparts < 1 || p.nparts > kMaxMergeParts || p.dh < 32 || p.dh > 1024) return cudaErrorInvalidValue;
+  if (p.npeer < 0 || p.npeer > kMaxPeers || (p.npeer > 0 && (!p.dst_f32 || !p.dst_lse)))
+    return cudaErrorInvalidValue;
   if (p.rows == 0) return cudaSuccess;
   merge_kernel<<<dim3(p.rows, p.hq), p.dh, 0, stream>>>(p);
   return cudaGetLastError();

@@ -201,27 +201,33 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const float* __rest
 }
 
 // warp per selected row; rows >= count are zero-filled so the slot is well defined.
+// Peer fabric: the same rows (and the slot's index list / count) are also stored straight
+// into every peer GPU's exchange slot over NVLink -- the pass round is this kernel's
+// epilogue, no separate collective.
 __global__ void gather_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ count,
                               int global_offset, int l_p, const uint4* __restrict__ k,
                               const uint4* __restrict__ v, long long ld16, int w16,
                               uint4* __restrict__ k_out, uint4* __restrict__ v_out,
-                              long long ld_out16) {
+                              long long ld_out16, const __grid_constant__ PeerSlots peers) {
   const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (r >= l_p) return;
   const int n = *count;
-  uint4* ko = k_out + r * ld_out16;
-  uint4* vo = v_out + r * ld_out16;
-  if (r < n) {
-    const long long src = static_cast<long long>(idx[r] - global_offset) * ld16;
-    for (int c = lane; c < w16; c += 32) {
-      ko[c] = k[src + c];
-      vo[c] = v[src + c];
+  const long long o = r * ld_out16;
+  if (lane == 0)
+    for (int q = 0; q < peers.n; ++q) {
+      static_cast<int32_t*>(peers.idx[q])[r] = idx[r];
+      if (r == 0) *static_cast<int32_t*>(peers.cnt[q]) = n;
     }
-  } else {
-    for (int c = lane; c < w16; c += 32) {
-      ko[c] = make_uint4(0, 0, 0, 0);
-      vo[c] = make_uint4(0, 0, 0, 0);
+  const long long src = r < n ? static_cast<long long>(idx[r] - global_offset) * ld16 : 0;
+  for (int c = lane; c < w16; c += 32) {
+    const uint4 kx = r < n ? k[src + c] : make_uint4(0, 0, 0, 0);
+    const uint4 vx = r < n ? v[src + c] : make_uint4(0, 0, 0, 0);
+    k_out[o + c] = kx;
+    v_out[o + c] = vx;
+    for (int q = 0; q < peers.n; ++q) {
+      static_cast<uint4*>(peers.k[q])[o + c] = kx;
+      static_cast<uint4*>(peers.v[q])[o + c] = vx;
     }
   }
 }
@@ -231,13 +237,17 @@ __global__ void gather_kernel(const int32_t* __restrict__ idx, const int32_t* __
 cudaError_t launch_select_pack(const float* scores, int l_b, int l_p, int global_offset,
                                const void* k, const void* v, long long ld, int width, int32_t* idx,
                                void* k_out, void* v_out, long long ld_out, int32_t* count,
-                               int32_t* status, cudaStream_t stream) {
+                               int32_t* status, cudaStream_t stream, const PeerSlots* peers) {
   if (l_p < 0 || l_p > l_b || (width % 8) || (ld % 8) || (ld_out % 8)) return cudaErrorInvalidValue;
+  if (peers && (peers->n < 0 || peers->n > kMaxPeers)) return cudaErrorInvalidValue;
   select_kernel<<<1, kSelThreads, 0, stream>>>(scores, l_b, l_p, global_offset, idx, count, status);
   if (l_p > 0 && k_out && v_out) {
     gather_kernel<<<(l_p + 7) / 8, 256, 0, stream>>>(
         idx, count, global_offset, l_p, static_cast<const uint4*>(k), static_cast<const uint4*>(v),
-        ld / 8, width / 8, static_cast<uint4*>(k_out), static_cast<uint4*>(v_out), ld_out / 8);
+        ld / 8, width / 8, static_cast<uint4*>(k_out), static_cast<uint4*>(v_out), ld_out / 8,
+        peers ? *peers : PeerSlots{});
+  } else if (peers && peers->n > 0) {
+    return cudaErrorInvalidValue;  // a peer slot is only published through the gather
   }
   return cudaGetLastError();
 }

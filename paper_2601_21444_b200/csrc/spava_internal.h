@@ -104,10 +104,22 @@ cudaError_t launch_score_fast2(int nblk, const void* q, long long ldq, int n_t,
                                cudaStream_t stream, std::string* err);
 
 // ---------------------------------------------------------------- selection
+// peer fabric: the same slot in up to kMaxPeers other GPUs' exchange buffers (IPC-mapped)
+constexpr int kMaxPeers = 7;
+struct PeerSlots {
+  void* k[kMaxPeers];
+  void* v[kMaxPeers];
+  void* idx[kMaxPeers];
+  void* cnt[kMaxPeers];
+  int n;
+};
 cudaError_t launch_select_pack(const float* scores, int l_b, int l_p, int global_offset,
                                const void* k, const void* v, long long ld, int width, int32_t* idx,
                                void* k_out, void* v_out, long long ld_out, int32_t* count,
-                               int32_t* status, cudaStream_t stream);
+                               int32_t* status, cudaStream_t stream, const PeerSlots* peers = nullptr);
+// stream memory operations (driver API): the peer fabric's arrival / release flags
+cudaError_t stream_write_u32(cudaStream_t s, uint32_t* addr, uint32_t value);
+cudaError_t stream_wait_geq_u32(cudaStream_t s, const uint32_t* addr, uint32_t value);
 
 // ---------------------------------------------------------------- split_context rows
 cudaError_t launch_split_rows(int l_a, int l_b, int n_t, int n_v, int lo, int hi, const void* src,
@@ -137,6 +149,10 @@ struct MergeParams {
   int dst_f32;
   float* dst_lse;  // nullable [rows][hq]
   int32_t* status; // nullable; set to 1 if a row is invalid in every part
+  // peer fabric: the merged rows / lse are also stored into these peers' slots (same layout)
+  int npeer;
+  void* peer_dst[kMaxPeers];
+  float* peer_lse[kMaxPeers];
 };
 cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream);
 cudaError_t launch_delay(unsigned long long ns, cudaStream_t stream);  // test: stream delay

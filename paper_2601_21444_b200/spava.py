@@ -35,6 +35,8 @@ EXPORTED_SYMBOLS = [
     "spava_score_block_fast", "spava_select_pack",
     "spava_attention_workspace", "spava_attention", "spava_mha_merge",
     "spava_fabric_create_local", "spava_nccl_unique_id", "spava_fabric_create_nccl",
+    "spava_fabric_create_peer", "spava_fabric_peer_handle", "spava_fabric_peer_open",
+    "spava_fabric_peer_attach",
     "spava_fabric_destroy", "spava_host_create", "spava_host_destroy", "spava_host_plan",
     "spava_host_rows", "spava_host_layer", "spava_host_layer_hostbuf", "spava_sim_layer",
     "spava_sim_layer_timed", "spava_host_set_trace", "spava_host_trace_read",
@@ -573,20 +575,50 @@ class Host:
             pass
 
 
-class Fabric:
-    """GatherFabric (simhost.cpp:61-166) equivalent: local (one device) or NCCL."""
+PEER_HANDLE_BYTES = 64
 
-    def __init__(self, cfg: LayerConfig, device=0, unique_id=None, world=1, rank=0):
+
+class Fabric:
+    """GatherFabric (simhost.cpp:61-166) equivalent: local (one device), NCCL, or peer
+    (NVLink P2P stores from the producing kernels + epoch flags; `Fabric.peer`)."""
+
+    def __init__(self, cfg: LayerConfig, device=0, unique_id=None, world=1, rank=0,
+                 peer=False):
         self.cfg = cfg
         self._p = C.c_void_p()
-        if unique_id is None:
+        self.nccl = self.peer = False
+        if peer:
+            _check(lib().spava_fabric_create_peer(C.byref(cfg), device, world, rank,
+                                                  C.byref(self._p)))
+            self.peer = True
+        elif unique_id is None:
             _check(lib().spava_fabric_create_local(C.byref(cfg), device, C.byref(self._p)))
-            self.nccl = False
         else:
             buf = C.create_string_buffer(unique_id, 128)
             _check(lib().spava_fabric_create_nccl(C.byref(cfg), device, buf, world, rank,
                                                   C.byref(self._p)))
             self.nccl = True
+
+    @classmethod
+    def create_peer(cls, cfg: LayerConfig, device, world, rank):
+        return cls(cfg, device, world=world, rank=rank, peer=True)
+
+    def peer_handle(self) -> bytes:
+        """64-byte IPC handle of this rank's exchange buffer (send it to every rank)."""
+        buf = C.create_string_buffer(PEER_HANDLE_BYTES)
+        _check(lib().spava_fabric_peer_handle(self._p, buf))
+        return buf.raw
+
+    def peer_open(self, handles):
+        """Map every other rank's exchange buffer; `handles` = the ranks' handles in order."""
+        blob = b"".join(handles)
+        _check(lib().spava_fabric_peer_open(self._p, C.create_string_buffer(blob, len(blob))))
+
+    @staticmethod
+    def peer_attach(fabrics):
+        """In-process peer fabrics (one device): fabrics[r] is rank r."""
+        n = len(fabrics)
+        _check(lib().spava_fabric_peer_attach((C.c_void_p * n)(*[f._p.value for f in fabrics]), n))
 
     def host(self, h) -> Host:
         return Host(self, h)

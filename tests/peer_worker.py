@@ -1,0 +1,128 @@
+"""Peer-fabric (NVLink P2P) worker for tests/test_gpu_peer.py -- run as a subprocess so
+CUDA_DEVICE_MAX_CONNECTIONS and the process layout are under the test's control.
+
+  python -m tests.peer_worker inproc WORLD LAYERS   one process, WORLD peer fabrics on
+                                                    cuda:0, each rank on its own stream
+  python -m tests.peer_worker rank RANK WORLD LAYERS PORT
+                                                    one rank of a WORLD-process job on
+                                                    cuda:0 (IPC handles over gloo)
+
+Every rank runs LAYERS consecutive layers (different inputs each, so the epoch flags and
+the slot-release protocol are exercised) and checks its outputs and passing indices
+bit-identical against the local fabric (spava_sim_layer) on the same inputs.
+Prints one line "PEER_OK <rank|all> <layers>" on success.
+"""
+import os
+import sys
+
+import torch
+
+from paper_2601_21444_b200 import spava
+
+N_V, N_T, L_A, L_P, HQ, HKV = 5000, 64, 64, 160, 8, 2
+
+
+def inputs(world, layer):
+    """Per-host [anchor | lo | hi | query] buffers of one layer (same on every rank)."""
+    cfg = spava.LayerConfig.make(N_V, N_T, world, L_A, L_P, HQ, HKV)
+    plan = spava.make_plan(N_V, N_T, world, L_A, L_P, True)
+    rows = L_A + 2 * plan.l_b + N_T
+    g = torch.Generator(device="cuda:0").manual_seed(1000 + layer)
+    qs, ks, vs = [], [], []
+    for _ in range(world):
+        qs.append(torch.randn(rows, HQ * 128, device="cuda:0", generator=g).to(torch.bfloat16))
+        ks.append(torch.randn(rows, HKV * 128, device="cuda:0", generator=g).to(torch.bfloat16))
+        vs.append(torch.randn(rows, HKV * 128, device="cuda:0", generator=g).to(torch.bfloat16))
+    return cfg, rows, qs, ks, vs
+
+
+def reference(world, layers):
+    """Local fabric (the in-process GatherFabric) outputs, per layer and host."""
+    res = []
+    for layer in range(layers):
+        cfg, rows, qs, ks, vs = inputs(world, layer)
+        fab = spava.Fabric(cfg, 0)
+        hs = [fab.host(h) for h in range(world)]
+        outs = [torch.zeros(rows, HQ * 128, dtype=torch.bfloat16, device="cuda:0") for _ in hs]
+        sels = [torch.zeros(2, L_P, dtype=torch.int32, device="cuda:0") for _ in hs]
+        fab.sim_layer(hs, qs, ks, vs, outs, sels)
+        torch.cuda.synchronize()
+        assert all(h.status() == 0 for h in hs)
+        res.append((outs, sels))
+        for h in hs:
+            h.close()
+        fab.close()
+    return res
+
+
+def check(ref, layer, rank, out, sel):
+    want_out, want_sel = ref[layer][0][rank], ref[layer][1][rank]
+    if not torch.equal(sel, want_sel):
+        raise AssertionError(f"layer {layer} rank {rank}: passing indices differ")
+    if not torch.equal(out, want_out):
+        d = (out.float() - want_out.float()).abs().max().item()
+        raise AssertionError(f"layer {layer} rank {rank}: output differs (max {d})")
+
+
+def inproc(world, layers):
+    ref = reference(world, layers)
+    cfg, rows, _, _, _ = inputs(world, 0)
+    fabs = [spava.Fabric.create_peer(cfg, 0, world, r) for r in range(world)]
+    spava.Fabric.peer_attach(fabs)
+    hosts = [f.host(r) for r, f in enumerate(fabs)]
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    for layer in range(layers):
+        _, _, qs, ks, vs = inputs(world, layer)
+        torch.cuda.synchronize()
+        outs = [torch.zeros(rows, HQ * 128, dtype=torch.bfloat16, device="cuda:0") for _ in hosts]
+        sels = [torch.zeros(2, L_P, dtype=torch.int32, device="cuda:0") for _ in hosts]
+        # enqueue every rank before any waits can be satisfied: the flag waits are in-stream
+        for r in range(world):
+            hosts[r].layer(qs[r], ks[r], vs[r], outs[r], sels[r], stream=streams[r])
+        torch.cuda.synchronize()
+        for r in range(world):
+            assert hosts[r].status() == 0
+            check(ref, layer, r, outs[r], sels[r])
+    for h in hosts:
+        h.close()
+    for f in fabs:
+        f.close()
+    print(f"PEER_OK all {layers}", flush=True)
+
+
+def one_rank(rank, world, layers, port):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ref = reference(world, layers)
+    cfg, rows, _, _, _ = inputs(world, 0)
+    fab = spava.Fabric.create_peer(cfg, 0, world, rank)
+    handles = [None] * world
+    dist.all_gather_object(handles, fab.peer_handle())
+    fab.peer_open(handles)
+    host = fab.host(rank)
+    stream = torch.cuda.Stream()
+    for layer in range(layers):
+        _, _, qs, ks, vs = inputs(world, layer)
+        torch.cuda.synchronize()
+        out = torch.zeros(rows, HQ * 128, dtype=torch.bfloat16, device="cuda:0")
+        sel = torch.zeros(2, L_P, dtype=torch.int32, device="cuda:0")
+        host.layer(qs[rank], ks[rank], vs[rank], out, sel, stream=stream)
+        stream.synchronize()
+        assert host.status() == 0
+        check(ref, layer, rank, out, sel)
+    dist.barrier()  # peers store into this rank's buffer until their last layer is done
+    host.close()
+    fab.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    print(f"PEER_OK {rank} {layers}", flush=True)
+
+
+if __name__ == "__main__":
+    mode = sys.argv[1]
+    if mode == "inproc":
+        inproc(int(sys.argv[2]), int(sys.argv[3]))
+    else:
+        one_rank(int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]))

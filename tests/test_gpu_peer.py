@@ -1,0 +1,62 @@
+"""GPU tests of the peer fabric (NVLink P2P exchange without a collective library).
+
+The pass rounds are stored by the select gather kernel and the qpartial round by the
+query split-merge kernel straight into every peer's exchange slot; epoch flags (stream
+memory operations) order them.  Parity bar: every rank's layer output and passing
+indices bit-identical to the local fabric (the reference's in-process GatherFabric
+order, simhost.cpp:61-166) over several consecutive layers.
+
+Only one GPU is available, so the ranks share cuda:0: either WORLD fabrics in one
+process on WORLD streams, or WORLD real processes that map each other's exchange
+buffers through CUDA IPC (the multi-GPU code path, minus NVLink itself).  Each runs in a
+subprocess under a timeout.
+"""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _env():
+    env = dict(os.environ)
+    env["CUDA_DEVICE_MAX_CONNECTIONS"] = "32"  # every rank stream its own hardware queue
+    env["PYTHONPATH"] = ROOT + os.pathsep + env.get("PYTHONPATH", "")
+    return env
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_fabric_inprocess_matches_local(cuda, world):
+    r = subprocess.run([sys.executable, "-m", "tests.peer_worker", "inproc", str(world), "3"],
+                       cwd=ROOT, env=_env(), capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0 and "PEER_OK all 3" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def test_peer_fabric_two_processes_ipc_matches_local(cuda):
+    world, port = 2, _free_port()
+    procs = [subprocess.Popen([sys.executable, "-m", "tests.peer_worker", "rank", str(r), str(world),
+                               "3", str(port)], cwd=ROOT, env=_env(), stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True) for r in range(world)]
+    outs = []
+    try:
+        for p in procs:
+            outs.append(p.communicate(timeout=300))
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    for r, (p, (o, e)) in enumerate(zip(procs, outs)):
+        assert p.returncode == 0 and f"PEER_OK {r} 3" in o, o[-2000:] + e[-4000:]
