@@ -122,53 +122,42 @@ __device__ __forceinline__ void load_exp_table(double* tab) {
   if (t < 16) tab[t] = c_exp2_16[t];
 }
 
-// Raw bf16 chunk staged in registers: the global loads of chunk c+1 are issued before the
-// FFMA2 loop of chunk c and converted + stored to smem (transposed, [c][row]) after it.
-struct RawChunk {
-  uint2 q[2], k[2];
-};
+// Raw bf16 chunks are staged by cp.async two chunks ahead (no registers held across the
+// FFMA2 loop -- a register prefetch was sunk by ptxas to just before its use, exposing
+// the full global latency every chunk).  Thread t copies 16 B (8 c of one row) of Q and
+// of K per chunk and later converts exactly those bytes, so cp.async.wait_group alone
+// orders copy and conversion (no barrier between them).
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* src, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-__device__ __forceinline__ void load_chunk(const ScoreArgs& a, const __nv_bfloat16* k, int h, int hk,
-                                           int r0, int j0, int c0, RawChunk& rc) {
-  // 256 threads x 4 bf16 x 2 = 128 rows x 16 c for Q, same for K (lane walks the row
-  // dimension so the transposed smem stores are conflict-free)
+// row / 8-c group of this thread's 16-byte piece (lanes walk rows: conflict-free STS later)
+__device__ __forceinline__ void issue_chunk(const ScoreArgs& a, const __nv_bfloat16* k, int h, int hk,
+                                            int r0, int j0, int c0, uint4* Rq, uint4* Rk) {
   const int tid = threadIdx.x;
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int e = tid + u * kThr;  // 0..511: row = e % 128, c-quad = e / 128
-    const int row = e % kTM, cq = (e / kTM) * 4;
-    rc.q[u] = make_uint2(0u, 0u);
-    rc.k[u] = make_uint2(0u, 0u);
-    if (r0 + row < a.n_t)
-      rc.q[u] = __ldg(reinterpret_cast<const uint2*>(a.q + static_cast<long long>(r0 + row) * a.ldq +
-                                                     h * kDh + c0 + cq));
-    if (j0 + row < a.l_b)
-      rc.k[u] = __ldg(reinterpret_cast<const uint2*>(k + static_cast<long long>(j0 + row) * a.ldk +
-                                                     hk * kDh + c0 + cq));
-  }
+  const int row = tid % kTM, c8 = (tid / kTM) * 8;
+  const bool vq = r0 + row < a.n_t, vk = j0 + row < a.l_b;
+  const __nv_bfloat16* sq = a.q + static_cast<long long>(vq ? r0 + row : 0) * a.ldq + h * kDh + c0 + c8;
+  const __nv_bfloat16* sk = k + static_cast<long long>(vk ? j0 + row : 0) * a.ldk + hk * kDh + c0 + c8;
+  cp_async16(Rq + tid, sq, vq);
+  cp_async16(Rk + tid, sk, vk);
 }
 
-__device__ __forceinline__ void bf16x4_to_f32(uint2 r, float (&f)[4]) {
-  f[0] = __uint_as_float(r.x << 16);
-  f[1] = __uint_as_float(r.x & 0xffff0000u);
-  f[2] = __uint_as_float(r.y << 16);
-  f[3] = __uint_as_float(r.y & 0xffff0000u);
-}
-
-__device__ __forceinline__ void store_chunk(float* Qs, float* Ks, const RawChunk& rc) {
+__device__ __forceinline__ void convert_chunk(float* Qs, float* Ks, const uint4* Rq, const uint4* Rk) {
   const int tid = threadIdx.x;
+  const int row = tid % kTM, c8 = (tid / kTM) * 8;
+  const uint4 q = Rq[tid], kk = Rk[tid];
+  const uint32_t qw[4] = {q.x, q.y, q.z, q.w}, kw[4] = {kk.x, kk.y, kk.z, kk.w};
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int e = tid + u * kThr;
-    const int row = e % kTM, cq = (e / kTM) * 4;
-    float qf[4], kf[4];
-    bf16x4_to_f32(rc.q[u], qf);
-    bf16x4_to_f32(rc.k[u], kf);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      Qs[(cq + c) * kTM + row] = qf[c];
-      Ks[(cq + c) * kTN + row] = kf[c];
-    }
+  for (int i = 0; i < 4; ++i) {
+    Qs[(c8 + 2 * i) * kTM + row] = __uint_as_float(qw[i] << 16);
+    Qs[(c8 + 2 * i + 1) * kTM + row] = __uint_as_float(qw[i] & 0xffff0000u);
+    Ks[(c8 + 2 * i) * kTN + row] = __uint_as_float(kw[i] << 16);
+    Ks[(c8 + 2 * i + 1) * kTN + row] = __uint_as_float(kw[i] & 0xffff0000u);
   }
 }
 
@@ -176,11 +165,14 @@ __device__ __forceinline__ void store_chunk(float* Qs, float* Ks, const RawChunk
 __global__ void __launch_bounds__(kThr, 2) logits_kernel(const __grid_constant__ ScoreArgs a) {
   __shared__ __align__(16) float Qs[2][kKC * kTM];
   __shared__ __align__(16) float Ks[2][kKC * kTN];
+  __shared__ __align__(16) uint4 Rq[2][kThr];  // raw bf16 chunks (cp.async ring)
+  __shared__ __align__(16) uint4 Rk[2][kThr];
   const int tile = blockIdx.x, h = blockIdx.y, blk = blockIdx.z;
   const int hk = h / (a.hq / a.hkv);
   const int j0 = tile * kTN;
   const __nv_bfloat16* k = a.k[blk];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  constexpr int kChunks = kDh / kKC;
   for (int r0 = 0; r0 < a.n_t; r0 += kTM) {
     // accumulators as fp32 pairs over adjacent keys: one packed FFMA2 (fma.rn.f32x2,
     // two independent IEEE fp32 FMAs) per pair -- sm_100's full fp32 rate.
@@ -189,14 +181,18 @@ __global__ void __launch_bounds__(kThr, 2) logits_kernel(const __grid_constant__
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc2[i][j] = make_float2(0.f, 0.f);
-    RawChunk rc;
-    load_chunk(a, k, h, hk, r0, j0, 0, rc);
-    store_chunk(Qs[0], Ks[0], rc);
+    issue_chunk(a, k, h, hk, r0, j0, 0, Rq[0], Rk[0]);
+    cp_async_commit();
+    issue_chunk(a, k, h, hk, r0, j0, kKC, Rq[1], Rk[1]);
+    cp_async_commit();
+    cp_async_wait1();
+    convert_chunk(Qs[0], Ks[0], Rq[0], Rk[0]);
     __syncthreads();
-    constexpr int kChunks = kDh / kKC;
     for (int ch = 0; ch < kChunks; ++ch) {
       const int cur = ch & 1;
-      if (ch + 1 < kChunks) load_chunk(a, k, h, hk, r0, j0, (ch + 1) * kKC, rc);
+      // chunk ch+2 into the raw slot this thread converted from last (its own bytes only)
+      if (ch + 2 < kChunks) issue_chunk(a, k, h, hk, r0, j0, (ch + 2) * kKC, Rq[cur], Rk[cur]);
+      cp_async_commit();
 #pragma unroll
       for (int c = 0; c < kKC; ++c) {  // ascending c within the chunk, chunks ascending
         const float4 qa = *reinterpret_cast<const float4*>(&Qs[cur][c * kTM + ty * 4]);
@@ -214,7 +210,8 @@ __global__ void __launch_bounds__(kThr, 2) logits_kernel(const __grid_constant__
         }
       }
       if (ch + 1 < kChunks) {
-        store_chunk(Qs[cur ^ 1], Ks[cur ^ 1], rc);
+        cp_async_wait1();  // chunk ch+1 landed (ch+2 may still be in flight)
+        convert_chunk(Qs[cur ^ 1], Ks[cur ^ 1], Rq[cur ^ 1], Rk[cur ^ 1]);
         __syncthreads();
       }
     }
