@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <cstdio>
 #include <string>
 #include <vector>
 
@@ -204,13 +205,18 @@ struct spava_host {
   // scoring runs on a high-priority side stream forked from the caller's stream, so the
   // CUDA-core/FP64 scorer overlaps the query / stage-1 attention that does not need it
   cudaStream_t side = nullptr;
+  // host-buffer layer: scoring on a LOW-priority side stream -- the copies, not the SMs,
+  // bound that path, so the row-chunk attention (whose outputs feed the D2H stream) goes
+  // first and the scorer fills the gaps (it is only needed by stage 2)
+  cudaStream_t side_lo = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_sel = nullptr;
   // host-buffer layer (spava_host_layer_hostbuf): H2D / D2H copy streams and their edges
   cudaStream_t h2d = nullptr, d2h = nullptr;
   // row-chunk pipeline: q rows of block lo / hi arrive in kCopyChunks chunks each; the
   // stage-1/2 attention runs per chunk and each chunk's output leaves as soon as it is final
-  static constexpr int kCopyChunks = 4;
-  cudaEvent_t ev_kvq = nullptr;                  // k, v and the query rows of q are on device
+  static constexpr int kCopyChunks = 5;
+  cudaEvent_t ev_kvq = nullptr;                  // all k and the query rows of q are on device (scorer)
+  cudaEvent_t ev_vhi = nullptr;                  // v rows of block hi and the query are on device
   cudaEvent_t ev_qc[2 * kCopyChunks] = {};       // q rows of chunk c (chunk 0 of lo + anchor)
   cudaEvent_t ev_oc[2 * kCopyChunks + 1] = {};   // output chunk c final (last: merged query)
   cudaEvent_t ev_d2h = nullptr;
@@ -407,7 +413,8 @@ int peer_release(spava_fabric* F, cudaStream_t s) {
   return SPAVA_OK;
 }
 
-int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record) {
+int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record,
+                 cudaEvent_t before_hi = nullptr) {
   const spava_fabric& F = *H->fab;
   const spava_layer_cfg& c = F.cfg;
   const spava_plan& p = F.plan;
@@ -443,6 +450,7 @@ int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record)
     uint8_t* k_out = static_cast<uint8_t*>(H->ex->passK[r]) + slot * dk * 2;
     uint8_t* v_out = static_cast<uint8_t*>(H->ex->passV[r]) + slot * dk * 2;
     int32_t* cnt_out = H->ex->passCnt[r] + H->h;
+    if (r == 1 && before_hi) CU_TRY(cudaStreamWaitEvent(st, before_hi, 0));  // v rows of hi
     PeerSlots peers{};
     if (F.peer && p.l_p > 0)  // the gather also stores the slot into every peer's buffer
       for (int q = 0; q < F.world; ++q)
@@ -1099,9 +1107,11 @@ int host_init_streams(spava_host* H) {
   int prio_lo = 0, prio_hi = 0;
   CU_TRY(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   CU_TRY(cudaStreamCreateWithPriority(&H->side, cudaStreamNonBlocking, prio_hi));
+  CU_TRY(cudaStreamCreateWithPriority(&H->side_lo, cudaStreamNonBlocking, prio_lo));
   CU_TRY(cudaStreamCreateWithFlags(&H->h2d, cudaStreamNonBlocking));
   CU_TRY(cudaStreamCreateWithFlags(&H->d2h, cudaStreamNonBlocking));
   CU_TRY(cudaEventCreateWithFlags(&H->ev_kvq, cudaEventDisableTiming));
+  CU_TRY(cudaEventCreateWithFlags(&H->ev_vhi, cudaEventDisableTiming));
   CU_TRY(cudaEventCreateWithFlags(&H->ev_d2h, cudaEventDisableTiming));
   for (auto& e : H->ev_qc) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto& e : H->ev_oc) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1174,6 +1184,7 @@ int spava_host_destroy(spava_host* H) {
   if (H->graph) cudaGraphDestroy(H->graph);
   gemm_handle_destroy(H->gemm);
   if (H->side) cudaStreamDestroy(H->side);
+  if (H->side_lo) cudaStreamDestroy(H->side_lo);
   if (H->h2d) cudaStreamDestroy(H->h2d);
   if (H->d2h) cudaStreamDestroy(H->d2h);
   for (auto& e : H->ev_qc)
@@ -1181,6 +1192,7 @@ int spava_host_destroy(spava_host* H) {
   for (auto& e : H->ev_oc)
     if (e) cudaEventDestroy(e);
   if (H->ev_kvq) cudaEventDestroy(H->ev_kvq);
+  if (H->ev_vhi) cudaEventDestroy(H->ev_vhi);
   if (H->ev_d2h) cudaEventDestroy(H->ev_d2h);
   for (auto& e : H->ev_pool) cudaEventDestroy(e);
   for (auto& e : H->trace_pool) cudaEventDestroy(e);
@@ -1211,30 +1223,39 @@ struct CopyEdges {
 };
 
 CopyEdges copy_edges(const spava_plan& p) {
+  // uneven row chunks (multiples of 256 rows, one ping-pong CTA unit): block lo runs its
+  // chunks in row order and block hi in REVERSE order, so the first output is ready early
+  // (small first lo chunk) and the last chunk to arrive is the smallest and lightest
+  // (causal rows [0, l_b/16) of hi) -- the tail after the last H2D byte is short
+  static constexpr int kFrac16[spava_host::kCopyChunks + 1] = {0, 1, 4, 8, 12, 16};
   CopyEdges cp;
   cp.on = true;
   const int n = spava_host::kCopyChunks;
-  for (int c = 0; c <= n; ++c) {  // multiples of 256 rows (one ping-pong CTA unit)
-    const long long r = (static_cast<long long>(p.l_b) * c / n + 255) / 256 * 256;
+  for (int c = 0; c <= n; ++c) {
+    const long long r = (static_cast<long long>(p.l_b) * kFrac16[c] / 16 + 255) / 256 * 256;
     cp.cb[c] = static_cast<int>(std::min<long long>(r, p.l_b));
   }
   cp.cb[n] = p.l_b;
   return cp;
 }
 
-// stage 1 / stage 2 as row chunks (copy pipeline) or whole blocks
+// row chunk of block `which` processed at position k (hi runs in reverse)
+inline int chunk_of(int which, int k) { return which == 0 ? k : spava_host::kCopyChunks - 1 - k; }
+
+// stage 1 / stage 2 as row chunks (copy pipeline) or whole blocks; events are indexed by
+// processing position
 int stage_chunks(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdges& cp, int which) {
   if (!cp.on) return which == 0 ? phase_stage1(H, b, st) : phase_stage2(H, b, st);
   const spava_layer_cfg& c = H->fab->cfg;
   const int n = spava_host::kCopyChunks;
   for (int k = 0; k < n; ++k) {
-    const int idx = which * n + k;
+    const int idx = which * n + k, rc = chunk_of(which, k);
     CU_TRY(cudaStreamWaitEvent(st, H->ev_qc[idx], 0));
-    if (cp.cb[k + 1] > cp.cb[k]) {
-      ProbView pv[2] = {block_chunk_problem(H, b, which, cp.cb[k], cp.cb[k + 1]), anchor_problem(H, b)};
-      const int np = (which == 0 && k == 0 && H->fab->plan.l_a > 0) ? 2 : 1;  // anchor with lo chunk 0
-      ST_TRY(attention_impl(pv, np, c.hq, c.hkv, c.dh, st, H));
-    } else if (which == 0 && k == 0 && H->fab->plan.l_a > 0) {
+    const bool anchor = which == 0 && k == 0 && H->fab->plan.l_a > 0;  // anchor with lo chunk 0
+    if (cp.cb[rc + 1] > cp.cb[rc]) {
+      ProbView pv[2] = {block_chunk_problem(H, b, which, cp.cb[rc], cp.cb[rc + 1]), anchor_problem(H, b)};
+      ST_TRY(attention_impl(pv, anchor ? 2 : 1, c.hq, c.hkv, c.dh, st, H));
+    } else if (anchor) {
       ProbView pa = anchor_problem(H, b);
       ST_TRY(attention_impl(&pa, 1, c.hq, c.hkv, c.dh, st, H));
     }
@@ -1245,10 +1266,7 @@ int stage_chunks(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEd
 
 int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdges& cp) {
   spava_fabric* F = H->fab;
-  cudaStream_t ss = H->serial ? st : H->side;
-  auto need_kvq = [&](cudaStream_t s) -> cudaError_t {
-    return cp.on ? cudaStreamWaitEvent(s, H->ev_kvq, 0) : cudaSuccess;
-  };
+  cudaStream_t ss = H->serial ? st : cp.on ? H->side_lo : H->side;
   auto merged = [&](cudaStream_t s) -> cudaError_t {
     return cp.on ? cudaEventRecord(H->ev_oc[2 * spava_host::kCopyChunks], s) : cudaSuccess;
   };
@@ -1256,29 +1274,38 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
   auto T = [&](cudaStream_t s, int kind, const char* label, bool comm = false) {
     trace_ev(H, s, kind, label, comm);
   };
+  // host-buffer pipeline (cp.on): the side stream starts once all k and the query rows are
+  // in (scorer); select hi additionally waits for v of block hi; the caller's stream waits
+  // per row chunk, and the query attention (it reads every key) runs after stage 1
+  cudaEvent_t before_hi = cp.on ? H->ev_vhi : nullptr;
   // fork: scoring + selection on the side stream (its inputs are this step's q/k on st)
   CU_TRY(cudaEventRecord(H->ev_fork, st));
   CU_TRY(cudaStreamWaitEvent(ss, H->ev_fork, 0));
-  CU_TRY(need_kvq(ss));
-  CU_TRY(need_kvq(st));
+  if (cp.on) CU_TRY(cudaStreamWaitEvent(ss, H->ev_kvq, 0));
   CU_TRY(launch_delay(H->delay_ns[0], ss));
   CU_TRY(launch_delay(H->delay_ns[2], st));
   if (!F->nccl && !F->peer) {
     // H = 1: block lo (v = 0) has no passing segment, so only stage 2 waits for selection
-    ST_TRY(phase_select(H, b, ss, false));
+    ST_TRY(phase_select(H, b, ss, false, before_hi));
     CU_TRY(cudaEventRecord(H->ev_sel, ss));
     T(ss, kCommIssued, "pass1", true);
     T(ss, kCommIssued, "pass2", true);
-    T(st, kComputeBegin, "query_attn");
-    ST_TRY(phase_query(H, b, st, false));
-    T(st, kComputeEnd, "query_attn");
-    T(st, kCommIssued, "qpartial", true);
+    auto query = [&]() -> int {
+      T(st, kComputeBegin, "query_attn");
+      if (cp.on) CU_TRY(cudaStreamWaitEvent(st, H->ev_vhi, 0));
+      ST_TRY(phase_query(H, b, st, false));
+      T(st, kComputeEnd, "query_attn");
+      T(st, kCommIssued, "qpartial", true);
+      return SPAVA_OK;
+    };
+    if (!cp.on) ST_TRY(query());
     T(st, kCommWaitStart, "pass1", true);
     T(st, kCommCompleted, "pass1", true);
     CU_TRY(launch_delay(H->delay_ns[3], st));
     T(st, kComputeBegin, "stage1");
     ST_TRY(stage_chunks(H, b, st, cp, 0));
     T(st, kComputeEnd, "stage1");
+    if (cp.on) ST_TRY(query());
     T(st, kCommWaitStart, "pass2", true);
     CU_TRY(cudaStreamWaitEvent(st, H->ev_sel, 0));
     T(st, kCommCompleted, "pass2", true);
@@ -1302,7 +1329,7 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     ST_TRY(peer_wait_done(F, ss));  // peers have released the previous epoch's slots
     ST_TRY(peer_wait_done(F, st));
   }
-  ST_TRY(phase_select(H, b, ss, true));  // records pass1_ready, pass2_ready on ss
+  ST_TRY(phase_select(H, b, ss, true, before_hi));  // records pass1_ready, pass2_ready on ss
   CU_TRY(cudaEventRecord(H->ev_sel, ss));
   if (F->peer) {
     T(ss, kCommIssued, "pass1", true);
@@ -1318,17 +1345,22 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     ST_TRY(nccl_round(F, H->ex, 1));
     CU_TRY(cudaEventRecord(H->ev[4], cs));
   }
-  T(st, kComputeBegin, "query_attn");
-  ST_TRY(phase_query(H, b, st, true));  // overlaps scoring and the pass rounds
-  T(st, kComputeEnd, "query_attn");
-  if (F->peer) {
-    T(st, kCommIssued, "qpartial", true);
-  } else {
-    CU_TRY(cudaStreamWaitEvent(cs, H->ev[2], 0));
-    T(cs, kCommIssued, "qpartial", true);
-    ST_TRY(nccl_qround(F, H->ex));
-    CU_TRY(cudaEventRecord(H->ev[5], cs));
-  }
+  auto query = [&]() -> int {
+    T(st, kComputeBegin, "query_attn");
+    if (cp.on) CU_TRY(cudaStreamWaitEvent(st, H->ev_vhi, 0));
+    ST_TRY(phase_query(H, b, st, true));  // overlaps scoring and the pass rounds
+    T(st, kComputeEnd, "query_attn");
+    if (F->peer) {
+      T(st, kCommIssued, "qpartial", true);
+    } else {
+      CU_TRY(cudaStreamWaitEvent(cs, H->ev[2], 0));
+      T(cs, kCommIssued, "qpartial", true);
+      ST_TRY(nccl_qround(F, H->ex));
+      CU_TRY(cudaEventRecord(H->ev[5], cs));
+    }
+    return SPAVA_OK;
+  };
+  if (!cp.on) ST_TRY(query());
   // st waits for round k (0 pass1, 1 pass2, 2 qpartial) of every host
   auto wait_round = [&](int k) -> int {
     if (!F->peer) {
@@ -1364,6 +1396,7 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     T(st, kComputeBegin, "stage1");
     ST_TRY(stage_chunks(H, b, st, cp, 0));
     T(st, kComputeEnd, "stage1");
+    if (cp.on) ST_TRY(query());
     if (F->plan.zigzag) {
       T(st, kCommWaitStart, "pass2", true);
       ST_TRY(wait_round(1));
@@ -1398,6 +1431,43 @@ int spava_host_layer(spava_host* H, const void* q, const void* k, const void* v,
   return layer_impl(H, b, as_stream(stream), CopyEdges{});
 }
 
+namespace {
+// dev: SPAVA_HOSTBUF_TIMELINE=1 prints when each copy / chunk of one host-buffer layer ends
+// (ms after the fork point; synchronises -- never set while timing)
+struct Timeline {
+  bool on = false;
+  std::vector<std::pair<std::string, cudaEvent_t>> ev;
+  void mark(const std::string& name, cudaStream_t s) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.emplace_back(name, e);
+  }
+  void dump() {
+    if (!on || ev.empty()) return;
+    cudaDeviceSynchronize();
+    for (auto& [n, e] : ev) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[0].second, e);
+      fprintf(stderr, "timeline %-14s %8.3f ms\n", n.c_str(), ms);
+    }
+    for (auto& pe : ev) cudaEventDestroy(pe.second);
+    ev.clear();
+  }
+};
+Timeline& timeline() {
+  static Timeline t;
+  static bool init = [] {
+    const char* e = getenv("SPAVA_HOSTBUF_TIMELINE");
+    t.on = e && atoi(e) != 0;
+    return true;
+  }();
+  (void)init;
+  return t;
+}
+}  // namespace
+
 int spava_host_layer_hostbuf(spava_host* H, const void* q_h, const void* k_h, const void* v_h,
                              void* out_h, int32_t* sel_h, void* q_d, void* k_d, void* v_d,
                              void* out_d, int32_t* sel_d, void* stream) {
@@ -1419,39 +1489,62 @@ int spava_host_layer_hostbuf(spava_host* H, const void* q_h, const void* k_h, co
   auto* oh = static_cast<uint8_t*>(out_h);
   cudaStream_t hs = H->h2d, ds = H->d2h;
   // inputs, in the order the phases consume them (the previous step's work on st is done
-  // before the buffers are overwritten: h2d waits for the fork point of this step)
+  // before the buffers are overwritten: h2d waits for the fork point of this step):
+  //   k, v of [anchor | lo]  ->  q query rows  ->  q lo chunk 0 (+ anchor rows)  -> k of
+  //   [hi | query] (ev_kvq: the scorer starts)  ->  q lo chunks 1..  ->  v of [hi | query]
+  //   (ev_vhi: select hi, query attention)  ->  q hi chunks, heaviest (last rows) first
   const CopyEdges cp = copy_edges(p);
   const int nc = spava_host::kCopyChunks;
-  CU_TRY(cudaEventRecord(H->ev_fork, st));
-  CU_TRY(cudaStreamWaitEvent(hs, H->ev_fork, 0));
-  CU_TRY(cudaMemcpyAsync(k_d, k_h, rows * rk, cudaMemcpyHostToDevice, hs));
-  CU_TRY(cudaMemcpyAsync(v_d, v_h, rows * rk, cudaMemcpyHostToDevice, hs));
-  CU_TRY(cudaMemcpyAsync(qd + qrow * rq, qh + qrow * rq, static_cast<size_t>(p.n_t) * rq, cudaMemcpyHostToDevice, hs));
-  CU_TRY(cudaEventRecord(H->ev_kvq, hs));
-  // q chunk rows (chunk 0 of block lo also carries the anchor rows)
+  const size_t lo_rows = lo_end, rest = rows - lo_end;
+  Timeline& TL = timeline();
+  auto* kd = static_cast<uint8_t*>(k_d);
+  auto* vd = static_cast<uint8_t*>(v_d);
+  const auto* kh = static_cast<const uint8_t*>(k_h);
+  const auto* vh = static_cast<const uint8_t*>(v_h);
+  // q rows of the chunk at processing position idx (chunk 0 of block lo carries the anchor)
   auto chunk_rows = [&](int idx, size_t* r0, size_t* r1) {
-    const int which = idx / nc, k = idx % nc;
+    const int which = idx / nc, c = chunk_of(which, idx % nc);
     const size_t base = static_cast<size_t>(p.l_a) + static_cast<size_t>(which) * p.l_b;
-    *r0 = (which == 0 && k == 0) ? 0 : base + cp.cb[k];
-    *r1 = base + cp.cb[k + 1];
+    *r0 = (which == 0 && c == 0) ? 0 : base + cp.cb[c];
+    *r1 = base + cp.cb[c + 1];
   };
-  for (int idx = 0; idx < 2 * nc; ++idx) {
+  auto put_q = [&](int idx) -> int {
     size_t r0, r1;
     chunk_rows(idx, &r0, &r1);
     if (r1 > r0)
       CU_TRY(cudaMemcpyAsync(qd + r0 * rq, qh + r0 * rq, (r1 - r0) * rq, cudaMemcpyHostToDevice, hs));
     CU_TRY(cudaEventRecord(H->ev_qc[idx], hs));
-  }
+    TL.mark("h2d q" + std::to_string(idx), hs);
+    return SPAVA_OK;
+  };
+  TL.mark("fork", st);
+  CU_TRY(cudaEventRecord(H->ev_fork, st));
+  CU_TRY(cudaStreamWaitEvent(hs, H->ev_fork, 0));
+  CU_TRY(cudaMemcpyAsync(kd, kh, lo_rows * rk, cudaMemcpyHostToDevice, hs));
+  CU_TRY(cudaMemcpyAsync(vd, vh, lo_rows * rk, cudaMemcpyHostToDevice, hs));
+  CU_TRY(cudaMemcpyAsync(qd + qrow * rq, qh + qrow * rq, static_cast<size_t>(p.n_t) * rq, cudaMemcpyHostToDevice, hs));
+  ST_TRY(put_q(0));
+  CU_TRY(cudaMemcpyAsync(kd + lo_rows * rk, kh + lo_rows * rk, rest * rk, cudaMemcpyHostToDevice, hs));
+  CU_TRY(cudaEventRecord(H->ev_kvq, hs));
+  TL.mark("h2d k all", hs);
+  for (int idx = 1; idx < nc; ++idx) ST_TRY(put_q(idx));
+  CU_TRY(cudaMemcpyAsync(vd + lo_rows * rk, vh + lo_rows * rk, rest * rk, cudaMemcpyHostToDevice, hs));
+  CU_TRY(cudaEventRecord(H->ev_vhi, hs));
+  TL.mark("h2d v hi", hs);
+  for (int idx = nc; idx < 2 * nc; ++idx) ST_TRY(put_q(idx));
   HostBufs b{static_cast<const uint8_t*>(q_d), static_cast<const uint8_t*>(k_d),
              static_cast<const uint8_t*>(v_d), od, sel_d};
   ST_TRY(layer_impl(H, b, st, cp));
+  TL.mark("compute end", st);
   // outputs as soon as each row chunk is final
   for (int idx = 0; idx < 2 * nc; ++idx) {
     size_t r0, r1;
     chunk_rows(idx, &r0, &r1);
     CU_TRY(cudaStreamWaitEvent(ds, H->ev_oc[idx], 0));
+    TL.mark("out ready " + std::to_string(idx), ds);
     if (r1 > r0)
       CU_TRY(cudaMemcpyAsync(oh + r0 * rq, od + r0 * rq, (r1 - r0) * rq, cudaMemcpyDeviceToHost, ds));
+    TL.mark("d2h done " + std::to_string(idx), ds);
   }
   CU_TRY(cudaStreamWaitEvent(ds, H->ev_oc[2 * nc], 0));
   CU_TRY(cudaMemcpyAsync(oh + qrow * rq, od + qrow * rq, static_cast<size_t>(p.n_t) * rq,
@@ -1460,6 +1553,8 @@ int spava_host_layer_hostbuf(spava_host* H, const void* q_h, const void* k_h, co
     CU_TRY(cudaMemcpyAsync(sel_h, sel_d, 2ull * p.l_p * sizeof(int32_t), cudaMemcpyDeviceToHost, ds));
   CU_TRY(cudaEventRecord(H->ev_d2h, ds));
   CU_TRY(cudaStreamWaitEvent(st, H->ev_d2h, 0));  // the caller's stream covers the copies
+  TL.mark("end", st);
+  TL.dump();
   return SPAVA_OK;
 }
 

@@ -77,12 +77,29 @@ def inproc(world, layers):
         outs = [torch.zeros(rows, HQ * 128, dtype=torch.bfloat16, device="cuda:0") for _ in hosts]
         sels = [torch.zeros(2, L_P, dtype=torch.int32, device="cuda:0") for _ in hosts]
         # enqueue every rank before any waits can be satisfied: the flag waits are in-stream
+        hostbuf = layer == layers - 1  # last layer through the host-buffer entry point
+        staged = []
         for r in range(world):
-            hosts[r].layer(qs[r], ks[r], vs[r], outs[r], sels[r], stream=streams[r])
+            if hostbuf:
+                hb = [t.cpu().pin_memory() for t in (qs[r], ks[r], vs[r])]
+                oh = torch.empty(outs[r].shape, dtype=outs[r].dtype).pin_memory()
+                sh = torch.empty(sels[r].shape, dtype=sels[r].dtype).pin_memory()
+                dq, dk, dv = (torch.empty_like(t) for t in (qs[r], ks[r], vs[r]))
+                staged.append((oh, sh, dq, dk, dv, hb))
+        torch.cuda.synchronize()
+        for r in range(world):
+            if hostbuf:
+                oh, sh, dq, dk, dv, hb = staged[r]
+                hosts[r].layer_hostbuf(hb[0], hb[1], hb[2], oh, dq, dk, dv, outs[r], sh,
+                                       sels[r], stream=streams[r])
+            else:
+                hosts[r].layer(qs[r], ks[r], vs[r], outs[r], sels[r], stream=streams[r])
         torch.cuda.synchronize()
         for r in range(world):
             assert hosts[r].status() == 0
             check(ref, layer, r, outs[r], sels[r])
+            if hostbuf:
+                check(ref, layer, r, staged[r][0].to("cuda:0"), staged[r][1].to("cuda:0"))
     for h in hosts:
         h.close()
     for f in fabs:
