@@ -201,13 +201,38 @@ int spava_fabric_create_nccl(const spava_layer_cfg* cfg, int device, const void*
  * barrier), since peers store into this rank's buffer.                        */
 #define SPAVA_PEER_HANDLE_BYTES 64
 int spava_fabric_create_peer(const spava_layer_cfg* cfg, int device, int world, int rank,
-                             spava_fabric** out);
+                             int64_t encode_bytes, spava_fabric** out);
 int spava_fabric_peer_handle(spava_fabric* fab, void* handle_64);
 int spava_fabric_peer_open(spava_fabric* fab, const void* handles_world_x_64);
 /* In-process variant (tests, one device): fabrics[r] = the peer fabric of rank r;
  * each rank's layer must then run on its own stream (the flag waits are in-stream). */
 int spava_fabric_peer_attach(spava_fabric* const* fabrics, int world);
 int spava_fabric_destroy(spava_fabric* fab);
+
+/* ---------------------------------------------- frame-parallel encode gather
+ * frame_partition (partition.cpp:30-37): counts[h] = frames/hosts + (h < frames%hosts).
+ * Host h encodes frames [sum counts[<h], +counts[h]) (simhost.cpp:285-291), i.e. global
+ * E_v rows [off_h, off_h + part_rows[h]).                                      */
+int spava_frame_partition(int frames, int hosts, int* counts);
+/* The encode AllGather + concat_rows + split_context of run_host (simhost.cpp:293-302)
+ * fused into one row gather: host h's [anchor | lo | hi | query] rows are read straight
+ * from the owning host's part (parts[q], rows part_rows[q], stride ld_part_bytes; the
+ * query rows from e_q) -- only l_a + 2*l_b + n_t rows move, E_v is never assembled.
+ * part_rows must sum to n_v.  parts may be IPC-mapped peer pointers.            */
+int spava_gather_split_rows(const spava_plan* plan, int h, const void* const* parts,
+                            const int64_t* part_rows, int64_t ld_part_bytes, const void* e_q,
+                            int64_t ld_q_bytes, void* dst, int64_t ld_dst_bytes, int row_bytes,
+                            void* stream);
+/* Peer fabric (created with encode_bytes > 0): each rank's encoder writes its E_v rows
+ * into its encode region; spava_host_gather_context then announces them (epoch flag),
+ * waits for every peer's, and gathers this host's rows over NVLink.  Before writing
+ * the region again, enqueue spava_fabric_encode_acquire on the writer's stream (waits
+ * until every peer has read the previous round).                               */
+int spava_fabric_encode_region(spava_fabric* fab, void** ptr, int64_t* bytes);
+int spava_fabric_encode_acquire(spava_fabric* fab, void* stream);
+int spava_host_gather_context(spava_host* host, const int64_t* part_rows, int64_t ld_part_bytes,
+                              const void* e_q, int64_t ld_q_bytes, void* dst, int64_t ld_dst_bytes,
+                              int row_bytes, void* stream);
 
 int spava_host_create(spava_fabric* fab, int h, spava_host** out);
 int spava_host_destroy(spava_host* host);

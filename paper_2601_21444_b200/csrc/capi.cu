@@ -128,12 +128,15 @@ struct Exchange {
   // peer fabric flags (epochs): arrive[round][q] = last epoch whose round-`round` slot from
   // host q has landed here (rounds 0 pass1, 1 pass2, 2 qpartial); done[q] = last epoch host
   // q has finished reading its own exchange buffer (so this host may overwrite its slot there)
-  static constexpr size_t kFlagBytes = 4096;
-  static constexpr int kArrive = 0, kDone = 3 * 256;
+  // round 3 = the encode gather (arrive), doneEnc[q] = host q has read the encode regions
+  static constexpr size_t kFlagBytes = 8192;
+  static constexpr int kArrive = 0, kDone = 4 * 256, kDoneEnc = 5 * 256;
   uint32_t* flags = nullptr;
+  void* encode = nullptr;  // peer fabric: this rank's share of E_v rows (encode_bytes)
+  size_t encode_bytes = 0;
   void* base = nullptr;
 
-  int alloc(const spava_layer_cfg& c, const spava_plan& p) {
+  int alloc(const spava_layer_cfg& c, const spava_plan& p, size_t enc_bytes = 0) {
     const size_t H = p.hosts, dk = static_cast<size_t>(c.hkv) * c.dh, dq = static_cast<size_t>(c.hq) * c.dh;
     const size_t lp = std::max(p.l_p, 1);
     const size_t kv = H * lp * dk * 2;
@@ -142,7 +145,7 @@ struct Exchange {
     const size_t qo = H * std::max(p.n_t, 1) * dq * 4;
     const size_t ql = H * std::max(p.n_t, 1) * c.hq * 4;
     auto al = [](size_t x) { return (x + 255) / 256 * 256; };
-    const size_t total = 2 * (2 * al(kv) + al(idx) + al(cnt)) + al(qo) + al(ql) + kFlagBytes;
+    const size_t total = 2 * (2 * al(kv) + al(idx) + al(cnt)) + al(qo) + al(ql) + kFlagBytes + al(enc_bytes);
     CU_TRY(cudaMalloc(&base, total));
     CU_TRY(cudaMemset(base, 0, total));
     uint8_t* b = static_cast<uint8_t*>(base);
@@ -154,7 +157,9 @@ struct Exchange {
     }
     qOut = reinterpret_cast<float*>(b); b += al(qo);
     qLse = reinterpret_cast<float*>(b); b += al(ql);
-    flags = reinterpret_cast<uint32_t*>(b);
+    flags = reinterpret_cast<uint32_t*>(b); b += kFlagBytes;
+    encode = enc_bytes ? b : nullptr;
+    encode_bytes = enc_bytes;
     return SPAVA_OK;
   }
   void release() {
@@ -177,6 +182,7 @@ struct spava_fabric {
   bool peer = false;
   bool peer_ready = false;
   uint32_t epoch = 0;                        // layers run on this fabric
+  uint32_t enc_epoch = 0;                    // encode gathers run on this fabric
   uint8_t* peer_base[kMaxMergeParts] = {};   // [world]; own base at [rank]
   bool peer_ipc[kMaxMergeParts] = {};        // opened through cudaIpcOpenMemHandle
   // pointer p into the own exchange buffer, translated into peer q's copy (same layout)
@@ -1016,7 +1022,8 @@ int spava_fabric_create_nccl(const spava_layer_cfg* cfg, int device, const void*
 }
 
 int spava_fabric_create_peer(const spava_layer_cfg* cfg, int device, int world, int rank,
-                             spava_fabric** out) {
+                             int64_t encode_bytes, spava_fabric** out) {
+  if (encode_bytes < 0) return fail(SPAVA_EINVAL, "peer fabric: encode_bytes");
   spava_plan plan;
   ST_TRY(cfg_check(cfg, &plan));
   if (world != cfg->hosts) return fail(SPAVA_EINVAL, "peer fabric: world size must equal hosts");
@@ -1031,7 +1038,7 @@ int spava_fabric_create_peer(const spava_layer_cfg* cfg, int device, int world, 
   F->peer = true;
   F->world = world;
   F->rank = rank;
-  const int s = F->shared.alloc(*cfg, plan);
+  const int s = F->shared.alloc(*cfg, plan, static_cast<size_t>(encode_bytes));
   if (s != SPAVA_OK) {
     delete F;
     return s;
@@ -1084,6 +1091,106 @@ int spava_fabric_peer_attach(spava_fabric* const* fabrics, int world) {
   for (int r = 0; r < world; ++r)
     for (int q = 0; q < world; ++q) fabrics[r]->peer_base[q] = static_cast<uint8_t*>(fabrics[q]->shared.base);
   for (int r = 0; r < world; ++r) fabrics[r]->peer_ready = true;
+  return SPAVA_OK;
+}
+
+// ------------------------------------------------- frame-parallel encode gather (f4)
+int spava_frame_partition(int frames, int hosts, int* counts) {
+  if (hosts < 1) return fail(SPAVA_EINVAL, "frame_partition: need at least one host");
+  if (!counts) return fail(SPAVA_EINVAL, "frame_partition: null counts");
+  for (int h = 0; h < hosts; ++h) counts[h] = frames / hosts + (h < frames % hosts ? 1 : 0);
+  return SPAVA_OK;
+}
+
+namespace {
+int make_parts(const spava_plan* p, const void* const* parts, const int64_t* part_rows, int64_t ld,
+               GatherParts* gp) {
+  if (p->hosts > kMaxPeers + 1) return fail(SPAVA_EINVAL, "gather_split: at most 8 hosts");
+  gp->n = p->hosts;
+  gp->ld = ld;
+  gp->off[0] = 0;
+  for (int q = 0; q < p->hosts; ++q) {
+    if (part_rows[q] < 0) return fail(SPAVA_EINVAL, "gather_split: negative part rows");
+    if (part_rows[q] > 0 && !parts[q]) return fail(SPAVA_EINVAL, "gather_split: null part");
+    gp->base[q] = parts[q];
+    gp->off[q + 1] = gp->off[q] + part_rows[q];
+  }
+  // concat_rows of the gathered parts is E_v (simhost.cpp:296-298)
+  if (gp->off[p->hosts] != p->n_v) return fail(SPAVA_EINVAL, "gather_split: part rows must sum to n_v");
+  return SPAVA_OK;
+}
+
+int gather_split_impl(const spava_plan* p, int h, const GatherParts& gp, const void* e_q, int64_t ld_q,
+                      void* dst, int64_t ld_dst, int row_bytes, cudaStream_t st) {
+  int lo, hi;
+  ST_TRY(spava_virtual_pair(p, h, &lo, &hi));
+  cudaError_t e = launch_gather_split(p->l_a, p->l_b, p->n_t, p->n_v, lo, hi, gp, e_q, ld_q, dst, ld_dst,
+                                      row_bytes, st);
+  if (e != cudaSuccess)
+    return fail(e == cudaErrorInvalidValue ? SPAVA_EINVAL : SPAVA_ECUDA,
+                "gather_split: rows, strides and pointers must be 16-byte aligned");
+  ++g_launches;
+  return SPAVA_OK;
+}
+}  // namespace
+
+int spava_gather_split_rows(const spava_plan* p, int h, const void* const* parts, const int64_t* part_rows,
+                            int64_t ld_part_bytes, const void* e_q, int64_t ld_q_bytes, void* dst,
+                            int64_t ld_dst_bytes, int row_bytes, void* stream) {
+  if (!p || !parts || !part_rows || !dst || (p->n_t > 0 && !e_q))
+    return fail(SPAVA_EINVAL, "gather_split_rows: null argument");
+  if (h < 0 || h >= p->hosts) return fail(SPAVA_ERANGE, "gather_split_rows: host index");
+  ST_TRY(require_device());
+  GatherParts gp{};
+  ST_TRY(make_parts(p, parts, part_rows, ld_part_bytes, &gp));
+  return gather_split_impl(p, h, gp, e_q, ld_q_bytes, dst, ld_dst_bytes, row_bytes, as_stream(stream));
+}
+
+int spava_fabric_encode_region(spava_fabric* F, void** ptr, int64_t* bytes) {
+  if (!F || !F->peer) return fail(SPAVA_EINVAL, "encode_region: not a peer fabric");
+  if (ptr) *ptr = F->shared.encode;
+  if (bytes) *bytes = static_cast<int64_t>(F->shared.encode_bytes);
+  return SPAVA_OK;
+}
+
+int spava_fabric_encode_acquire(spava_fabric* F, void* stream) {
+  if (!F || !F->peer || !F->peer_ready) return fail(SPAVA_EINVAL, "encode_acquire: peer fabric not open");
+  CU_TRY(cudaSetDevice(F->device));
+  if (F->enc_epoch == 0) return SPAVA_OK;
+  for (int q = 0; q < F->world; ++q)
+    if (q != F->rank)
+      CU_TRY(stream_wait_geq_u32(as_stream(stream), F->shared.flags + Exchange::kDoneEnc + q, F->enc_epoch));
+  return SPAVA_OK;
+}
+
+int spava_host_gather_context(spava_host* H, const int64_t* part_rows, int64_t ld_part_bytes, const void* e_q,
+                              int64_t ld_q_bytes, void* dst, int64_t ld_dst_bytes, int row_bytes, void* stream) {
+  if (!H || !part_rows || !dst) return fail(SPAVA_EINVAL, "gather_context: null argument");
+  spava_fabric* F = H->fab;
+  if (!F->peer || !F->peer_ready) return fail(SPAVA_EINVAL, "gather_context: needs an open peer fabric");
+  if (!F->shared.encode) return fail(SPAVA_EINVAL, "gather_context: fabric created with encode_bytes = 0");
+  const spava_plan& p = F->plan;
+  for (int q = 0; q < p.hosts; ++q)
+    if (part_rows[q] < 0 || static_cast<uint64_t>(part_rows[q]) * static_cast<uint64_t>(ld_part_bytes) >
+                                F->shared.encode_bytes)
+      return fail(SPAVA_EINVAL, "gather_context: a host's part exceeds the encode region");
+  CU_TRY(cudaSetDevice(F->device));
+  cudaStream_t st = as_stream(stream);
+  std::vector<const void*> parts(p.hosts);
+  for (int q = 0; q < p.hosts; ++q) parts[q] = F->at_peer(q, static_cast<uint8_t*>(F->shared.encode));
+  GatherParts gp{};
+  ST_TRY(make_parts(&p, parts.data(), part_rows, ld_part_bytes, &gp));
+  const uint32_t e = ++F->enc_epoch;
+  uint32_t* fl = F->shared.flags;
+  // the encoder's writes to this rank's region precede this call on `stream`: announce them
+  for (int q = 0; q < F->world; ++q)
+    if (q != F->rank)
+      CU_TRY(stream_write_u32(st, F->at_peer(q, fl) + Exchange::kArrive + 3 * 256 + F->rank, e));
+  for (int q = 0; q < F->world; ++q)
+    if (q != F->rank) CU_TRY(stream_wait_geq_u32(st, fl + Exchange::kArrive + 3 * 256 + q, e));
+  ST_TRY(gather_split_impl(&p, H->h, gp, e_q, ld_q_bytes, dst, ld_dst_bytes, row_bytes, st));
+  for (int q = 0; q < F->world; ++q)  // this rank has read every peer's region
+    if (q != F->rank) CU_TRY(stream_write_u32(st, F->at_peer(q, fl) + Exchange::kDoneEnc + F->rank, e));
   return SPAVA_OK;
 }
 

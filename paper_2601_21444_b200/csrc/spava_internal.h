@@ -117,6 +117,16 @@ cudaError_t launch_select_pack(const float* scores, int l_b, int l_p, int global
                                const void* k, const void* v, long long ld, int width, int32_t* idx,
                                void* k_out, void* v_out, long long ld_out, int32_t* count,
                                int32_t* status, cudaStream_t stream, const PeerSlots* peers = nullptr);
+// encode gather: rank q's share of E_v rows [off[q], off[q+1]) at base[q] (row stride ld)
+struct GatherParts {
+  const void* base[kMaxPeers + 1];
+  long long off[kMaxPeers + 2];
+  long long ld;
+  int n;
+};
+cudaError_t launch_gather_split(int l_a, int l_b, int n_t, int n_v, int lo, int hi, const GatherParts& parts,
+                                const void* eq, long long ld_q, void* dst, long long ld_dst, int row_bytes,
+                                cudaStream_t stream);
 // stream memory operations (driver API): the peer fabric's arrival / release flags
 cudaError_t stream_write_u32(cudaStream_t s, uint32_t* addr, uint32_t value);
 cudaError_t stream_wait_geq_u32(cudaStream_t s, const uint32_t* addr, uint32_t value);

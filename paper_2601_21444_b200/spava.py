@@ -36,7 +36,8 @@ EXPORTED_SYMBOLS = [
     "spava_attention_workspace", "spava_attention", "spava_mha_merge",
     "spava_fabric_create_local", "spava_nccl_unique_id", "spava_fabric_create_nccl",
     "spava_fabric_create_peer", "spava_fabric_peer_handle", "spava_fabric_peer_open",
-    "spava_fabric_peer_attach",
+    "spava_fabric_peer_attach", "spava_frame_partition", "spava_gather_split_rows",
+    "spava_fabric_encode_region", "spava_fabric_encode_acquire", "spava_host_gather_context",
     "spava_fabric_destroy", "spava_host_create", "spava_host_destroy", "spava_host_plan",
     "spava_host_rows", "spava_host_layer", "spava_host_layer_hostbuf", "spava_sim_layer",
     "spava_sim_layer_timed", "spava_host_set_trace", "spava_host_trace_read",
@@ -189,6 +190,15 @@ def lib():
                                        C.c_int, C.c_void_p]
         L.spava_merge_rows.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                                        C.c_int, C.c_int, C.c_void_p]
+        L.spava_fabric_create_peer.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int64, C.c_void_p]
+        L.spava_frame_partition.argtypes = [C.c_int, C.c_int, C.c_void_p]
+        L.spava_gather_split_rows.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int64,
+                                              C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int,
+                                              C.c_void_p]
+        L.spava_fabric_encode_region.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.spava_fabric_encode_acquire.argtypes = [C.c_void_p, C.c_void_p]
+        L.spava_host_gather_context.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                                C.c_void_p, C.c_int64, C.c_int, C.c_void_p]
         L.spava_host_trace_read.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
         L.spava_host_create.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
         L.spava_host_destroy.argtypes = [C.c_void_p]
@@ -331,6 +341,40 @@ def split_rows(plan, h, src, dst=None, stream=None):
     _check(lib().spava_split_rows(C.byref(plan), h, _ptr(src), src.stride(0) * es, _ptr(dst),
                                   dst.stride(0) * es, src.shape[1] * es, _stream(stream)))
     return dst
+
+
+def frame_partition(frames, hosts):
+    """frame_partition (partition.cpp:30-37): frames per host, the first frames % hosts get +1."""
+    out = (C.c_int * max(hosts, 1))()
+    _check(lib().spava_frame_partition(frames, hosts, out))
+    return list(out)[:hosts]
+
+
+def gather_split_rows(plan, h, parts, part_rows, e_q, dst=None, stream=None):
+    """Encode gather fused with split_context: host h's rows [anchor | lo | hi | query] read
+    from the hosts' E_v parts (tensors [part_rows[q], w], frame order) and e_q [n_t, w]."""
+    import torch
+
+    rows = plan.l_a + 2 * plan.l_b + plan.n_t
+    ref = next(t for t in parts if t is not None)
+    if dst is None:
+        dst = torch.empty((rows, ref.shape[1]), dtype=ref.dtype, device=ref.device)
+    es = ref.element_size()
+    n = len(parts)
+    ptrs = (C.c_void_p * n)(*[t.data_ptr() if t is not None and t.numel() else None for t in parts])
+    prow = (C.c_int64 * n)(*part_rows)
+    _check(lib().spava_gather_split_rows(C.byref(plan), h, ptrs, prow, ref.stride(0) * es, _ptr(e_q),
+                                         e_q.stride(0) * es, _ptr(dst), dst.stride(0) * es,
+                                         ref.shape[1] * es, _stream(stream)))
+    return dst
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of raw device memory (torch.as_tensor aliases it)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"data": (ptr, False), "shape": tuple(shape),
+                                         "typestr": typestr, "version": 3, "strides": None}
 
 
 def merge_rows(plan, h, src, dst, write_shared, stream=None):
@@ -493,6 +537,15 @@ class Host:
         _check(lib().spava_host_layer(self._p, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(sel),
                                       _stream(stream)))
 
+    def gather_context(self, part_rows, e_q, dst, ld_part_bytes, stream=None):
+        """Peer fabric: announce this rank's encode region, wait for the peers', and gather
+        this host's [anchor | lo | hi | query] rows over NVLink (spava_host_gather_context)."""
+        es = dst.element_size()
+        prow = (C.c_int64 * len(part_rows))(*part_rows)
+        _check(lib().spava_host_gather_context(self._p, prow, ld_part_bytes, _ptr(e_q), e_q.stride(0) * es,
+                                               _ptr(dst), dst.stride(0) * es, dst.shape[1] * es,
+                                               _stream(stream)))
+
     def layer_hostbuf(self, q_h, k_h, v_h, out_h, q_d, k_d, v_d, out_d, sel_h=None, sel_d=None,
                       stream=None):
         """One layer from HOST buffers (pinned CPU tensors) through caller-owned device
@@ -583,12 +636,13 @@ class Fabric:
     (NVLink P2P stores from the producing kernels + epoch flags; `Fabric.peer`)."""
 
     def __init__(self, cfg: LayerConfig, device=0, unique_id=None, world=1, rank=0,
-                 peer=False):
+                 peer=False, encode_bytes=0):
         self.cfg = cfg
+        self.device = device
         self._p = C.c_void_p()
         self.nccl = self.peer = False
         if peer:
-            _check(lib().spava_fabric_create_peer(C.byref(cfg), device, world, rank,
+            _check(lib().spava_fabric_create_peer(C.byref(cfg), device, world, rank, encode_bytes,
                                                   C.byref(self._p)))
             self.peer = True
         elif unique_id is None:
@@ -600,8 +654,23 @@ class Fabric:
             self.nccl = True
 
     @classmethod
-    def create_peer(cls, cfg: LayerConfig, device, world, rank):
-        return cls(cfg, device, world=world, rank=rank, peer=True)
+    def create_peer(cls, cfg: LayerConfig, device, world, rank, encode_bytes=0):
+        return cls(cfg, device, world=world, rank=rank, peer=True, encode_bytes=encode_bytes)
+
+    def encode_tensor(self, rows, cols):
+        """bf16 [rows, cols] torch view of this rank's encode region (its E_v share)."""
+        import torch
+
+        ptr, nbytes = C.c_void_p(), C.c_int64()
+        _check(lib().spava_fabric_encode_region(self._p, C.byref(ptr), C.byref(nbytes)))
+        if rows * cols * 2 > nbytes.value:
+            raise ValueError("encode_tensor: larger than the encode region")
+        arr = _CudaArray(ptr.value, (rows, cols), "<i2")
+        return torch.as_tensor(arr, device=f"cuda:{self.device}").view(torch.bfloat16)
+
+    def encode_acquire(self, stream=None):
+        """Enqueue: wait until every peer has read the previous encode round."""
+        _check(lib().spava_fabric_encode_acquire(self._p, _stream(stream)))
 
     def peer_handle(self) -> bytes:
         """64-byte IPC handle of this rank's exchange buffer (send it to every rank)."""

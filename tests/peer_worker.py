@@ -107,6 +107,49 @@ def inproc(world, layers):
     print(f"PEER_OK all {layers}", flush=True)
 
 
+def encode_inproc(world, rounds):
+    """Frame-parallel encode gather over the peer fabric: every rank's E_v share lives in
+    its encode region; gather_context must equal split_context of the concatenation."""
+    frames, tpf, width = 37, 96, 1024  # rows per frame, row width (bf16)
+    n_v, n_t = frames * tpf, 24
+    l_a, l_p = n_v // 64, n_v // 128
+    cfg = spava.LayerConfig.make(n_v, n_t, world, l_a, l_p, HQ, HKV)
+    plan = spava.make_plan(n_v, n_t, world, l_a, l_p, True)
+    counts = spava.frame_partition(frames, world)
+    rows = [c * tpf for c in counts]
+    cap = max(rows) * width * 2
+    fabs = [spava.Fabric.create_peer(cfg, 0, world, r, encode_bytes=cap) for r in range(world)]
+    spava.Fabric.peer_attach(fabs)
+    hosts = [f.host(r) for r, f in enumerate(fabs)]
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    for rnd in range(rounds):
+        g = torch.Generator(device="cuda:0").manual_seed(500 + rnd)
+        ev = torch.randn(n_v, width, device="cuda:0", generator=g).to(torch.bfloat16)
+        eq = torch.randn(n_t, width, device="cuda:0", generator=g).to(torch.bfloat16)
+        torch.cuda.synchronize()
+        outs = [torch.full((plan.l_a + 2 * plan.l_b + n_t, width), 7.0, dtype=torch.bfloat16,
+                           device="cuda:0") for _ in range(world)]
+        off = 0
+        for r in range(world):
+            with torch.cuda.stream(streams[r]):
+                fabs[r].encode_acquire(streams[r])  # peers have read the previous round
+                fabs[r].encode_tensor(rows[r], width).copy_(ev[off:off + rows[r]])
+            off += rows[r]
+        for r in range(world):
+            hosts[r].gather_context(rows, eq, outs[r], width * 2, stream=streams[r])
+        torch.cuda.synchronize()
+        glob = torch.cat([ev, eq])
+        for r in range(world):
+            want = spava.split_rows(plan, r, glob)
+            if not torch.equal(outs[r], want):
+                raise AssertionError(f"round {rnd} rank {r}: gathered rows differ")
+    for h in hosts:
+        h.close()
+    for f in fabs:
+        f.close()
+    print(f"PEER_OK encode {rounds}", flush=True)
+
+
 def one_rank(rank, world, layers, port):
     import torch.distributed as dist
 
@@ -141,5 +184,7 @@ if __name__ == "__main__":
     mode = sys.argv[1]
     if mode == "inproc":
         inproc(int(sys.argv[2]), int(sys.argv[3]))
+    elif mode == "encode":
+        encode_inproc(int(sys.argv[2]), int(sys.argv[3]))
     else:
         one_rank(int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]))

@@ -26,6 +26,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def _env():
     env = dict(os.environ)
     env["CUDA_DEVICE_MAX_CONNECTIONS"] = "32"  # every rank stream its own hardware queue
+    # one thread enqueues every rank: a lazily loaded kernel's first launch waits for the
+    # device, whose streams may wait on flags of ranks not yet enqueued -> load eagerly
+    env["CUDA_MODULE_LOADING"] = "EAGER"
     env["PYTHONPATH"] = ROOT + os.pathsep + env.get("PYTHONPATH", "")
     return env
 

@@ -67,6 +67,19 @@ def test_split_sweep_vs_oracle():
             assert spava.block_valid_rows(p, v) == int((g["pad_masks"][v] == 0).sum())
 
 
+def test_frame_partition():
+    """test_partition.cpp:23-28 pins; sums and balance (acceptance.cpp:186-195, Eq. 6)"""
+    assert spava.frame_partition(64, 8) == [8] * 8
+    assert spava.frame_partition(10, 3) == [4, 3, 3]
+    assert spava.frame_partition(7, 8) == [1, 1, 1, 1, 1, 1, 1, 0]
+    with pytest.raises(spava.SpavaError):
+        spava.frame_partition(4, 0)
+    for f in range(0, 40):
+        for h in range(1, 9):
+            c = spava.frame_partition(f, h)
+            assert sum(c) == f and max(c) - min(c) <= 1 and c == sorted(c, reverse=True)
+
+
 def test_slice_anchor():
     """test_partition.cpp:122-144"""
     assert spava.slice_anchor(8, 4, 0) == (0, 2) and spava.slice_anchor(8, 4, 3) == (6, 8)
