@@ -334,6 +334,7 @@ def run_spava_arm(args):
     g = geometry(cfg, H)
     hq, hkv = cfg["hq"], cfg["hkv"]
     lc = spava.LayerConfig.make(g["n_v"], g["n_t"], H, g["l_a"], g["l_p"], hq, hkv, DH)
+    fabric_note = None
     if world > 1:
         if os.environ.get("SPAVA_BENCH_ONE_GPU") == "1":
             if args.fabric != "peer":
@@ -341,14 +342,26 @@ def run_spava_arm(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
+        fab = None
         if args.fabric == "peer":
             # exchange rounds as NVLink stores from the producing kernels (IPC-mapped peer
             # exchange buffers) + epoch flags; torch.distributed only ships the handles
             fab = spava.Fabric.create_peer(lc, local, world, rank)
             handles = [None] * world
             dist.all_gather_object(handles, fab.peer_handle())
-            fab.peer_open(handles)
-        else:
+            err = ""
+            try:
+                fab.peer_open(handles)
+            except spava.SpavaError as e:  # e.g. peers not visible to this process
+                err = str(e)[:160]
+            errs = [None] * world
+            dist.all_gather_object(errs, err)
+            if any(errs):  # every rank switches together
+                fabric_note = "peer open failed (" + next(x for x in errs if x) + "); nccl used"
+                fab.close()
+                fab = None
+                args.fabric = "nccl"
+        if fab is None:
             obj = [spava.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
             fab = spava.Fabric(lc, local, unique_id=obj[0], world=world, rank=rank)
@@ -654,6 +667,7 @@ def run_spava_arm(args):
                    "exchange": ("local" if world == 1 else
                                 "peer (NVLink stores from the select / merge kernels + epoch flags)"
                                 if args.fabric == "peer" else "nccl allgather"),
+                   "exchange_note": fabric_note,
                    "l2": "flushed (256 MiB write) between timed steps, outside the events",
                    "scoring": "exact (bit-faithful to the reference)"},
         "e2e": {"value": tokens / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
