@@ -185,6 +185,7 @@ struct spava_fabric {
   uint32_t enc_epoch = 0;                    // encode gathers run on this fabric
   uint8_t* peer_base[kMaxMergeParts] = {};   // [world]; own base at [rank]
   bool peer_ipc[kMaxMergeParts] = {};        // opened through cudaIpcOpenMemHandle
+  uint32_t* flag_tmp[kMaxPeers] = {};        // scratch: the peers' flag addresses of one store
   // pointer p into the own exchange buffer, translated into peer q's copy (same layout)
   template <typename T>
   T* at_peer(int q, T* p) const {
@@ -391,8 +392,10 @@ uint32_t* done_flag(uint32_t* flags, int q) { return flags + Exchange::kDone + q
 
 // this rank's round-`round` slot has been stored into every peer: raise arrive[round][me]
 int peer_signal(spava_fabric* F, cudaStream_t s, int round) {
+  int n = 0;
   for (int q = 0; q < F->world; ++q)
-    if (q != F->rank) CU_TRY(stream_write_u32(s, arrive_flag(F->at_peer(q, F->shared.flags), round, F->rank), F->epoch));
+    if (q != F->rank) F->flag_tmp[n++] = arrive_flag(F->at_peer(q, F->shared.flags), round, F->rank);
+  CU_TRY(peer_flags_store(s, F->flag_tmp, n, F->epoch));
   return SPAVA_OK;
 }
 
@@ -414,8 +417,10 @@ int peer_wait_done(spava_fabric* F, cudaStream_t s) {
 
 // this rank has finished reading its exchange buffer for the epoch: tell every peer
 int peer_release(spava_fabric* F, cudaStream_t s) {
+  int n = 0;
   for (int q = 0; q < F->world; ++q)
-    if (q != F->rank) CU_TRY(stream_write_u32(s, done_flag(F->at_peer(q, F->shared.flags), F->rank), F->epoch));
+    if (q != F->rank) F->flag_tmp[n++] = done_flag(F->at_peer(q, F->shared.flags), F->rank);
+  CU_TRY(peer_flags_store(s, F->flag_tmp, n, F->epoch));
   return SPAVA_OK;
 }
 
@@ -1183,14 +1188,17 @@ int spava_host_gather_context(spava_host* H, const int64_t* part_rows, int64_t l
   const uint32_t e = ++F->enc_epoch;
   uint32_t* fl = F->shared.flags;
   // the encoder's writes to this rank's region precede this call on `stream`: announce them
+  int n = 0;
   for (int q = 0; q < F->world; ++q)
-    if (q != F->rank)
-      CU_TRY(stream_write_u32(st, F->at_peer(q, fl) + Exchange::kArrive + 3 * 256 + F->rank, e));
+    if (q != F->rank) F->flag_tmp[n++] = F->at_peer(q, fl) + Exchange::kArrive + 3 * 256 + F->rank;
+  CU_TRY(peer_flags_store(st, F->flag_tmp, n, e));
   for (int q = 0; q < F->world; ++q)
     if (q != F->rank) CU_TRY(stream_wait_geq_u32(st, fl + Exchange::kArrive + 3 * 256 + q, e));
   ST_TRY(gather_split_impl(&p, H->h, gp, e_q, ld_q_bytes, dst, ld_dst_bytes, row_bytes, st));
+  n = 0;
   for (int q = 0; q < F->world; ++q)  // this rank has read every peer's region
-    if (q != F->rank) CU_TRY(stream_write_u32(st, F->at_peer(q, fl) + Exchange::kDoneEnc + F->rank, e));
+    if (q != F->rank) F->flag_tmp[n++] = F->at_peer(q, fl) + Exchange::kDoneEnc + F->rank;
+  CU_TRY(peer_flags_store(st, F->flag_tmp, n, e));
   return SPAVA_OK;
 }
 

@@ -1,13 +1,15 @@
-// peer.cu -- stream memory operations for the peer (NVLink P2P) fabric.
+// peer.cu -- flag stores and stream waits for the peer (NVLink P2P) fabric.
 //
 // The peer fabric replaces the GatherFabric's ordered AllGather rounds
 // (simhost.cpp:73-124, rounds pass1 / pass2 / qpartial at :343-365, :404-414) with
 // stores from the producing kernels straight into every peer GPU's exchange slot (the
 // select gather and the query split-merge take the peers' IPC-mapped slot pointers).
 // Ordering between GPUs is carried by 32-bit epoch flags in each GPU's exchange buffer:
-//   * producer stream, after the storing kernel: cuStreamWriteValue32 into each peer's
-//     arrive[round][me] (the default write carries a system-scope memory fence, so the
-//     kernel's peer stores are visible before the flag);
+//   * producer stream, after the storing kernel: a one-warp kernel raises arrive[round][me]
+//     in every peer with a system-scope release store (the storing kernel completed
+//     earlier in stream order, so its peer stores happen-before the flag -- a kernel,
+//     not cuStreamWriteValue32, because peer device addresses are always valid kernel
+//     operands);
 //   * consumer stream, before the first reader: cuStreamWaitValue32(arrive[round][q] >=
 //     epoch) for every peer q -- the wait sits in the stream's hardware queue, no spinning
 //     kernel occupies an SM.
@@ -25,7 +27,6 @@ namespace {
 
 struct MemOps {
   PFN_cuStreamWaitValue32_v11070 wait = nullptr;
-  PFN_cuStreamWriteValue32_v11070 write = nullptr;
   unsigned wait_flags = CU_STREAM_WAIT_VALUE_GEQ;
 };
 
@@ -38,10 +39,6 @@ const MemOps& memops() {
     if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       m.wait = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
-    p = nullptr;
-    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      m.write = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(p);
     int dev = 0, flush = 0;
     if (cudaGetDevice(&dev) == cudaSuccess &&
         cudaDeviceGetAttribute(&flush, static_cast<cudaDeviceAttr>(CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES),
@@ -54,13 +51,27 @@ const MemOps& memops() {
 
 }  // namespace
 
-cudaError_t stream_write_u32(cudaStream_t s, uint32_t* addr, uint32_t value) {
-  const MemOps& m = memops();
-  if (!m.write) return cudaErrorNotSupported;
-  return m.write(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), value,
-                 CU_STREAM_WRITE_VALUE_DEFAULT) == CUDA_SUCCESS
-             ? cudaSuccess
-             : cudaErrorUnknown;
+namespace {
+struct FlagAddrs {
+  uint32_t* p[kMaxPeers];
+  int n;
+};
+__global__ void flag_store_kernel(const __grid_constant__ FlagAddrs f, uint32_t value) {
+  if (threadIdx.x < f.n) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f.p[threadIdx.x]), "r"(value) : "memory");
+  }
+}
+}  // namespace
+
+cudaError_t peer_flags_store(cudaStream_t s, uint32_t* const* addrs, int n, uint32_t value) {
+  if (n <= 0) return cudaSuccess;
+  if (n > kMaxPeers) return cudaErrorInvalidValue;
+  FlagAddrs f{};
+  for (int i = 0; i < n; ++i) f.p[i] = addrs[i];
+  f.n = n;
+  flag_store_kernel<<<1, 32, 0, s>>>(f, value);
+  return cudaGetLastError();
 }
 
 cudaError_t stream_wait_geq_u32(cudaStream_t s, const uint32_t* addr, uint32_t value) {

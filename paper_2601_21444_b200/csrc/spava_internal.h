@@ -128,7 +128,8 @@ cudaError_t launch_gather_split(int l_a, int l_b, int n_t, int n_v, int lo, int 
                                 const void* eq, long long ld_q, void* dst, long long ld_dst, int row_bytes,
                                 cudaStream_t stream);
 // stream memory operations (driver API): the peer fabric's arrival / release flags
-cudaError_t stream_write_u32(cudaStream_t s, uint32_t* addr, uint32_t value);
+// one kernel: system-scope release store of `value` to every address (peer flags)
+cudaError_t peer_flags_store(cudaStream_t s, uint32_t* const* addrs, int n, uint32_t value);
 cudaError_t stream_wait_geq_u32(cudaStream_t s, const uint32_t* addr, uint32_t value);
 
 // ---------------------------------------------------------------- split_context rows
