@@ -20,12 +20,13 @@ import torch
 from paper_2601_21444_b200 import spava
 
 N_V, N_T, L_A, L_P, HQ, HKV = 5000, 64, 64, 160, 8, 2
+ZIGZAG = os.environ.get("PEER_ZIGZAG", "1") == "1"
 
 
 def inputs(world, layer):
     """Per-host [anchor | lo | hi | query] buffers of one layer (same on every rank)."""
-    cfg = spava.LayerConfig.make(N_V, N_T, world, L_A, L_P, HQ, HKV)
-    plan = spava.make_plan(N_V, N_T, world, L_A, L_P, True)
+    cfg = spava.LayerConfig.make(N_V, N_T, world, L_A, L_P, HQ, HKV, zigzag=ZIGZAG)
+    plan = spava.make_plan(N_V, N_T, world, L_A, L_P, ZIGZAG)
     rows = L_A + 2 * plan.l_b + N_T
     g = torch.Generator(device="cuda:0").manual_seed(1000 + layer)
     qs, ks, vs = [], [], []

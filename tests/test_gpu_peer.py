@@ -41,10 +41,12 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_peer_fabric_inprocess_matches_local(cuda, world):
+@pytest.mark.parametrize("world,zigzag", [(2, True), (4, True), (3, False)])
+def test_peer_fabric_inprocess_matches_local(cuda, world, zigzag):
+    env = _env()
+    env["PEER_ZIGZAG"] = "1" if zigzag else "0"
     r = subprocess.run([sys.executable, "-m", "tests.peer_worker", "inproc", str(world), "3"],
-                       cwd=ROOT, env=_env(), capture_output=True, text=True, timeout=240)
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=240)
     assert r.returncode == 0 and "PEER_OK all 3" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
 
 
