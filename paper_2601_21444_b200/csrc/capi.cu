@@ -366,7 +366,7 @@ int auto_splits(int nq, int hq, int hkv, int total_keys) {
   const bool pair = nq <= kBlockM && (hq / hkv) % 2 == 0;  // mirrors launch_attention
   const int ctas = pair ? hq / 2 : hq * ((nq + 255) / 256);
   const int tiles = std::max(1, (total_keys + kBlockN - 1) / kBlockN);
-  int s = (148 + ctas - 1) / ctas;
+  int s = 148 / ctas;  // one wave: ceil would leave a few CTAs for a second full-length wave
   s = std::min(s, tiles);
   s = std::min(s, 32);
   return std::max(1, s);
