@@ -454,6 +454,10 @@ int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record,
     }
     span(H, 1, t0, st);
   }
+  // both blocks in one select and one gather launch, unless select hi must wait for its
+  // v rows (host-buffer pipeline) -- then lo goes first so pass1 is not held back
+  SelectPackJob jobs[2];
+  PeerSlots peers[2] = {};
   for (int r = 0; r < 2; ++r) {
     const long long krow = p.l_a + static_cast<long long>(r) * p.l_b;
     const long long slot = static_cast<long long>(H->h) * p.l_p;
@@ -461,31 +465,38 @@ int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record,
     uint8_t* k_out = static_cast<uint8_t*>(H->ex->passK[r]) + slot * dk * 2;
     uint8_t* v_out = static_cast<uint8_t*>(H->ex->passV[r]) + slot * dk * 2;
     int32_t* cnt_out = H->ex->passCnt[r] + H->h;
-    if (r == 1 && before_hi) CU_TRY(cudaStreamWaitEvent(st, before_hi, 0));  // v rows of hi
-    PeerSlots peers{};
     if (F.peer && p.l_p > 0)  // the gather also stores the slot into every peer's buffer
       for (int q = 0; q < F.world; ++q)
         if (q != F.rank) {
-          peers.k[peers.n] = F.at_peer(q, k_out);
-          peers.v[peers.n] = F.at_peer(q, v_out);
-          peers.idx[peers.n] = F.at_peer(q, idx_out);
-          peers.cnt[peers.n] = F.at_peer(q, cnt_out);
-          ++peers.n;
+          PeerSlots& ps = peers[r];
+          ps.k[ps.n] = F.at_peer(q, k_out);
+          ps.v[ps.n] = F.at_peer(q, v_out);
+          ps.idx[ps.n] = F.at_peer(q, idx_out);
+          ps.cnt[ps.n] = F.at_peer(q, cnt_out);
+          ++ps.n;
         }
-    const size_t t0 = mark(H, st);
-    cudaError_t e = launch_select_pack(H->scores[r], p.l_b, p.l_p, p.l_a + vs[r] * p.l_b, row_ptr(b.k, krow, dk),
-                           row_ptr(b.v, krow, dk), dk, static_cast<int>(dk), idx_out, k_out, v_out, dk,
-                           cnt_out, H->status, st, &peers);
-    if (e != cudaSuccess) return fail(SPAVA_ECUDA, std::string("select: ") + cudaGetErrorString(e));
+    jobs[r] = SelectPackJob{H->scores[r], p.l_a + vs[r] * p.l_b, row_ptr(b.k, krow, dk), row_ptr(b.v, krow, dk),
+                            idx_out, k_out, v_out, cnt_out, &peers[r]};
+  }
+  auto finish = [&](int r) -> int {  // after round r's select + pack
     if (F.peer) ST_TRY(peer_signal(H->fab, st, r));
-    g_launches += p.l_p > 0 ? 2 : 1;
-    span(H, 2, t0, st);
     if (b.sel && p.l_p > 0)
-      CU_TRY(cudaMemcpyAsync(b.sel + r * p.l_p, idx_out, sizeof(int32_t) * p.l_p,
+      CU_TRY(cudaMemcpyAsync(b.sel + r * p.l_p, jobs[r].idx, sizeof(int32_t) * p.l_p,
                              cudaMemcpyDeviceToDevice, st));
     if (record) CU_TRY(cudaEventRecord(H->ev[r], st));
-    if (r == 1) trace_ev(H, st, kComputeEnd, "score", false);
+    return SPAVA_OK;
+  };
+  const int per = before_hi ? 1 : 2;  // blocks per launch
+  for (int r0 = 0; r0 < 2; r0 += per) {
+    if (r0 == 1) CU_TRY(cudaStreamWaitEvent(st, before_hi, 0));  // v rows of hi
+    const size_t t0 = mark(H, st);
+    cudaError_t e = launch_select_pack_n(jobs + r0, per, p.l_b, p.l_p, dk, static_cast<int>(dk), dk, H->status, st);
+    if (e != cudaSuccess) return fail(SPAVA_ECUDA, std::string("select: ") + cudaGetErrorString(e));
+    g_launches += p.l_p > 0 ? 2 : 1;
+    span(H, 2, t0, st);
+    for (int r = r0; r < r0 + per; ++r) ST_TRY(finish(r));
   }
+  trace_ev(H, st, kComputeEnd, "score", false);
   return SPAVA_OK;
 }
 

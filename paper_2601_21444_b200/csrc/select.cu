@@ -78,11 +78,32 @@ __device__ __forceinline__ void load_items(const float* s, int l_b, int base, fl
   }
 }
 
-__global__ void __launch_bounds__(kSelThreads) select_kernel(const float* __restrict__ scores,
-                                                             int l_b, int l_p, int global_offset,
-                                                             int32_t* __restrict__ idx,
-                                                             int32_t* __restrict__ count,
-                                                             int32_t* __restrict__ status) {
+// one job per block (lo, hi): selection and gather of both blocks in one launch each
+struct SelJob {
+  const float* scores;
+  int global_offset;
+  int32_t* idx;
+  int32_t* count;
+  const uint4* k;
+  const uint4* v;
+  uint4* k_out;
+  uint4* v_out;
+  PeerSlots peers;
+};
+struct SelJobs {
+  SelJob j[2];
+  int l_b, l_p, w16;
+  long long ld16, ld_out16;
+  int32_t* status;
+};
+
+__global__ void __launch_bounds__(kSelThreads) select_kernel(const __grid_constant__ SelJobs J) {
+  const SelJob& jb = J.j[blockIdx.x];
+  const float* __restrict__ scores = jb.scores;
+  const int l_b = J.l_b, l_p = J.l_p, global_offset = jb.global_offset;
+  int32_t* __restrict__ idx = jb.idx;
+  int32_t* __restrict__ count = jb.count;
+  int32_t* __restrict__ status = J.status;
   __shared__ int hist[2048];
   __shared__ int red[kWarps + 1];
   __shared__ uint32_t sh_prefix;
@@ -204,27 +225,26 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const float* __rest
 // Peer fabric: the same rows (and the slot's index list / count) are also stored straight
 // into every peer GPU's exchange slot over NVLink -- the pass round is this kernel's
 // epilogue, no separate collective.
-__global__ void gather_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ count,
-                              int global_offset, int l_p, const uint4* __restrict__ k,
-                              const uint4* __restrict__ v, long long ld16, int w16,
-                              uint4* __restrict__ k_out, uint4* __restrict__ v_out,
-                              long long ld_out16, const __grid_constant__ PeerSlots peers) {
+__global__ void gather_kernel(const __grid_constant__ SelJobs J) {
+  const SelJob& jb = J.j[blockIdx.y];
   const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
-  if (r >= l_p) return;
-  const int n = *count;
-  const long long o = r * ld_out16;
+  if (r >= J.l_p) return;
+  const int n = *jb.count;
+  const int32_t* idx = jb.idx;
+  const PeerSlots& peers = jb.peers;
+  const long long o = r * J.ld_out16;
   if (lane == 0)
     for (int q = 0; q < peers.n; ++q) {
       static_cast<int32_t*>(peers.idx[q])[r] = idx[r];
       if (r == 0) *static_cast<int32_t*>(peers.cnt[q]) = n;
     }
-  const long long src = r < n ? static_cast<long long>(idx[r] - global_offset) * ld16 : 0;
-  for (int c = lane; c < w16; c += 32) {
-    const uint4 kx = r < n ? k[src + c] : make_uint4(0, 0, 0, 0);
-    const uint4 vx = r < n ? v[src + c] : make_uint4(0, 0, 0, 0);
-    k_out[o + c] = kx;
-    v_out[o + c] = vx;
+  const long long src = r < n ? static_cast<long long>(idx[r] - jb.global_offset) * J.ld16 : 0;
+  for (int c = lane; c < J.w16; c += 32) {
+    const uint4 kx = r < n ? jb.k[src + c] : make_uint4(0, 0, 0, 0);
+    const uint4 vx = r < n ? jb.v[src + c] : make_uint4(0, 0, 0, 0);
+    jb.k_out[o + c] = kx;
+    jb.v_out[o + c] = vx;
     for (int q = 0; q < peers.n; ++q) {
       static_cast<uint4*>(peers.k[q])[o + c] = kx;
       static_cast<uint4*>(peers.v[q])[o + c] = vx;
@@ -234,22 +254,46 @@ __global__ void gather_kernel(const int32_t* __restrict__ idx, const int32_t* __
 
 }  // namespace
 
+cudaError_t launch_select_pack_n(const SelectPackJob* jobs, int n, int l_b, int l_p, long long ld, int width,
+                                 long long ld_out, int32_t* status, cudaStream_t stream) {
+  if (n < 1 || n > 2 || l_p < 0 || l_p > l_b || (width % 8) || (ld % 8) || (ld_out % 8))
+    return cudaErrorInvalidValue;
+  SelJobs J{};
+  J.l_b = l_b;
+  J.l_p = l_p;
+  J.w16 = width / 8;
+  J.ld16 = ld / 8;
+  J.ld_out16 = ld_out / 8;
+  J.status = status;
+  bool gather = l_p > 0;
+  for (int i = 0; i < n; ++i) {
+    const SelectPackJob& s = jobs[i];
+    if (s.peers && (s.peers->n < 0 || s.peers->n > kMaxPeers)) return cudaErrorInvalidValue;
+    SelJob& j = J.j[i];
+    j.scores = s.scores;
+    j.global_offset = s.global_offset;
+    j.idx = s.idx;
+    j.count = s.count;
+    j.k = static_cast<const uint4*>(s.k);
+    j.v = static_cast<const uint4*>(s.v);
+    j.k_out = static_cast<uint4*>(s.k_out);
+    j.v_out = static_cast<uint4*>(s.v_out);
+    if (s.peers) j.peers = *s.peers;
+    gather = gather && s.k_out && s.v_out;
+    if (!(l_p > 0 && s.k_out && s.v_out) && j.peers.n > 0)
+      return cudaErrorInvalidValue;  // a peer slot is only published through the gather
+  }
+  select_kernel<<<n, kSelThreads, 0, stream>>>(J);
+  if (gather) gather_kernel<<<dim3((l_p + 7) / 8, n), 256, 0, stream>>>(J);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_select_pack(const float* scores, int l_b, int l_p, int global_offset,
                                const void* k, const void* v, long long ld, int width, int32_t* idx,
                                void* k_out, void* v_out, long long ld_out, int32_t* count,
                                int32_t* status, cudaStream_t stream, const PeerSlots* peers) {
-  if (l_p < 0 || l_p > l_b || (width % 8) || (ld % 8) || (ld_out % 8)) return cudaErrorInvalidValue;
-  if (peers && (peers->n < 0 || peers->n > kMaxPeers)) return cudaErrorInvalidValue;
-  select_kernel<<<1, kSelThreads, 0, stream>>>(scores, l_b, l_p, global_offset, idx, count, status);
-  if (l_p > 0 && k_out && v_out) {
-    gather_kernel<<<(l_p + 7) / 8, 256, 0, stream>>>(
-        idx, count, global_offset, l_p, static_cast<const uint4*>(k), static_cast<const uint4*>(v),
-        ld / 8, width / 8, static_cast<uint4*>(k_out), static_cast<uint4*>(v_out), ld_out / 8,
-        peers ? *peers : PeerSlots{});
-  } else if (peers && peers->n > 0) {
-    return cudaErrorInvalidValue;  // a peer slot is only published through the gather
-  }
-  return cudaGetLastError();
+  const SelectPackJob job{scores, global_offset, k, v, idx, k_out, v_out, count, peers};
+  return launch_select_pack_n(&job, 1, l_b, l_p, ld, width, ld_out, status, stream);
 }
 
 }  // namespace spava

@@ -113,6 +113,20 @@ struct PeerSlots {
   void* cnt[kMaxPeers];
   int n;
 };
+struct SelectPackJob {
+  const float* scores;
+  int global_offset;
+  const void* k;
+  const void* v;
+  int32_t* idx;
+  void* k_out;
+  void* v_out;
+  int32_t* count;
+  const PeerSlots* peers;  // nullable
+};
+// select + pack of 1 or 2 blocks (same l_b / l_p / widths) in one select and one gather launch
+cudaError_t launch_select_pack_n(const SelectPackJob* jobs, int n, int l_b, int l_p, long long ld, int width,
+                                 long long ld_out, int32_t* status, cudaStream_t stream);
 cudaError_t launch_select_pack(const float* scores, int l_b, int l_p, int global_offset,
                                const void* k, const void* v, long long ld, int width, int32_t* idx,
                                void* k_out, void* v_out, long long ld_out, int32_t* count,
