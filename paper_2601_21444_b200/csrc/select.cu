@@ -3,8 +3,8 @@
 // select_essential (approx.cpp:71-102): stable descending sort of the block's scores
 // (ties -> lower index), take at most l_p stopping at the first non-finite, return the
 // chosen indices ascending (+ global offset) and gather their K/V rows.
-// GPU form, no sort at all (one 1024-thread CTA, each thread owning 16 consecutive keys
-// of a 16K-key chunk):
+// GPU form, no sort at all (one CTA per block -- 1024 threads, or 256 for l_b <= 4096 --
+// each thread owning 16 consecutive keys of a chunk):
 //   1. count finite scores (k = min(l_p, #finite); any +inf sorts first and ends the
 //      selection immediately; NaN is rejected),
 //   2. 3-pass MSB radix select (11/11/10-bit digits, warp-aggregated smem histograms,
@@ -22,10 +22,10 @@ namespace spava {
 
 namespace {
 
-constexpr int kSelThreads = 1024;
 constexpr int kItems = 16;
-constexpr int kChunk = kSelThreads * kItems;
-constexpr int kWarps = kSelThreads / 32;
+// 1024 threads for long blocks; 256 for l_b <= 4096 (H >= 4 shapes), where the selection
+// is latency-bound and a smaller CTA halves the barrier / scan depth
+constexpr int kSelBig = 1024, kSelSmall = 256;
 
 __device__ __forceinline__ uint32_t order_key(float s) {
   const uint32_t u = __float_as_uint(s);
@@ -43,7 +43,8 @@ __device__ __forceinline__ int warp_incl(int v) {
   return v;
 }
 
-// exclusive block scan of v (thread order); *total = block sum.  Uses red[kWarps + 1].
+// exclusive block scan of v (thread order); *total = block sum.  Uses red[NW + 1].
+template <int NW>
 __device__ __forceinline__ int block_excl(int v, int* red, int* total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int inc = warp_incl(v);
@@ -51,17 +52,18 @@ __device__ __forceinline__ int block_excl(int v, int* red, int* total) {
   if (lane == 31) red[w] = inc;
   __syncthreads();
   if (w == 0) {
-    const int x = red[lane];
+    const int x = lane < NW ? red[lane] : 0;
     const int xi = warp_incl(x);
-    red[lane] = xi - x;
-    if (lane == 31) red[kWarps] = xi;
+    if (lane < NW) red[lane] = xi - x;
+    if (lane == 31) red[NW] = xi;
   }
   __syncthreads();
-  *total = red[kWarps];
+  *total = red[NW];
   return red[w] + inc - v;
 }
 
 __device__ __forceinline__ void load_items(const float* s, int l_b, int base, float (&v)[kItems]) {
+  // thread t owns keys [base + t*kItems, +kItems)
   const int j0 = base + threadIdx.x * kItems;
   if (j0 + kItems <= l_b && ((reinterpret_cast<uintptr_t>(s + j0) & 15) == 0)) {
 #pragma unroll
@@ -97,7 +99,10 @@ struct SelJobs {
   int32_t* status;
 };
 
+template <int kSelThreads>
 __global__ void __launch_bounds__(kSelThreads) select_kernel(const __grid_constant__ SelJobs J) {
+  constexpr int kChunk = kSelThreads * kItems;
+  constexpr int kWarps = kSelThreads / 32;
   const SelJob& jb = J.j[blockIdx.x];
   const float* __restrict__ scores = jb.scores;
   const int l_b = J.l_b, l_p = J.l_p, global_offset = jb.global_offset;
@@ -121,8 +126,8 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const __grid_consta
     }
   }
   int tot_fin, tot_bad;
-  block_excl(fin, red, &tot_fin);
-  block_excl(bad, red, &tot_bad);
+  block_excl<kWarps>(fin, red, &tot_fin);
+  block_excl<kWarps>(bad, red, &tot_bad);
   const int k = tot_bad > 0 ? 0 : min(l_p, tot_fin);
   if (tot_bad > 0 && tid == 0 && status) {
     // NaN is invalid input; +inf sorts first and stops the selection at once
@@ -161,11 +166,11 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const __grid_consta
     }
     __syncthreads();
     // bucket holding the need-th largest: descending suffix scan (2 buckets / thread)
-    const int per = nb / kSelThreads;  // 2 or 1
+    const int per = nb / kSelThreads;  // buckets per thread
     int c = 0;
     for (int u = 0; u < per; ++u) c += hist[nb - 1 - (tid * per + u)];
     int tot;
-    const int before = block_excl(c, red, &tot);  // keys in buckets above this thread's
+    const int before = block_excl<kWarps>(c, red, &tot);  // keys in buckets above this thread's
     if (before < need && before + c >= need) {
       int cum = before;
       for (int u = 0; u < per; ++u) {
@@ -193,7 +198,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const __grid_consta
 #pragma unroll
     for (int t = 0; t < kItems; ++t) n_eq += (isfinite(v[t]) && order_key(v[t]) == T) ? 1 : 0;
     int eq_tot;
-    int eq_rank = eq_base + block_excl(n_eq, red, &eq_tot);
+    int eq_rank = eq_base + block_excl<kWarps>(n_eq, red, &eq_tot);
     int flags = 0, n_sel = 0;
 #pragma unroll
     for (int t = 0; t < kItems; ++t) {
@@ -210,7 +215,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const __grid_consta
       }
     }
     int sel_tot;
-    int pos = out_base + block_excl(n_sel, red, &sel_tot);
+    int pos = out_base + block_excl<kWarps>(n_sel, red, &sel_tot);
     const int j0 = base + tid * kItems;
 #pragma unroll
     for (int t = 0; t < kItems; ++t)
@@ -283,7 +288,10 @@ cudaError_t launch_select_pack_n(const SelectPackJob* jobs, int n, int l_b, int 
     if (!(l_p > 0 && s.k_out && s.v_out) && j.peers.n > 0)
       return cudaErrorInvalidValue;  // a peer slot is only published through the gather
   }
-  select_kernel<<<n, kSelThreads, 0, stream>>>(J);
+  if (l_b <= kSelSmall * kItems)
+    select_kernel<kSelSmall><<<n, kSelSmall, 0, stream>>>(J);
+  else
+    select_kernel<kSelBig><<<n, kSelBig, 0, stream>>>(J);
   if (gather) gather_kernel<<<dim3((l_p + 7) / 8, n), 256, 0, stream>>>(J);
   return cudaGetLastError();
 }
