@@ -41,7 +41,6 @@ namespace {
 
 constexpr int kVStages = 2;      // V ring depth
 constexpr int kMaxKStages = 3;   // K ring depth (template parameter, <= 3)
-constexpr int kSoftmaxWarps = 8;
 constexpr int kProducerWarp = 8;
 constexpr int kMmaWarp = 9;
 constexpr int kThreads = 320;
@@ -71,6 +70,11 @@ __device__ unsigned long long g_attn_prof[16];
 // 2^x for finite x <= 8 (x clamped at -125), fp32 pair: x = n + f, n = rint(x) via the
 // 1.5*2^23 magic add, 2^f (|f| <= 1/2) by a minimax cubic (max rel. err 7.8e-5), and n
 // added to the exponent field.
+// pair j (of 16 per 32-key chunk) takes the FMA-pipe exp2 when kEmu of every 16 do
+__device__ __forceinline__ constexpr bool emu_slot(int j, int emu) {
+  return emu > 0 && (j % (16 / (emu > 0 ? emu : 1))) == (16 / (emu > 0 ? emu : 1)) - 1;
+}
+
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   x.x = fmaxf(x.x, -125.f);
   x.y = fmaxf(x.y, -125.f);
@@ -378,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
           const float2 x2 = __ffma2_rn(
               make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1])), sl2v, negm);
           float2 p2;
-          if (kEmu > 0 && emu && (j % (16 / kEmu)) == (16 / kEmu) - 1)
+          if (kEmu > 0 && emu && emu_slot(j, kEmu))
             p2 = exp2_poly2(x2);
           else
             p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));  // -inf -> 0
@@ -401,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
           const float2 x2 = __ffma2_rn(
               make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1])), sl2v, negm);
           float2 p2;
-          if (kEmu > 0 && emu && (j % (16 / kEmu)) == (16 / kEmu) - 1)
+          if (kEmu > 0 && emu && emu_slot(j, kEmu))
             p2 = exp2_poly2(x2);
           else
             p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));  // -inf -> 0
@@ -892,7 +896,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd4_kernel(const __grid_con
             const float2 x2 = __ffma2_rn(make_float2(__uint_as_float(sr[c][2 * jv]),
                                                      __uint_as_float(sr[c][2 * jv + 1])), sl2v, negm);
             float2 p2;
-            if (kEmu > 0 && mode == kFull && (jv % (16 / kEmu)) == (16 / kEmu) - 1)
+            if (kEmu > 0 && mode == kFull && emu_slot(jv, kEmu))
               p2 = exp2_poly2(x2);
             else
               p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));
@@ -1180,7 +1184,7 @@ __global__ void __launch_bounds__(kThreads1, 1) attn_fwd1_kernel(const __grid_co
           const float2 x2 = __ffma2_rn(
               make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1])), sl2v, negm);
           float2 p2;
-          if (kEmu > 0 && emu && (j % (16 / kEmu)) == (16 / kEmu) - 1)
+          if (kEmu > 0 && emu && emu_slot(j, kEmu))
             p2 = exp2_poly2(x2);
           else
             p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));  // -inf -> 0
@@ -1552,7 +1556,7 @@ __global__ void __launch_bounds__(kThreads3, 1) attn_fwd3_kernel(const __grid_co
           const float2 x2 = __ffma2_rn(
               make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1])), sl2v, negm);
           float2 p2;
-          if (kEmu > 0 && emu && (j % (16 / kEmu)) == (16 / kEmu) - 1)
+          if (kEmu > 0 && emu && emu_slot(j, kEmu))
             p2 = exp2_poly2(x2);
           else
             p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));
@@ -1989,7 +1993,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd2_kernel(const __grid_con
           const float2 x2 = __ffma2_rn(
               make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1])), sl2v, negm);
           float2 p2;
-          if (kEmu > 0 && emu && (j % (16 / kEmu)) == (16 / kEmu) - 1)
+          if (kEmu > 0 && emu && emu_slot(j, kEmu))
             p2 = exp2_poly2(x2);
           else
             p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));  // -inf -> 0
