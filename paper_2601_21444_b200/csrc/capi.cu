@@ -401,8 +401,10 @@ int peer_signal(spava_fabric* F, cudaStream_t s, int round) {
 
 // the stream waits until every peer's round-`round` slot of this epoch is here
 int peer_wait_arrive(spava_fabric* F, cudaStream_t s, int round) {
+  int n = 0;
   for (int q = 0; q < F->world; ++q)
-    if (q != F->rank) CU_TRY(stream_wait_geq_u32(s, arrive_flag(F->shared.flags, round, q), F->epoch));
+    if (q != F->rank) F->flag_tmp[n++] = arrive_flag(F->shared.flags, round, q);
+  CU_TRY(stream_wait_all_geq_u32(s, F->flag_tmp, n, F->epoch));
   return SPAVA_OK;
 }
 
@@ -410,8 +412,10 @@ int peer_wait_arrive(spava_fabric* F, cudaStream_t s, int round) {
 // this rank may overwrite its slots in their buffers
 int peer_wait_done(spava_fabric* F, cudaStream_t s) {
   if (F->epoch <= 1) return SPAVA_OK;
+  int n = 0;
   for (int q = 0; q < F->world; ++q)
-    if (q != F->rank) CU_TRY(stream_wait_geq_u32(s, done_flag(F->shared.flags, q), F->epoch - 1));
+    if (q != F->rank) F->flag_tmp[n++] = done_flag(F->shared.flags, q);
+  CU_TRY(stream_wait_all_geq_u32(s, F->flag_tmp, n, F->epoch - 1));
   return SPAVA_OK;
 }
 
@@ -1173,9 +1177,10 @@ int spava_fabric_encode_acquire(spava_fabric* F, void* stream) {
   if (!F || !F->peer || !F->peer_ready) return fail(SPAVA_EINVAL, "encode_acquire: peer fabric not open");
   CU_TRY(cudaSetDevice(F->device));
   if (F->enc_epoch == 0) return SPAVA_OK;
+  int n = 0;
   for (int q = 0; q < F->world; ++q)
-    if (q != F->rank)
-      CU_TRY(stream_wait_geq_u32(as_stream(stream), F->shared.flags + Exchange::kDoneEnc + q, F->enc_epoch));
+    if (q != F->rank) F->flag_tmp[n++] = F->shared.flags + Exchange::kDoneEnc + q;
+  CU_TRY(stream_wait_all_geq_u32(as_stream(stream), F->flag_tmp, n, F->enc_epoch));
   return SPAVA_OK;
 }
 
@@ -1203,8 +1208,10 @@ int spava_host_gather_context(spava_host* H, const int64_t* part_rows, int64_t l
   for (int q = 0; q < F->world; ++q)
     if (q != F->rank) F->flag_tmp[n++] = F->at_peer(q, fl) + Exchange::kArrive + 3 * 256 + F->rank;
   CU_TRY(peer_flags_store(st, F->flag_tmp, n, e));
+  n = 0;
   for (int q = 0; q < F->world; ++q)
-    if (q != F->rank) CU_TRY(stream_wait_geq_u32(st, fl + Exchange::kArrive + 3 * 256 + q, e));
+    if (q != F->rank) F->flag_tmp[n++] = fl + Exchange::kArrive + 3 * 256 + q;
+  CU_TRY(stream_wait_all_geq_u32(st, F->flag_tmp, n, e));
   ST_TRY(gather_split_impl(&p, H->h, gp, e_q, ld_q_bytes, dst, ld_dst_bytes, row_bytes, st));
   n = 0;
   for (int q = 0; q < F->world; ++q)  // this rank has read every peer's region

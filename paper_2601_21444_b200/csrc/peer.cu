@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "spava_internal.h"
@@ -27,6 +28,7 @@ namespace {
 
 struct MemOps {
   PFN_cuStreamWaitValue32_v11070 wait = nullptr;
+  PFN_cuStreamBatchMemOp_v11070 batch = nullptr;
   unsigned wait_flags = CU_STREAM_WAIT_VALUE_GEQ;
 };
 
@@ -39,6 +41,10 @@ const MemOps& memops() {
     if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       m.wait = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(p);
+    p = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamBatchMemOp", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      m.batch = reinterpret_cast<PFN_cuStreamBatchMemOp_v11070>(p);
     int dev = 0, flush = 0;
     if (cudaGetDevice(&dev) == cudaSuccess &&
         cudaDeviceGetAttribute(&flush, static_cast<cudaDeviceAttr>(CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES),
@@ -79,6 +85,31 @@ cudaError_t stream_wait_geq_u32(cudaStream_t s, const uint32_t* addr, uint32_t v
   if (!m.wait) return cudaErrorNotSupported;
   return m.wait(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), value, m.wait_flags) ==
                  CUDA_SUCCESS
+             ? cudaSuccess
+             : cudaErrorUnknown;
+}
+
+// every address >= value, as one batched stream memory operation (one host call for all
+// peers' flags of a round instead of one per peer)
+cudaError_t stream_wait_all_geq_u32(cudaStream_t s, const uint32_t* const* addrs, int n, uint32_t value) {
+  if (n <= 0) return cudaSuccess;
+  const MemOps& m = memops();
+  if (!m.batch || n > kMaxPeers) {
+    for (int i = 0; i < n; ++i) {
+      const cudaError_t e = stream_wait_geq_u32(s, addrs[i], value);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  CUstreamBatchMemOpParams ops[kMaxPeers];
+  std::memset(ops, 0, sizeof(ops));
+  for (int i = 0; i < n; ++i) {
+    ops[i].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+    ops[i].waitValue.address = reinterpret_cast<CUdeviceptr>(addrs[i]);
+    ops[i].waitValue.value = value;
+    ops[i].waitValue.flags = m.wait_flags;
+  }
+  return m.batch(reinterpret_cast<CUstream>(s), static_cast<unsigned>(n), ops, 0) == CUDA_SUCCESS
              ? cudaSuccess
              : cudaErrorUnknown;
 }

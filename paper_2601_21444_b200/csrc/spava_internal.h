@@ -145,6 +145,7 @@ cudaError_t launch_gather_split(int l_a, int l_b, int n_t, int n_v, int lo, int 
 // one kernel: system-scope release store of `value` to every address (peer flags)
 cudaError_t peer_flags_store(cudaStream_t s, uint32_t* const* addrs, int n, uint32_t value);
 cudaError_t stream_wait_geq_u32(cudaStream_t s, const uint32_t* addr, uint32_t value);
+cudaError_t stream_wait_all_geq_u32(cudaStream_t s, const uint32_t* const* addrs, int n, uint32_t value);
 
 // ---------------------------------------------------------------- split_context rows
 cudaError_t launch_split_rows(int l_a, int l_b, int n_t, int n_v, int lo, int hi, const void* src,
