@@ -338,6 +338,83 @@ __global__ void __launch_bounds__(256) rowstats_kernel(const __grid_constant__ S
   }
 }
 
+// Short blocks (l_b <= 4096, H >= 4): one WARP per row, 8 rows per CTA -- the same
+// statistics with warp-only reductions (the CTA-per-row kernel is dominated by its two
+// block reductions there).  Tail pads only (n_valid); two streaming passes over the row
+// (the second hits L1/L2).
+__global__ void __launch_bounds__(256) rowstats_warp_kernel(const __grid_constant__ ScoreArgs a, int rows) {
+  __shared__ double tab[16];
+  load_exp_table(tab);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int blk = r >= a.hq * a.n_t ? 1 : 0;
+  const float* L = a.L + static_cast<long long>(r) * a.ldL;
+  const int nv = min(a.n_valid[blk], a.l_b);
+  constexpr int kU = 4;
+  float mxf = -INFINITY;
+  for (int j0 = lane * 4; j0 < nv; j0 += kU * 128) {
+    float4 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      v[u] = j0 + u * 128 < nv ? *reinterpret_cast<const float4*>(L + j0 + u * 128)
+                               : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int j = j0 + u * 128;
+      if (j + 4 <= nv) {
+        mxf = fmaxf(fmaxf(mxf, fmaxf(v[u].x, v[u].y)), fmaxf(v[u].z, v[u].w));
+      } else {
+        if (j < nv) mxf = fmaxf(mxf, v[u].x);
+        if (j + 1 < nv) mxf = fmaxf(mxf, v[u].y);
+        if (j + 2 < nv) mxf = fmaxf(mxf, v[u].z);
+        if (j + 3 < nv) mxf = fmaxf(mxf, v[u].w);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
+  const double sc = static_cast<double>(a.scale);
+  const double mx = static_cast<double>(mxf) * sc;
+  const float lthr = static_cast<float>((mx - 110.0) / sc);
+  double s0 = 0.0, s1 = 0.0;
+  if (mxf != -INFINITY) {
+    for (int j0 = lane * 4; j0 < nv; j0 += kU * 128) {
+      float4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        v[u] = j0 + u * 128 < nv ? *reinterpret_cast<const float4*>(L + j0 + u * 128)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int j = j0 + u * 128;
+        if (j >= nv) continue;
+        double e0 = exp_neg(xrel(v[u].x, lthr, sc, mx), tab);
+        double e1 = exp_neg(xrel(v[u].y, lthr, sc, mx), tab);
+        double e2 = exp_neg(xrel(v[u].z, lthr, sc, mx), tab);
+        double e3 = exp_neg(xrel(v[u].w, lthr, sc, mx), tab);
+        if (j + 4 > nv) {
+          e1 = j + 1 < nv ? e1 : 0.0;
+          e2 = j + 2 < nv ? e2 : 0.0;
+          e3 = j + 3 < nv ? e3 : 0.0;
+        }
+        s0 += e0 + e1;
+        s1 += e2 + e3;
+      }
+    }
+  }
+  double sum = s0 + s1;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) {
+    a.stats[static_cast<long long>(r) * kStat + 0] = mxf == -INFINITY ? -INFINITY : mx;
+    a.stats[static_cast<long long>(r) * kStat + 1] = sum;
+    a.stats[static_cast<long long>(r) * kStat + 2] = 1.0 / sum;
+    a.stats[static_cast<long long>(r) * kStat + 3] = __hiloint2double(0, __float_as_int(lthr));
+  }
+}
+
 __device__ __forceinline__ float lthr_of(const double* st) {
   return __int_as_float(__double2loint(st[3]));
 }
@@ -488,6 +565,8 @@ cudaError_t launch_score_exact2(int nblk, const void* q, long long ldq, int n_t,
     for (int b = 0; b < nblk; ++b) any_pad |= a.pad[b] != nullptr;
     if (any_pad)
       rowstats_kernel<true, 0><<<grid, 256, 0, stream>>>(a);
+    else if (l_b <= 4 * 1024)
+      rowstats_warp_kernel<<<(grid + 7) / 8, 256, 0, stream>>>(a, static_cast<int>(rows));
     else if (l_b <= 8 * 1024)
       rowstats_kernel<false, 8><<<grid, 256, 0, stream>>>(a);
     else if (l_b <= 16 * 1024)
