@@ -396,6 +396,7 @@ int peer_signal(spava_fabric* F, cudaStream_t s, int round) {
   for (int q = 0; q < F->world; ++q)
     if (q != F->rank) F->flag_tmp[n++] = arrive_flag(F->at_peer(q, F->shared.flags), round, F->rank);
   CU_TRY(peer_flags_store(s, F->flag_tmp, n, F->epoch));
+  if (n > 0) ++g_launches;
   return SPAVA_OK;
 }
 
@@ -425,6 +426,7 @@ int peer_release(spava_fabric* F, cudaStream_t s) {
   for (int q = 0; q < F->world; ++q)
     if (q != F->rank) F->flag_tmp[n++] = done_flag(F->at_peer(q, F->shared.flags), F->rank);
   CU_TRY(peer_flags_store(s, F->flag_tmp, n, F->epoch));
+  if (n > 0) ++g_launches;
   return SPAVA_OK;
 }
 
@@ -1208,6 +1210,7 @@ int spava_host_gather_context(spava_host* H, const int64_t* part_rows, int64_t l
   for (int q = 0; q < F->world; ++q)
     if (q != F->rank) F->flag_tmp[n++] = F->at_peer(q, fl) + Exchange::kArrive + 3 * 256 + F->rank;
   CU_TRY(peer_flags_store(st, F->flag_tmp, n, e));
+  if (n > 0) ++g_launches;
   n = 0;
   for (int q = 0; q < F->world; ++q)
     if (q != F->rank) F->flag_tmp[n++] = fl + Exchange::kArrive + 3 * 256 + q;
@@ -1217,6 +1220,7 @@ int spava_host_gather_context(spava_host* H, const int64_t* part_rows, int64_t l
   for (int q = 0; q < F->world; ++q)  // this rank has read every peer's region
     if (q != F->rank) F->flag_tmp[n++] = F->at_peer(q, fl) + Exchange::kDoneEnc + F->rank;
   CU_TRY(peer_flags_store(st, F->flag_tmp, n, e));
+  if (n > 0) ++g_launches;
   return SPAVA_OK;
 }
 
