@@ -108,6 +108,33 @@ def inproc(world, layers):
     print(f"PEER_OK all {layers}", flush=True)
 
 
+def trace_inproc(world, layers):
+    """Peer-fabric layers with the event trace on; prints the trace JSONL (reference
+    Event schema, Lamport clocks) between markers for the reference validator."""
+    cfg, rows, _, _, _ = inputs(world, 0)
+    fabs = [spava.Fabric.create_peer(cfg, 0, world, r) for r in range(world)]
+    spava.Fabric.peer_attach(fabs)
+    hosts = [f.host(r) for r, f in enumerate(fabs)]
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    for h in hosts:
+        h.set_trace(True)
+    for layer in range(layers):
+        _, _, qs, ks, vs = inputs(world, layer)
+        outs = [torch.zeros(rows, HQ * 128, dtype=torch.bfloat16, device="cuda:0") for _ in hosts]
+        torch.cuda.synchronize()
+        for r in range(world):
+            hosts[r].layer(qs[r], ks[r], vs[r], outs[r], stream=streams[r])
+        torch.cuda.synchronize()
+    events = spava.trace_events([h.trace_records() for h in hosts])
+    print("TRACE_JSONL_BEGIN")
+    print(spava.trace_jsonl(events))
+    print("TRACE_JSONL_END", flush=True)
+    for h in hosts:
+        h.close()
+    for f in fabs:
+        f.close()
+
+
 def encode_inproc(world, rounds):
     """Frame-parallel encode gather over the peer fabric: every rank's E_v share lives in
     its encode region; gather_context must equal split_context of the concatenation."""
@@ -185,6 +212,8 @@ if __name__ == "__main__":
     mode = sys.argv[1]
     if mode == "inproc":
         inproc(int(sys.argv[2]), int(sys.argv[3]))
+    elif mode == "trace":
+        trace_inproc(int(sys.argv[2]), int(sys.argv[3]))
     elif mode == "encode":
         encode_inproc(int(sys.argv[2]), int(sys.argv[3]))
     else:

@@ -90,3 +90,22 @@ def test_host_layer_trace_overlap(cuda, nccl):
         assert t[("compute_begin", "merge")] >= t[("compute_end", "stage2")]
     host.close()
     fab.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_fabric_trace_passes_reference_validator(cuda, world):
+    """Peer fabric (ranks on one GPU, in one process): the per-rank program-order traces of
+    two layers, joined by the exchange rounds' Lamport clocks, pass validate_trace."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32", CUDA_MODULE_LOADING="EAGER",
+               PYTHONPATH=ROOT + os.pathsep + os.environ.get("PYTHONPATH", ""))
+    r = subprocess.run([sys.executable, "-m", "tests.peer_worker", "trace", str(world), "2"], cwd=ROOT,
+                       env=env, capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    body = r.stdout.split("TRACE_JSONL_BEGIN\n", 1)[1].split("TRACE_JSONL_END", 1)[0]
+    lines = [x for x in body.splitlines() if x.strip()]
+    assert len(lines) == world * 2 * 19
+    n, msg = ref_validate("\n".join(lines) + "\n")
+    assert n == 0, msg
