@@ -14,7 +14,8 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libspava_b200.so")
+# SPAVA_LIB: dev-only override (A/B timing of two builds of the same C ABI)
+LIB_PATH = os.environ.get("SPAVA_LIB") or os.path.join(HERE, "libspava_b200.so")
 
 __all__ = [
     "SpavaError", "lib", "Plan", "LayerConfig", "Fabric", "Host", "make_plan", "default_plan",
