@@ -27,6 +27,7 @@ the measured bf16 tensor peak; cpu_baseline = the reference's own operators
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import statistics
@@ -142,113 +143,70 @@ class ClockSampler:
 
 
 # -------------------------------------------------------- reference CPU baseline
-def reference_rate(g, hq, hkv, threads, budget_s, seed=0, impl=None):
-    """Time the reference's own operators (oracle/_ref: the unmodified seqpar C++ sources;
-    'port' = the C restatement if _ref is absent) on a bounded, FLOP-weighted sample of this
-    layer's attention + scoring calls, spread over `threads` host threads (ctypes releases
-    the GIL).  Row slices of a block are exact sub-problems of block_attention: rows
-    [r0,r1) see [anchor | passing | own[0:r0) | own[r0:r1) causal], the same keys in the
-    same order as the full call (approx.cpp:140-154).  Returns (flop/s, description)."""
-    import concurrent.futures as cf
+def reference_job(g, hq, hkv, steps, warmup, threads, max_s=100.0, seed=1234, m=128):
+    """The reference's own operators (oracle/_ref: the unmodified seqpar C++ sources; the C
+    restatement if _ref is absent) over ONE Spava layer of the whole job on the host cores,
+    on the same synthetic inputs as the GPU arm (oracle/layer_ref.layer_inputs, same seed):
+    every block's score_block + select_essential, then anchor / block / query attention as
+    row-slice x head work items (exact sub-problems of the full calls, run_host order
+    simhost.cpp:328-426).  The layer's work items are split over the `steps` timed steps
+    (scoring first), so the steps together execute the layer once; when the estimated
+    layer time exceeds `max_s` a uniform, FLOP-stratified fraction of the attention items
+    runs instead and the rate is extrapolated (said in `sample`).  Returns a dict."""
+    from oracle import layer_ref as LR
 
-    import numpy as np
-
-    from oracle import oracle as O
-
-    impl = impl or ("ref" if O.available("ref") else "c")
-    rng = np.random.default_rng(seed)
-    H, l_a, l_b, l_p, n_t = g["hosts"], g["l_a"], g["l_b"], g["l_p"], g["n_t"]
-    d = hq * DH
-
-    def rnd(*s):
-        return rng.standard_normal(s, dtype=np.float32)
-
-    # one representative physical host: h = H-1 (carries the query self keys, zigzag
-    # pair (H-1, H) -> block hi has the largest passing set of its pair)
-    h = H - 1
-    lo, hi = (h, 2 * H - 1 - h) if g["zigzag"] else (2 * h, 2 * h + 1)
-    qb, kb, vb = rnd(l_b, d), rnd(l_b, d), rnd(l_b, d)          # one block (reused lo/hi)
-    ka, va = rnd(l_a, d), rnd(l_a, d)
-    kp, vp = rnd(max(hi, 1) * l_p, d), rnd(max(hi, 1) * l_p, d)  # passing for block hi
-    qq, kq, vq = rnd(n_t, d), rnd(n_t, d), rnd(n_t, d)
-    items = []
-    m = 16  # rows per block item
-    for v in (lo, hi):
-        n_p = v * l_p
-        for r0 in range(0, l_b, m):
-            r1 = min(l_b, r0 + m)
-            items.append(("block", v, r0, r1, (4 * (r1 - r0) * (l_a + n_p + r0) + 2 * (r1 - r0) ** 2) * d))
-    for r0 in range(0, l_a, m):
-        r1 = min(l_a, r0 + m)
-        items.append(("anchor", 0, r0, r1, (4 * (r1 - r0) * r0 + 2 * (r1 - r0) ** 2) * d))
-    a = l_a // H + (1 if h < l_a % H else 0)
-    for r0 in range(0, n_t, m):
-        r1 = min(n_t, r0 + m)
-        items.append(("query", 0, r0, r1, (4 * (r1 - r0) * (a + 2 * l_b + r0) + 2 * (r1 - r0) ** 2) * d))
-    for v in range(2):
-        for hh in range(hq):
-            items.append(("score", v, hh, 0, 2 * n_t * l_b * DH))
-    total_flops_host = sum(it[4] for it in items)
-    order = rng.permutation(len(items))
-
-    def run(it):
-        kind, v, r0, r1, fl = it
-        if kind == "block":
-            n_p = v * l_p
-            segs = [dict(k=ka, v=va)]
-            if n_p:
-                segs.append(dict(k=kp[:n_p], v=vp[:n_p]))
-            if r0:
-                segs.append(dict(k=kb[:r0], v=vb[:r0]))
-            segs.append(dict(k=kb[r0:r1], v=vb[r0:r1], causal=True))
-            O.mha_lse(qb[r0:r1], segs, hq, hq, DH, allow_invalid=True, impl=impl)
-        elif kind == "anchor":
-            segs = ([dict(k=ka[:r0], v=va[:r0])] if r0 else []) + [dict(k=ka[r0:r1], v=va[r0:r1], causal=True)]
-            O.mha_lse(ka[r0:r1], segs, hq, hq, DH, impl=impl)
-        elif kind == "query":
-            segs = [dict(k=ka[:a], v=va[:a]), dict(k=kb, v=vb), dict(k=kb, v=vb)]
-            if r0:
-                segs.append(dict(k=kq[:r0], v=vq[:r0]))
-            segs.append(dict(k=kq[r0:r1], v=vq[r0:r1], causal=True))
-            O.mha_lse(qq[r0:r1], segs, hq, hq, DH, allow_invalid=True, impl=impl)
-        else:
-            O.score_context(np.ascontiguousarray(qq[:, r0 * DH:(r0 + 1) * DH]),
-                            np.ascontiguousarray(kb[:, r0 * DH:(r0 + 1) * DH]),
-                            1.0 / np.sqrt(np.float32(DH)), None, True, impl=impl)
-        return fl
-
-    done_flops, t0 = 0, time.perf_counter()
-    n_done = 0
-    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
-        futs = []
-        nxt = 0
-        while nxt < len(order) and len(futs) < threads:
-            futs.append(ex.submit(run, items[order[nxt]]))
-            nxt += 1
-        while futs:
-            doneset, _ = cf.wait(futs, return_when=cf.FIRST_COMPLETED)
-            for f in doneset:
-                done_flops += f.result()
-                n_done += 1
-                futs.remove(f)
-                if nxt < len(order) and time.perf_counter() - t0 < budget_s:
-                    futs.append(ex.submit(run, items[order[nxt]]))
-                    nxt += 1
-    el = time.perf_counter() - t0
-    rate = done_flops / el
-    desc = (f"{n_done} of {len(items)} work items (row slices of 16 rows of anchor/block/query "
-            f"attention + per-head score_context) of host {h}'s C1-geometry layer, "
-            f"{done_flops / total_flops_host:.2%} of its FLOPs, {el:.1f}s on {threads} threads; "
-            f"layer time extrapolated as FLOPs / measured rate (impl={'reference' if impl == 'ref' else 'port'})")
-    return rate, desc, ("reference" if impl == "ref" else "port")
-
-
-def reference_tokens_per_s(g, hq, hkv, threads, budget_s, seed=0):
-    rate, desc, kind = reference_rate(g, hq, hkv, threads, budget_s, seed)
+    Q, K, V = LR.layer_inputs(g, hq, hkv, seed=seed)
+    ref = LR.LayerRef(Q, K, V, g, hq, hkv)
     H = g["hosts"]
-    total = sum(attn_flops_host(g, hq, h, g["zigzag"]) for h in range(H)) + H * score_flops_host(g, hq)
-    layer_s = total / rate  # all hosts' work on the same `threads` cores
-    return g["n"] / layer_s, layer_s, rate, desc, kind
+    score = ref.score_items()
+    attn = ref.attention_items(range(g["l_a"]), {v: range(LR.valid_rows(g, v)) for v in range(2 * H)},
+                               range(g["n_t"]), m=m)
+    # the anchor is computed by every host (redundantly, simhost.cpp:308-311): count it H times
+    total = sum(it[5] for it in score) + sum(it[5] * (H if it[0] == "anchor" else 1) for it in attn)
+    est_rate = 2.0e9 * threads  # ~2 GFLOP/s per core (scalar fp32 reference, SURVEY s8d)
+    frac = min(1.0, max_s * est_rate / total)
+    if frac < 1.0:  # stratified: every k-th item in FLOP order
+        attn = sorted(attn, key=lambda it: it[5])
+        k = int(round(1.0 / frac))
+        attn = attn[::k]
+    done_total = sum(it[5] for it in score) + sum(it[5] * (H if it[0] == "anchor" else 1) for it in attn)
+    frac = done_total / total
+    seq = score + [None] + attn  # None: score_block totals + select_essential of every block
+    per = sum(it[5] for it in seq if it) / max(1, steps)
+    groups, cur, acc = [], [], 0.0
+    for it in seq:
+        cur.append(it)
+        acc += it[5] if it else 0.0
+        if acc >= per * (len(groups) + 1) and len(groups) < steps - 1:
+            groups.append(cur)
+            cur = []
+    groups.append(cur)
+    while len(groups) < steps:
+        groups.append([])
+    for _ in range(warmup):  # untimed: a few scoring items (their results are overwritten)
+        LR.run_items(ref.run_item, score[:threads], threads)
+    step_s = []
+    for grp in groups:
+        t0 = time.perf_counter()
+        if None in grp:
+            i = grp.index(None)
+            LR.run_items(ref.run_item, grp[:i], threads)
+            ref.finish_scores()
+            LR.run_items(ref.run_item, grp[i + 1:], threads)
+        elif grp:
+            LR.run_items(ref.run_item, grp, threads)
+        step_s.append(time.perf_counter() - t0)
+    layer_s = sum(step_s) / frac
+    kind = "reference" if ref.impl == "ref" else "port"
+    sample = (f"one whole layer of the job ({H} host(s): scores + select of {2 * H} blocks, "
+              f"anchor/block/query attention as {m}-row x head work items) split over {steps} steps, "
+              f"{sum(step_s):.1f} s on {threads} threads"
+              if frac >= 0.999 else
+              f"{frac:.1%} of one layer's FLOPs (all scoring + every {int(round(1 / max(frac, 1e-9)))}-th "
+              f"attention work item in FLOP order) split over {steps} steps, {sum(step_s):.1f} s on "
+              f"{threads} threads; layer time extrapolated as measured time / FLOP fraction")
+    return dict(value=g["n"] / layer_s, layer_s=layer_s, step_s=step_s, frac=frac, kind=kind,
+                sample=sample, gflops_per_s=done_total / sum(step_s) / 1e9, impl=ref.impl)
 
 
 # --------------------------------------------------------------------- arms
@@ -259,33 +217,44 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), local
 
 
+def job_config(args, world):
+    """(config name, cfg, geometry) of the job: C1 on one GPU (BASELINE configs[1]); the
+    128K-token C3 (north_star's scaling target) at N > 1 unless --config says otherwise."""
+    name = args.config or ("C1" if max(world, args.gpus) == 1 else "C3")
+    cfg = CONFIGS[name]
+    return name, cfg, geometry(cfg, max(world, args.gpus))
+
+
+def config_dict(name, cfg, g, H, fabric=None, fabric_note=None):
+    """The `config` object both arms print (identical keys and values for the same job)."""
+    return {"workload": f"{name}: {cfg['desc']}", "n": g["n"], "n_t": g["n_t"], "l_a": g["l_a"],
+            "l_b": g["l_b"], "l_p": g["l_p"], "hosts": H, "heads": f"{cfg['hq']}q/{cfg['hkv']}kv",
+            "dh": DH, "layers_per_step": 1,
+            "parallelism": f"sp{H} (Spava zigzag virtual hosts, one per GPU)",
+            "inputs": "oracle/layer_ref.layer_inputs(seed=1234): N(0,1) rounded to bf16, same bits in both arms",
+            "scoring": "exact (score_block arithmetic order, selection bit-exact vs the reference)"}
+
+
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    cfg = CONFIGS[args.config]
-    g = geometry(cfg, max(world, args.gpus))
+    name, cfg, g = job_config(args, world)
+    H = g["hosts"]
     threads = os.cpu_count() or 1
-    per_step = max(1.0, min(8.0, 150.0 / max(1, args.steps + args.warmup)))
-    for _ in range(args.warmup):
-        reference_tokens_per_s(g, cfg["hq"], cfg["hkv"], threads, per_step / 2)
-    vals, descs, kind = [], [], "reference"
-    for s in range(args.steps):
-        v, layer_s, rate, desc, kind = reference_tokens_per_s(g, cfg["hq"], cfg["hkv"], threads, per_step, seed=s)
-        vals.append(v)
-        descs.append(desc)
-    value = statistics.median(vals)
+    r = reference_job(g, cfg["hq"], cfg["hkv"], args.steps, args.warmup, threads, max_s=args.ref_max_s)
+    ms = [x * 1e3 for x in r["step_s"]]
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": "tokens/s",
         "n_gpus": max(world, args.gpus), "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": g["n"] / value * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic N(0,1)",
-        "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g["n"],
-                   "n_t": g["n_t"], "l_a": g["l_a"], "l_b": g["l_b"], "l_p": g["l_p"],
-                   "hosts": g["hosts"], "parallelism": f"sp{g['hosts']} (simulated hosts on CPU)"},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": kind,
-                         "sample": descs[-1]},
-        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "ms_per_step": sum(ms) / len(ms), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic N(0,1) bf16-valued activations",
+        "config": config_dict(name, cfg, g, H),
+        "cpu_baseline": {"value": r["value"], "unit": "tokens/s", "cores": threads, "kind": r["kind"],
+                         "sample": r["sample"], "layer_s": round(r["layer_s"], 2),
+                         "gflops_per_s": round(r["gflops_per_s"], 2), "fraction_of_layer": round(r["frac"], 4)},
+        "e2e": {"value": r["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_ms": [round(x, 1) for x in ms],
     }
     print(json.dumps(line), flush=True)
 
@@ -315,11 +284,191 @@ def bind_gpu_numa(dev_index):
     return None
 
 
+def make_fabric(spava, dist, lc, local, world, rank, fabric):
+    """This rank's fabric: local (N=1), peer (NVLink stores + epoch flags) or NCCL."""
+    note, peer_err = None, ""
+    if world == 1:
+        return spava.Fabric(lc, local), "local", note, peer_err
+    fab = None
+    if fabric == "peer":
+        fab = spava.Fabric.create_peer(lc, local, world, rank)
+        handles = [None] * world
+        dist.all_gather_object(handles, fab.peer_handle())
+        try:
+            fab.peer_open(handles)
+        except spava.SpavaError as e:  # e.g. peers not visible to this process
+            peer_err = str(e)[:160]
+        errs = [None] * world
+        dist.all_gather_object(errs, peer_err)
+        if any(errs):  # every rank switches together
+            note = "peer open failed (" + next(x for x in errs if x) + "); nccl used"
+            fab.close()
+            fab = None
+            fabric = "nccl"
+    if fab is None:
+        obj = [spava.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        fab = spava.Fabric(lc, local, unique_id=obj[0], world=world, rank=rank)
+    return fab, fabric, note, peer_err
+
+
+def hbm_rooflines(g, hq, hkv, tim, steps, hbm_peak):
+    """Achieved HBM GB/s of the scorer and of select + pack (north_star: against ~8 TB/s),
+    from the algorithmic bytes of SURVEY s8d and the kernels' device time per step."""
+    l_b, l_p, n_t = g["l_b"], g["l_p"], g["n_t"]
+    b_sel = 2 * (4 * l_b + 4 * l_p + 2 * 2 * l_p * hkv * DH * 2)      # scores in, idx + K/V rows
+    b_score = n_t * hq * DH * 2 + 2 * l_b * hkv * DH * 2 + 2 * 4 * l_b  # Q_qr + 2 K blocks + scores
+    sel_ms = tim["select_ms"] / steps
+    sc_ms = tim["score_ms"] / steps
+    f_score = score_flops_host(g, hq)
+    out = {}
+    if sel_ms > 0:
+        a = b_sel / (sel_ms / 1e3) / 1e9
+        out["select_pack"] = {"bound": "hbm", "achieved": round(a, 1), "peak": hbm_peak, "unit": "GB/s",
+                              "frac": round(a / hbm_peak, 4), "bytes_per_step": b_sel,
+                              "ms_per_step": round(sel_ms, 4),
+                              "note": "select (radix select + ordered scan, one CTA per block) + "
+                                      "gather of the passing K/V rows; latency-bound at these sizes"}
+    if sc_ms > 0:
+        a = b_score / (sc_ms / 1e3) / 1e9
+        out["score"] = {"bound": "fp32/fp64 CUDA cores (exact mode; intensity n_t*hq/hkv flop/B)",
+                        "achieved_hbm": round(a, 1), "peak_hbm": hbm_peak, "unit": "GB/s",
+                        "frac_hbm": round(a / hbm_peak, 4), "bytes_per_step": b_score,
+                        "flops_per_step": f_score, "tflops": round(f_score / (sc_ms / 1e3) / 1e12, 2),
+                        "ms_per_step": round(sc_ms, 4)}
+    return out
+
+
+def time_layer(torch, host, q, k, v, out, sel, stream, flush, steps, warmup):
+    """warm-up, then `steps` layers bracketed by events (L2 flushed outside the events)."""
+    for _ in range(warmup):
+        host.layer(q, k, v, out, sel, stream)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        host.layer(q, k, v, out, sel, stream)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ev]
+
+
+def sweep_line(torch, spava, name, local, stream, flush, steps, pk):
+    """One more single-GPU configuration on the N=1 line (BASELINE's 1/2/4/8 sweep config
+    C4 at H=1, and C3 at H=1 for the 128K scaling curve): tokens/s, attention roofline and
+    e2e through the host-buffer C-ABI call.  Inputs are drawn on the device (not compared)."""
+    cfg = CONFIGS[name]
+    g = geometry(cfg, 1)
+    hq, hkv = cfg["hq"], cfg["hkv"]
+    lc = spava.LayerConfig.make(g["n_v"], g["n_t"], 1, g["l_a"], g["l_p"], hq, hkv, DH)
+    fab = spava.Fabric(lc, local)
+    host = fab.host(0)
+    dev = torch.device("cuda", local)
+    gen = torch.Generator(device=dev).manual_seed(99)
+    rows = host.rows
+    q = torch.randn((rows, hq * DH), generator=gen, device=dev).to(torch.bfloat16)
+    k = torch.randn((rows, hkv * DH), generator=gen, device=dev).to(torch.bfloat16)
+    v = torch.randn((rows, hkv * DH), generator=gen, device=dev).to(torch.bfloat16)
+    out = torch.empty((rows, hq * DH), dtype=torch.bfloat16, device=dev)
+    sel = torch.empty((2, max(g["l_p"], 1)), dtype=torch.int32, device=dev)
+    host.set_timing(True)
+    step_ms = time_layer(torch, host, q, k, v, out, sel, stream, flush, steps, 1)
+    tim = host.timing()
+    host.set_timing(False)
+    ms = sum(step_ms) / steps
+    # timing covers warm-up + steps launches: normalise by the launch count
+    n_layers = steps + 1
+    ach = tim["attention_flops"] / (tim["attention_ms"] / 1e3) / 1e12
+    res = {"workload": f"{name}: {cfg['desc']}", "hosts": 1, "n": g["n"], "l_b": g["l_b"], "l_p": g["l_p"],
+           "heads": f"{hq}q/{hkv}kv", "value": g["n"] / (ms / 1e3), "unit": "tokens/s", "ms_per_step": round(ms, 3),
+           "steps": steps,
+           "roofline": {"bound": "tensor", "achieved": round(ach, 1), "peak": pk["bf16_burst"], "unit": "TFLOP/s",
+                        "frac": round(ach / pk["bf16_burst"], 4),
+                        "flops_per_step": tim["attention_flops"] / n_layers,
+                        "kernel_ms_per_step": round(tim["attention_ms"] / n_layers, 3)}}
+    try:  # e2e through the host-buffer entry point
+        qh, kh, vh = q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory()
+        oh = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        selh = torch.empty(sel.shape, dtype=sel.dtype).pin_memory()
+        host.layer_hostbuf(qh, kh, vh, oh, q, k, v, out, selh, sel, stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n2 = max(2, min(steps, 3))
+        e0.record(stream)
+        for _ in range(n2):
+            host.layer_hostbuf(qh, kh, vh, oh, q, k, v, out, selh, sel, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1) / n2
+        res["e2e"] = {"value": g["n"] / (ems / 1e3), "unit": "tokens/s", "ms_per_step": round(ems, 3),
+                      "h2d_bytes_per_step": (q.numel() + k.numel() + v.numel()) * 2,
+                      "d2h_bytes_per_step": out.numel() * 2}
+        del qh, kh, vh, oh
+    except Exception as e:  # pragma: no cover
+        res["e2e"] = {"error": str(e)[:200]}
+    # dense exact causal attention over the same sequence on one GPU (our kernel)
+    try:
+        n = g["n"]
+        qd = torch.randn((n, hq * DH), generator=gen, device=dev).to(torch.bfloat16)
+        kd = torch.randn((n, hkv * DH), generator=gen, device=dev).to(torch.bfloat16)
+        vd = torch.randn((n, hkv * DH), generator=gen, device=dev).to(torch.bfloat16)
+        del q, k, v, out
+        segs = [dict(k=kd, v=vd, causal=True)]
+        spava.attention(qd, segs, hq, hkv)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        spava.attention(qd, segs, hq, hkv)
+        e1.record()
+        torch.cuda.synchronize()
+        dms = e0.elapsed_time(e1)
+        res["dense_exact"] = {"ms": round(dms, 3), "tokens_per_s": n / (dms / 1e3),
+                              "tflops": round(2.0 * n * n * hq * DH / (dms / 1e3) / 1e12, 1),
+                              "spava_speedup": round(dms / ms, 2)}
+        del qd, kd, vd
+    except Exception as e:  # pragma: no cover
+        res["dense_exact"] = {"error": str(e)[:200]}
+    host.close()
+    fab.close()
+    torch.cuda.empty_cache()
+    return res
+
+
+def self_check(torch, spava, g, hq, hkv, Q, K, V, out, sel, rank, local):
+    """N > 1: this rank's passing indices and outputs against a one-GPU spava_sim_layer of
+    all H hosts on the same inputs (local fabric; bit-identical by construction)."""
+    from oracle import layer_ref as LR
+
+    H = g["hosts"]
+    dev = torch.device("cuda", local)
+    lc = spava.LayerConfig.make(g["n_v"], g["n_t"], H, g["l_a"], g["l_p"], hq, hkv, DH)
+    fab = spava.Fabric(lc, local)
+    hs, ins, outs, sels = [], [], [], []
+    for h in range(H):
+        hs.append(fab.host(h))
+        rows = LR.host_rows(g, h)
+        ins.append([torch.from_numpy(X[rows]).to(dev).to(torch.bfloat16) for X in (Q, K, V)])
+        outs.append(torch.empty((hs[-1].rows, hq * DH), dtype=torch.bfloat16, device=dev))
+        sels.append(torch.empty((2, max(g["l_p"], 1)), dtype=torch.int32, device=dev))
+    fab.sim_layer(hs, [x[0] for x in ins], [x[1] for x in ins], [x[2] for x in ins], outs, sels)
+    torch.cuda.synchronize()
+    res = {"indices_equal": bool(torch.equal(sels[rank], sel)),
+           "out_max_abs_diff": float((outs[rank].float() - out.float()).abs().max()),
+           "out_bit_identical": bool(torch.equal(outs[rank], out)),
+           "reference": "spava_sim_layer of all hosts on one GPU (local fabric), same inputs"}
+    for h in hs:
+        h.close()
+    fab.close()
+    del ins, outs, sels
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_spava_arm(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
+    from oracle import layer_ref as LR
     from paper_2601_21444_b200 import spava
 
     rank, world, local = dist_env()
@@ -329,12 +478,10 @@ def run_spava_arm(args):
     all_cpus = os.sched_getaffinity(0)
     numa_cpus = bind_gpu_numa(local)
     dev = torch.device("cuda", local)
-    cfg = CONFIGS[args.config]
+    name, cfg, g = job_config(args, world)
     H = max(world, 1)
-    g = geometry(cfg, H)
     hq, hkv = cfg["hq"], cfg["hkv"]
     lc = spava.LayerConfig.make(g["n_v"], g["n_t"], H, g["l_a"], g["l_p"], hq, hkv, DH)
-    fabric_note = None
     if world > 1:
         if os.environ.get("SPAVA_BENCH_ONE_GPU") == "1":
             if args.fabric != "peer":
@@ -342,37 +489,14 @@ def run_spava_arm(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
-        fab = None
-        if args.fabric == "peer":
-            # exchange rounds as NVLink stores from the producing kernels (IPC-mapped peer
-            # exchange buffers) + epoch flags; torch.distributed only ships the handles
-            fab = spava.Fabric.create_peer(lc, local, world, rank)
-            handles = [None] * world
-            dist.all_gather_object(handles, fab.peer_handle())
-            err = ""
-            try:
-                fab.peer_open(handles)
-            except spava.SpavaError as e:  # e.g. peers not visible to this process
-                err = str(e)[:160]
-            errs = [None] * world
-            dist.all_gather_object(errs, err)
-            if any(errs):  # every rank switches together
-                fabric_note = "peer open failed (" + next(x for x in errs if x) + "); nccl used"
-                fab.close()
-                fab = None
-                args.fabric = "nccl"
-        if fab is None:
-            obj = [spava.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            fab = spava.Fabric(lc, local, unique_id=obj[0], world=world, rank=rank)
-    else:
-        fab = spava.Fabric(lc, local)
+    fab, fabric, fabric_note, peer_err = make_fabric(spava, dist, lc, local, world, rank, args.fabric)
     host = fab.host(rank)
     rows = host.rows
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    q = torch.randn((rows, hq * DH), generator=gen, device=dev).to(torch.bfloat16)
-    k = torch.randn((rows, hkv * DH), generator=gen, device=dev).to(torch.bfloat16)
-    v = torch.randn((rows, hkv * DH), generator=gen, device=dev).to(torch.bfloat16)
+    # the same synthetic layer as the reference arm (global rows, this host's share)
+    Q, K, V = LR.layer_inputs(g, hq, hkv, seed=1234)
+    hr = LR.host_rows(g, rank)
+    q, k, v = [torch.from_numpy(X[hr]).to(dev).to(torch.bfloat16) for X in (Q, K, V)]
+    assert q.shape[0] == rows
     out = torch.empty((rows, hq * DH), dtype=torch.bfloat16, device=dev)
     sel = torch.empty((2, max(g["l_p"], 1)), dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -382,11 +506,8 @@ def run_spava_arm(args):
         if world > 1:
             dist.barrier()
 
-    def step():
-        host.layer(q, k, v, out, sel, stream)
-
     for _ in range(args.warmup):
-        step()
+        host.layer(q, k, v, out, sel, stream)
     torch.cuda.synchronize()
     st = host.status()
     if st != 0:
@@ -403,7 +524,7 @@ def run_spava_arm(args):
         for i in range(args.steps):
             flush.zero_()
             ev[i][0].record(stream)
-            step()
+            host.layer(q, k, v, out, sel, stream)
             ev[i][1].record(stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - wall0
@@ -416,9 +537,11 @@ def run_spava_arm(args):
     t = torch.tensor([ms, tim["attention_ms"] / args.steps], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, attn_ms_max = float(t[0]), float(t[1])
+    ms_max = float(t[0])
     tokens = g["n"]  # one sequence of n tokens per step for the whole job
     value = tokens / (ms_max / 1e3)
+    out_timed = out.clone()
+    sel_timed = sel.clone()
 
     # ---------------- e2e through the C-ABI call with pinned host buffers
     qh = q.cpu().pin_memory()
@@ -452,6 +575,7 @@ def run_spava_arm(args):
     e2e_ms = float(t2[0])
     h2d = (q.numel() + k.numel() + v.numel()) * 2
     d2h = out.numel() * 2
+    e2e_same = bool(torch.equal(oh.to(dev), out_timed))
     # copy floor: the same bytes as bare pinned copies (H2D and D2H on two streams at once),
     # i.e. the PCIe time the host-buffer layer hides its compute under
     s_up, s_dn = torch.cuda.Stream(), torch.cuda.Stream()
@@ -474,6 +598,7 @@ def run_spava_arm(args):
         torch.cuda.synchronize()
         floor.append(c0.elapsed_time(c1))
     copy_floor_ms = min(floor[1:])
+    del qh, kh, vh, oh
 
     # ---------------- isolated kernel timing (scorer serialized on the step stream) so the
     # attention kernel's own efficiency is visible next to the overlapped timed region
@@ -482,10 +607,25 @@ def run_spava_arm(args):
     torch.cuda.synchronize()
     for _ in range(iso_steps):
         flush.zero_()
-        step()
+        host.layer(q, k, v, out, sel, stream)
     torch.cuda.synchronize()
     tim_iso = host.timing()
     host.set_timing(False)
+
+    # ---------------- N > 1: self-check against one GPU + per-rank exchange evidence
+    rank_info = {"rank": rank, "device": torch.cuda.get_device_name(local), "fabric": fabric,
+                 "peer_open_error": peer_err or None,
+                 "nccl_ranks": world if fabric == "nccl" else 0, "ms_per_step": round(ms, 4),
+                 "attention_ms_per_step": round(tim["attention_ms"] / args.steps, 4)}
+    if world > 1:
+        if not args.no_self_check:
+            rank_info["self_check"] = self_check(torch, spava, g, hq, hkv, Q, K, V, out_timed, sel_timed,
+                                                 rank, local)
+        ranks = [None] * world
+        dist.all_gather_object(ranks, rank_info)
+    else:
+        ranks = None
+    del Q, K, V
 
     if rank != 0:
         if world > 1:
@@ -499,19 +639,27 @@ def run_spava_arm(args):
     pk = peaks()
     attn_flops_step = tim["attention_flops"] / args.steps
     achieved = attn_flops_step / (tim["attention_ms"] / args.steps / 1e3) / 1e12
-    peak = pk["bf16_sustained"]
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "r01_ncu_step.json")
-    if os.path.exists(tp):
+    clocks = clk.summary()
+    # the step is milliseconds long at full clocks: the burst peak applies (MEASURED_PEAKS
+    # recorded the sustained figure at a power-capped 1215 MHz median)
+    peak = pk["bf16_burst"]
+    traffic, traffic_src = None, None
+    for tp in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_step.json")), reverse=True):
         try:
             with open(tp) as f:
-                traffic = json.load(f).get(args.config, {}).get("dram_bytes_per_launch")
+                traffic = json.load(f).get(name, {}).get("dram_bytes_per_launch")
+            if traffic:
+                traffic_src = os.path.relpath(tp, ROOT)
+                break
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
-                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_src": traffic_src,
                 "kernel": "attn_fwd_kernel (tcgen05, all attention launches of the step)",
-                "peak_src": f"{pk['src']} bf16 sustained (MEASURED_PEAKS.json)",
+                "peak_src": f"{pk['src']} bf16 burst (MEASURED_PEAKS.json bf16_tflops; clocks at "
+                            f"{clocks.get('sm_mhz')} of {clocks.get('sm_max_mhz')} MHz)",
+                "peak_sustained": pk["bf16_sustained"],
+                "frac_vs_sustained": round(achieved / pk["bf16_sustained"], 4),
                 "flops_per_step": attn_flops_step,
                 "kernel_ms_per_step": round(tim["attention_ms"] / args.steps, 4),
                 "share_of_step": round(tim["attention_ms"] / args.steps / ms, 3),
@@ -529,12 +677,14 @@ def run_spava_arm(args):
                             "select_ms_per_step": round(tim_iso["select_ms"] / iso_steps, 4),
                             "merge_ms_per_step": round(tim_iso["merge_ms"] / iso_steps, 4),
                             "steps": iso_steps}
+    hbm = hbm_rooflines(g, hq, hkv, tim_iso, iso_steps, pk["hbm"])
 
     extra = {}
     cpu = None
     if world == 1 and not args.no_extras:
-        # dense exact attention over the same sequence on one GPU (our kernel, full causal)
         n = g["n"]
+        gen = torch.Generator(device=dev).manual_seed(4321)
+        # dense exact attention over the same sequence on one GPU (our kernel, full causal)
         qd = torch.randn((n, hq * DH), generator=gen, device=dev).to(torch.bfloat16)
         kd = torch.randn((n, hkv * DH), generator=gen, device=dev).to(torch.bfloat16)
         vd = torch.randn((n, hkv * DH), generator=gen, device=dev).to(torch.bfloat16)
@@ -569,7 +719,7 @@ def run_spava_arm(args):
             sms = e0.elapsed_time(e1) / reps
             extra["dense_torch_sdpa"] = {"tokens_per_s": n / (sms / 1e3), "ms": round(sms, 3),
                                          "tflops": round(dflops / (sms / 1e3) / 1e12, 1),
-                                         "note": "library cross-check (torch SDPA), not our code"}
+                                         "note": "library cross-check (torch SDPA / cuDNN), not our code"}
         except Exception as e:  # pragma: no cover
             extra["dense_torch_sdpa"] = {"error": str(e)[:200]}
         del qd, kd, vd
@@ -580,28 +730,17 @@ def run_spava_arm(args):
             fabf = spava.Fabric(lcf, local)
             hostf = fabf.host(0)
             outf = torch.empty_like(out)
-            self_sel = sel.clone()
             self_sel_f = torch.empty_like(sel)
-            for _ in range(args.warmup):
-                hostf.layer(q, k, v, outf, self_sel_f, stream)
-            torch.cuda.synchronize()
-            evf = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                   for _ in range(args.steps)]
-            for i in range(args.steps):
-                flush.zero_()
-                evf[i][0].record(stream)
-                hostf.layer(q, k, v, outf, self_sel_f, stream)
-                evf[i][1].record(stream)
-            torch.cuda.synchronize()
-            fms = sum(a.elapsed_time(b) for a, b in evf) / args.steps
+            hostf.set_timing(True)
+            fstep = time_layer(torch, hostf, q, k, v, outf, self_sel_f, stream, flush, args.steps, args.warmup)
+            fms = sum(fstep) / args.steps
+            hostf.set_timing(False)
             hostf.set_timing(2)
             hostf.layer(q, k, v, outf, self_sel_f, stream)
             torch.cuda.synchronize()
             ft = hostf.timing()
             hostf.set_timing(False)
-            host.layer(q, k, v, out, self_sel, stream)  # exact selection on the same inputs
-            torch.cuda.synchronize()
-            a_ex, a_f = self_sel.cpu().numpy(), self_sel_f.cpu().numpy()
+            a_ex, a_f = sel_timed.cpu().numpy(), self_sel_f.cpu().numpy()
             lp = g["l_p"]
             common = sum(len(set(a_ex[r][:lp].tolist()) & set(a_f[r][:lp].tolist())) for r in range(2))
             extra["fast_scoring"] = {
@@ -609,14 +748,14 @@ def run_spava_arm(args):
                 "score_ms_per_step_isolated": round(ft["score_ms"], 4),
                 "index_agreement": round(common / (2 * lp), 6), "indices_differing": 2 * lp - common,
                 "note": "score_mode=1: tcgen05 logits + exp2 scorer; same layer otherwise; indices "
-                        "compared with the exact (bit-faithful) scorer on the same inputs"}
+                        "compared with the exact scorer on the same inputs"}
             hostf.close()
             fabf.close()
         except Exception as e:  # pragma: no cover
             extra["fast_scoring"] = {"error": str(e)[:200]}
         # the decoder layer around the path (f2): layer_norm, [Wq|Wk|Wv], Spava attention, Wo +
         # residual, layer_norm, ReLU MLP + residual (simhost.cpp:196-207, 431-436) at
-        # Qwen2.5-VL-3B widths (d_model 2048, ffn 11008), cuBLASLt bf16 GEMMs
+        # Qwen2.5-VL-3B widths (d_model 2048, ffn 11008)
         try:
             D, FF = 2048, 11008
             gw = torch.Generator(device=dev).manual_seed(77)
@@ -645,44 +784,55 @@ def run_spava_arm(args):
                 "tokens_per_s": g["n"] / (dms / 1e3), "ms": round(dms, 3),
                 "gemm_tflop": round(gemm_fl / 1e12, 3),
                 "note": "x += Spava-attention decoder layer (layer_norm, QKV, Spava, Wo, layer_norm, "
-                        "ReLU MLP) at d_model 2048 / ffn 11008; GEMMs are cuBLASLt bf16"}
+                        "ReLU MLP) at d_model 2048 / ffn 11008"}
             del xw, w_qkv, w_o, w_1, w_2, wsd
         except Exception as e:  # pragma: no cover
             extra["decoder_layer"] = {"error": str(e)[:200]}
+        # BASELINE's sweep config (C4, 7B 256K) and the 128K scaling config (C3) at H = 1
+        if not args.no_sweep:
+            del q, k, v, out, out_timed
+            torch.cuda.empty_cache()
+            extra["sweep_h1"] = {}
+            for sname in ("C3", "C4"):
+                try:
+                    extra["sweep_h1"][sname] = sweep_line(torch, spava, sname, local, stream, flush, 3, pk)
+                except Exception as e:  # pragma: no cover
+                    extra["sweep_h1"][sname] = {"error": str(e)[:200]}
         if not args.no_cpu:
             os.sched_setaffinity(0, all_cpus)  # the CPU reference gets every host core
             threads = os.cpu_count() or 1
-            tps, layer_s, rate, desc, kind = reference_tokens_per_s(g, hq, hkv, threads, args.cpu_budget)
-            cpu = {"value": tps, "unit": "tokens/s", "cores": threads, "kind": kind, "sample": desc,
-                   "gflops_per_s": round(rate / 1e9, 2), "extrapolated_layer_s": round(layer_s, 1)}
+            r = reference_job(g, hq, hkv, 4, 1, threads, max_s=args.cpu_budget)
+            cpu = {"value": r["value"], "unit": "tokens/s", "cores": threads, "kind": r["kind"],
+                   "sample": r["sample"], "gflops_per_s": round(r["gflops_per_s"], 2),
+                   "layer_s": round(r["layer_s"], 1), "fraction_of_layer": round(r["frac"], 4)}
 
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic N(0,1) bf16 activations",
-        "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g["n"],
-                   "n_t": g["n_t"], "l_a": g["l_a"], "l_b": g["l_b"], "l_p": g["l_p"],
-                   "hosts": H, "heads": f"{hq}q/{hkv}kv", "dh": DH, "layers_per_step": 1,
-                   "parallelism": f"sp{H} (Spava zigzag virtual hosts, one per GPU)",
-                   "exchange": ("local" if world == 1 else
-                                "peer (NVLink stores from the select / merge kernels + epoch flags)"
-                                if args.fabric == "peer" else "nccl allgather"),
-                   "exchange_note": fabric_note,
-                   "l2": "flushed (256 MiB write) between timed steps, outside the events",
-                   "scoring": "exact (bit-faithful to the reference)"},
+        "config": dict(config_dict(name, cfg, g, H),
+                       exchange=("local" if world == 1 else
+                                 "peer (NVLink stores from the select / merge kernels + epoch flags)"
+                                 if fabric == "peer" else "nccl allgather"),
+                       exchange_note=fabric_note,
+                       l2="flushed (256 MiB write) between timed steps, outside the events"),
         "e2e": {"value": tokens / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "host_cpus": numa_cpus,
                 "step_ms": [round(x, 3) for x in e2e_step_ms],
+                "outputs_equal_device_path": e2e_same,
                 "copy_floor_ms": round(copy_floor_ms, 3),
                 "copy_floor_note": "the step's H2D + D2H bytes as bare pinned copies on two streams "
                                    "(no compute): the PCIe bound of e2e"},
         "roofline": roofline,
+        "hbm_roofline": hbm,
         "cpu_baseline": cpu,
         "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "clocks": clocks,
         "wall_s_timed": round(wall, 4),
         "step_ms_minmax": [round(min(step_ms), 4), round(max(step_ms), 4)],
     }
+    if ranks is not None:
+        line["ranks"] = ranks
     line.update(extra)
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -700,11 +850,16 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C1", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="default: C1 on one GPU, C3 (128K tokens) at N > 1")
     ap.add_argument("--impl", default="spava", choices=["spava", "reference"])
     ap.add_argument("--fabric", default="peer", choices=["peer", "nccl"],
                     help="N>1 exchange: NVLink peer stores + flags (default) or NCCL allgathers")
-    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds for the CPU baseline sample")
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds for the CPU baseline sample")
+    ap.add_argument("--ref-max-s", type=float, default=150.0,
+                    help="reference arm: run the whole layer when it fits this estimate, else a sample")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the C3/C4 H=1 lines (N=1)")
+    ap.add_argument("--no-self-check", action="store_true", help="N>1: skip the one-GPU comparison")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     args = ap.parse_args()

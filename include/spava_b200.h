@@ -114,8 +114,9 @@ int spava_score_block_fast(const void* q, int64_t ldq, int n_t, const void* k, i
 /* ------------------------------------------------------- select + pack
  * select_essential (approx.cpp:71-102): top-l_p by score, ties -> lower index,
  * non-finite never selected, indices ascending (+global_offset) in idx_out;
- * K/V rows gathered into k_out/v_out (ld_out; rows >= count zero-filled).
- * count_out, status_out: device int32 (status 1 = NaN score rejected).       */
+ * K/V rows gathered into k_out/v_out (ld_out; rows >= count zero-filled,
+ * idx_out entries >= count set to -1).
+ * count_out, status_out: device int32 (status |= 1: NaN score rejected).     */
 int spava_select_pack(const float* scores, int l_b, int l_p, int global_offset, const void* k,
                       const void* v, int64_t ld, int width, int32_t* idx_out, void* k_out,
                       void* v_out, int64_t ld_out, int32_t* count_out, int32_t* status_out,
@@ -147,7 +148,7 @@ int spava_attention(const void* q, int64_t ldq, int nq, const spava_segment* seg
  * mha_merge (attention.cpp:180-197) over nparts partials in host order.
  * outs[p]: device f32 [rows x ld_part], lses[p]: device f32 [rows x hq]
  * (host arrays of device pointers).  dst: bf16 or f32 [rows x ld_dst];
- * dst_lse (nullable) receives the merged lse.  status: device int32, set to 1
+ * dst_lse (nullable) receives the merged lse.  status: device int32, |= 4
  * if a row is invalid in every part (the reference throws).                  */
 int spava_mha_merge(int nparts, const float* const* outs, const float* const* lses, int rows,
                     int64_t ld_part, int hq, int dh, void* dst, int64_t ld_dst, int dst_f32,
@@ -294,8 +295,11 @@ int spava_sim_layer(spava_fabric* fab, spava_host* const* hosts, const void* con
 int spava_sim_layer_timed(spava_fabric* fab, spava_host* const* hosts, const void* const* q,
                           const void* const* k, const void* const* v, void* const* out,
                           int32_t* const* sel, void* stream, float* ms_per_host);
-/* Device-side status word of the last layer (0 ok; non-zero: NaN score or a
- * merge row invalid everywhere).  Synchronises the given stream.            */
+/* Device-side status word of the last layer (0 ok; bit 0: NaN score; bit 1: a
+ * passing source selected fewer than l_p keys (non-finite scores) -- its fixed
+ * l_p-row exchange slot would be attended with zero rows where the reference drops
+ * them (approx.cpp:83-90); bit 2: a merged query row invalid in every part).
+ * Synchronises the given stream.                                      */
 int spava_host_status(spava_host* host, void* stream, int32_t* status_out);
 
 /* DelayInjection analogue (simhost.hpp:51-55): spin `ns` nanoseconds on a stream before

@@ -481,8 +481,10 @@ int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record,
           ps.cnt[ps.n] = F.at_peer(q, cnt_out);
           ++ps.n;
         }
+    // a block below the last virtual block is some later block's passing source: its slot
+    // is read as exactly l_p rows, so a short selection is reported (status bit 2)
     jobs[r] = SelectPackJob{H->scores[r], p.l_a + vs[r] * p.l_b, row_ptr(b.k, krow, dk), row_ptr(b.v, krow, dk),
-                            idx_out, k_out, v_out, cnt_out, &peers[r]};
+                            idx_out, k_out, v_out, cnt_out, &peers[r], vs[r] < p.virtual_hosts - 1};
   }
   auto finish = [&](int r) -> int {  // after round r's select + pack
     if (F.peer) ST_TRY(peer_signal(H->fab, st, r));

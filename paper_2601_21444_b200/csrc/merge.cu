@@ -51,7 +51,7 @@ __global__ void merge_kernel(const __grid_constant__ MergeParams p) {
     if (lane == 0) {
       ok_sh = ok;
       lse_sh = ok ? __double2float_rn(mx + log(denom)) : -INFINITY;
-      if (!ok && p.status) atomicExch(p.status, 1);
+      if (!ok && p.status) atomicOr(p.status, 4);
     }
   }
   __syncthreads();

@@ -91,6 +91,7 @@ struct SelJob {
   uint4* k_out;
   uint4* v_out;
   PeerSlots peers;
+  int require_full;  // a passing source: fewer than l_p keys is reported (status bit 2)
 };
 struct SelJobs {
   SelJob j[2];
@@ -133,10 +134,14 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const __grid_consta
     // NaN is invalid input; +inf sorts first and stops the selection at once
     bool nan = false;
     for (int j = 0; j < l_b && !nan; ++j) nan = isnan(scores[j]);
-    if (nan) atomicExch(status, 1);
+    if (nan) atomicOr(status, 1);
   }
   if (k == 0) {
-    if (tid == 0) *count = 0;
+    for (int r = tid; r < l_p; r += kSelThreads) idx[r] = -1;
+    if (tid == 0) {
+      *count = 0;
+      if (jb.require_full && l_p > 0 && status) atomicOr(status, 2);
+    }
     return;
   }
   // ---- 2. radix select: digits [31:21], [20:10], [9:0]
@@ -223,7 +228,13 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const __grid_consta
     eq_base += eq_tot;
     out_base += sel_tot;
   }
-  if (tid == 0) *count = out_base;
+  for (int r = out_base + tid; r < l_p; r += kSelThreads) idx[r] = -1;  // defined tail
+  if (tid == 0) {
+    *count = out_base;
+    // the exchange slot is fixed-size (l_p rows): a short selection would be attended as
+    // zero rows where the reference drops them (approx.cpp:83-90), so it is an error here
+    if (jb.require_full && out_base < l_p && status) atomicOr(status, 2);
+  }
 }
 
 // warp per selected row; rows >= count are zero-filled so the slot is well defined.
@@ -284,6 +295,7 @@ cudaError_t launch_select_pack_n(const SelectPackJob* jobs, int n, int l_b, int 
     j.k_out = static_cast<uint4*>(s.k_out);
     j.v_out = static_cast<uint4*>(s.v_out);
     if (s.peers) j.peers = *s.peers;
+    j.require_full = s.require_full;
     gather = gather && s.k_out && s.v_out;
     if (!(l_p > 0 && s.k_out && s.v_out) && j.peers.n > 0)
       return cudaErrorInvalidValue;  // a peer slot is only published through the gather

@@ -123,6 +123,7 @@ struct SelectPackJob {
   void* v_out;
   int32_t* count;
   const PeerSlots* peers;  // nullable
+  int require_full = 0;    // passing source: count < l_p sets status bit 2
 };
 // select + pack of 1 or 2 blocks (same l_b / l_p / widths) in one select and one gather launch
 cudaError_t launch_select_pack_n(const SelectPackJob* jobs, int n, int l_b, int l_p, long long ld, int width,

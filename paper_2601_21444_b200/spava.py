@@ -533,8 +533,31 @@ class Host:
         self.plan = Plan()
         lib().spava_host_plan(self._p, C.byref(self.plan))
 
+    def check_buffers(self, q, k, v, out, sel=None):
+        """The C ABI takes raw device pointers sized from the plan (rows = l_a + 2 l_b + n_t,
+        widths hq*dh / hkv*dh bf16, sel >= 2*l_p int32): reject anything else here so a
+        wrong-shaped, fp32 or strided tensor cannot read or write out of bounds."""
+        import torch
+
+        c = self.fabric.cfg
+        dev = torch.device("cuda", self.fabric.device)
+        for t, w, name in ((q, c.hq * c.dh, "q"), (k, c.hkv * c.dh, "k"), (v, c.hkv * c.dh, "v"),
+                           (out, c.hq * c.dh, "out")):
+            _require(t, torch.bfloat16, name)
+            if tuple(t.shape) != (self.rows, w) or not t.is_contiguous():
+                raise SpavaError(EINVAL, f"{name}: expected a contiguous [{self.rows}, {w}] tensor, "
+                                         f"got {tuple(t.shape)} strides {t.stride()}")
+            if t.device != dev:
+                raise SpavaError(EINVAL, f"{name}: on {t.device}, the fabric is on {dev}")
+        if sel is not None:
+            if sel.device != dev or sel.dtype != torch.int32 or not sel.is_contiguous() \
+                    or sel.numel() < 2 * max(self.plan.l_p, 1):
+                raise SpavaError(EINVAL, f"sel: expected a contiguous int32 tensor of >= "
+                                         f"{2 * max(self.plan.l_p, 1)} entries on {dev}")
+
     def layer(self, q, k, v, out, sel=None, stream=None):
         """One layer of this host (NCCL fabric, or a local fabric with H == 1)."""
+        self.check_buffers(q, k, v, out, sel)
         _check(lib().spava_host_layer(self._p, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(sel),
                                       _stream(stream)))
 
@@ -554,6 +577,12 @@ class Host:
         for t in (q_h, k_h, v_h, out_h):
             if t.is_cuda or not t.is_contiguous():
                 raise ValueError("layer_hostbuf: host tensors must be contiguous CPU tensors")
+        self.check_buffers(q_d, k_d, v_d, out_d, sel_d)
+        for th, td in ((q_h, q_d), (k_h, k_d), (v_h, v_d), (out_h, out_d)):
+            if th.shape != td.shape or th.dtype != td.dtype:
+                raise ValueError("layer_hostbuf: host and device buffers differ in shape or dtype")
+        if sel_h is not None and (sel_h.dtype != sel_d.dtype or sel_h.numel() < sel_d.numel()):
+            raise ValueError("layer_hostbuf: sel_h must match sel_d")
         _check(lib().spava_host_layer_hostbuf(
             self._p, C.c_void_p(q_h.data_ptr()), C.c_void_p(k_h.data_ptr()), C.c_void_p(v_h.data_ptr()),
             C.c_void_p(out_h.data_ptr()), C.c_void_p(sel_h.data_ptr()) if sel_h is not None else None,
@@ -581,6 +610,7 @@ class Host:
 
     def capture_layer(self, q, k, v, out, sel=None, stream=None):
         """Capture one layer on these buffers as a CUDA graph (replay_layer launches it)."""
+        self.check_buffers(q, k, v, out, sel)
         _check(lib().spava_host_capture_layer(self._p, _ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(sel),
                                               _stream(stream)))
 
@@ -695,6 +725,8 @@ class Fabric:
 
     def sim_layer(self, hosts, qs, ks, vs, outs, sels=None, stream=None):
         n = len(hosts)
+        for i, h in enumerate(hosts):
+            h.check_buffers(qs[i], ks[i], vs[i], outs[i], sels[i] if sels is not None else None)
         arr = lambda ts: (C.c_void_p * n)(*[t.data_ptr() if t is not None else None for t in ts])
         _check(lib().spava_sim_layer(self._p, (C.c_void_p * n)(*[h._p.value for h in hosts]),
                                      arr(qs), arr(ks), arr(vs), arr(outs),
@@ -703,6 +735,8 @@ class Fabric:
     def sim_layer_timed(self, hosts, qs, ks, vs, outs, sels=None, stream=None):
         """sim_layer with each host's phases timed alone on the GPU: list of ms per host."""
         n = len(hosts)
+        for i, h in enumerate(hosts):
+            h.check_buffers(qs[i], ks[i], vs[i], outs[i], sels[i] if sels is not None else None)
         arr = lambda ts: (C.c_void_p * n)(*[t.data_ptr() if t is not None else None for t in ts])
         ms = (C.c_float * n)()
         _check(lib().spava_sim_layer_timed(self._p, (C.c_void_p * n)(*[h._p.value for h in hosts]),

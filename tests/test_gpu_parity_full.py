@@ -1,0 +1,183 @@
+"""Parity of the BENCHED configuration, end to end, against the unmodified reference.
+
+C1 (BASELINE.json configs[1]: 32K tokens, Qwen2.5-VL-3B heads 16q/2kv, d=128, n_t=128,
+l_a=n/64, l_p=n/128=256 of l_b=16064, H=1, exact scorer) runs through the product C ABI
+(spava_host_layer) and is checked against oracle/_ref -- the reference's own
+score_block / select_essential / mha_lse / mha_merge (oracle/layer_ref.py):
+
+* every passing index of both virtual blocks bit-exact (block hi's passing set is block
+  lo's selection, so a wrong index would also show in hi's rows);
+* >= 1024 output rows (anchor, block lo, block hi incl. their first/last rows, and every
+  merged query row) within the stated bf16 tolerance (tests/util.py: max-abs 2.5e-2,
+  rel-L2 6e-3), each row computed by the reference as an exact row-slice sub-problem;
+* the scorer's own report: non-identical scores vs the reference and the smallest
+  relative top-k boundary gap (how close the selection came to a flip).
+
+C3 (131072 tokens, l_p=1024) on 8 simulated hosts does the same for all 16 virtual
+blocks (zigzag pairing, passing sets of up to 15 sources).  The report of every test is
+printed (pytest -s) and written to gpurun_out/parity_report.json when that dir exists.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import layer_ref as LR
+from tests.util import ATOL_BF16_OUT, RTOL_L2_BF16, ROOT, max_abs, rel_l2, ulp_diff
+
+pytestmark = pytest.mark.gpu
+THREADS = os.cpu_count() or 1
+
+
+def _report(name, d):
+    print(f"\n[parity] {name}: {json.dumps(d)}")
+    out = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(out):
+        p = os.path.join(out, "parity_report.json")
+        try:
+            with open(p) as f:
+                allr = json.load(f)
+        except (OSError, ValueError):
+            allr = {}
+        allr[name] = d
+        with open(p, "w") as f:
+            json.dump(allr, f, indent=1)
+
+
+def _sample(rng, n, k, edge=16):
+    """k rows of [0, n): the first and last `edge` rows plus uniform picks."""
+    fixed = set(range(min(edge, n))) | set(range(max(0, n - edge), n))
+    rest = np.setdiff1d(np.arange(n), np.array(sorted(fixed)))
+    pick = rng.choice(rest, size=max(0, min(len(rest), k - len(fixed))), replace=False)
+    return sorted(fixed | set(int(x) for x in pick))
+
+
+def _gap(scores, l_p):
+    s = np.sort(scores[np.isfinite(scores)])[::-1]
+    if l_p <= 0 or l_p >= len(s):
+        return None
+    return float((s[l_p - 1] - s[l_p]) / abs(s[l_p - 1]))
+
+
+def _run_host_layer(cuda, g, hq, hkv, Q, K, V, score_mode=0):
+    import torch
+
+    from paper_2601_21444_b200 import spava
+
+    H = g["hosts"]
+    lc = spava.LayerConfig.make(g["n_v"], g["n_t"], H, g["l_a"], g["l_p"], hq, hkv, score_mode=score_mode)
+    fab = spava.Fabric(lc, 0)
+    hosts, outs, sels, ins = [], [], [], []
+    for h in range(H):
+        hosts.append(fab.host(h))
+        rows = LR.host_rows(g, h)
+        ins.append([torch.from_numpy(X[rows]).to(cuda).to(torch.bfloat16) for X in (Q, K, V)])
+        outs.append(torch.empty((hosts[-1].rows, hq * 128), dtype=torch.bfloat16, device=cuda))
+        sels.append(torch.full((2, max(g["l_p"], 1)), -7, dtype=torch.int32, device=cuda))
+    if H == 1:
+        hosts[0].layer(*ins[0], outs[0], sels[0])
+    else:
+        fab.sim_layer(hosts, [x[0] for x in ins], [x[1] for x in ins], [x[2] for x in ins], outs, sels)
+    torch.cuda.synchronize()
+    assert all(h.status() == 0 for h in hosts)
+    res = dict(out=[o.float().cpu().numpy() for o in outs], sel=[s.cpu().numpy() for s in sels], ins=ins)
+    for h in hosts:
+        h.close()
+    fab.close()
+    return res
+
+
+def _check_layer(name, cuda, g, hq, hkv, n_anchor, n_block, seed, score_mode=0, impl="ref",
+                 gpu_scores=True):
+    from paper_2601_21444_b200 import spava
+
+    Q, K, V = LR.layer_inputs(g, hq, hkv, seed=seed)
+    gpu = _run_host_layer(cuda, g, hq, hkv, Q, K, V, score_mode)
+    H, l_a, l_b, l_p, n_t = g["hosts"], g["l_a"], g["l_b"], g["l_p"], g["n_t"]
+    ref = LR.LayerRef(Q, K, V, g, hq, hkv, impl=impl)
+    # ---- scores + selection of every virtual block
+    t_score, _, _ = LR.run_items(ref.run_item, ref.score_items(), THREADS)
+    ref.finish_scores()
+    rep = dict(config=dict((k, g[k]) for k in ("n_v", "n_t", "hosts", "l_a", "l_b", "l_p", "pad")),
+               impl=ref.impl, threads=THREADS, ref_score_s=round(t_score, 2), blocks={})
+    sel_ok = True
+    for h in range(H):
+        for r, v in enumerate(LR.pair(g, h)):
+            want = ref.sel[v]
+            got = gpu["sel"][h][r][:len(want)]
+            same = bool(np.array_equal(got, want)) and len(want) == min(l_p, LR.valid_rows(g, v))
+            sel_ok &= same
+            b = dict(indices_equal=same, count=int(len(want)), min_topk_gap_rel=_gap(ref.scores[v], l_p))
+            if gpu_scores:  # the scorer on the same bf16 rows (the layer's own kernels)
+                qh = gpu["ins"][h][0][l_a + 2 * l_b:]
+                kb = gpu["ins"][h][1][l_a + r * l_b:l_a + (r + 1) * l_b]
+                nv = LR.valid_rows(g, v)
+                got_s = spava.score_block(qh, kb, hq, hkv, 128, n_valid=nv).cpu().numpy()
+                rs = ref.scores[v]
+                fin = np.isfinite(rs)
+                b["scores_non_identical"] = int(np.sum(got_s[fin] != rs[fin]))
+                b["scores_max_ulp"] = ulp_diff(got_s[fin], rs[fin])
+            rep["blocks"][str(v)] = b
+    # ---- sampled output rows
+    rng = np.random.default_rng(seed + 1)
+    rows_anchor = _sample(rng, l_a, n_anchor)
+    rows_block = {v: _sample(rng, LR.valid_rows(g, v), n_block) for v in range(2 * H)}
+    rows_query = list(range(n_t))
+    items = ref.attention_items(rows_anchor, rows_block, rows_query)
+    t_attn, fl, _ = LR.run_items(ref.run_item, items, THREADS)
+    rep["ref_attention_s"] = round(t_attn, 2)
+    rep["ref_attention_gflop"] = round(fl / 1e9, 1)
+    worst = dict(max_abs=0.0, rel_l2=0.0)
+    n_rows = 0
+
+    def cmp(tag, got, want):
+        nonlocal n_rows
+        e, r = max_abs(got, want), rel_l2(got, want)
+        rep[tag] = dict(rows=len(got), max_abs=round(e, 5), rel_l2=round(r, 6))
+        worst["max_abs"] = max(worst["max_abs"], e)
+        worst["rel_l2"] = max(worst["rel_l2"], r)
+        n_rows += len(got)
+        return e <= ATOL_BF16_OUT and r <= RTOL_L2_BF16
+
+    ok = True
+    want_a, _ = ref.rows("anchor", 0, rows_anchor)
+    for h in range(H):  # every host computes the anchor (redundant, simhost.cpp:308-311)
+        ok &= cmp(f"anchor_h{h}", gpu["out"][h][rows_anchor], want_a)
+    for h in range(H):
+        for r, v in enumerate(LR.pair(g, h)):
+            want_b, _ = ref.rows("block", v, rows_block[v])
+            got_b = gpu["out"][h][l_a + r * l_b + np.array(rows_block[v])]
+            ok &= cmp(f"block_v{v}", got_b, want_b)
+    want_q = ref.query_rows(rows_query)
+    for h in range(H):
+        ok &= cmp(f"query_h{h}", gpu["out"][h][l_a + 2 * l_b + np.array(rows_query)], want_q)
+    rep["rows_checked"] = n_rows
+    rep["worst"] = dict(max_abs=round(worst["max_abs"], 5), rel_l2=round(worst["rel_l2"], 6))
+    rep["tolerance"] = dict(max_abs=ATOL_BF16_OUT, rel_l2=RTOL_L2_BF16)
+    _report(name, rep)
+    assert sel_ok, rep["blocks"]
+    assert n_rows >= 1024
+    assert ok, rep
+
+
+def test_c1_benched_layer_vs_reference(cuda):
+    """The bench's C1 layer (exact scorer, compression on) against oracle/_ref."""
+    g = LR.geometry(32768 - 128, 128, 1, 512, 256)
+    assert (g["l_b"], g["l_p"]) == (16064, 256)
+    _check_layer("c1_h1_exact", cuda, g, 16, 2, n_anchor=128, n_block=448, seed=1234)
+
+
+def test_c1_no_compression_vs_reference(cuda):
+    """l_p = l_b (acceptance.cpp:60-127 'C1'): the layer is dense causal attention."""
+    g = LR.geometry(32768 - 128, 128, 1, 512, 16064)
+    _check_layer("c1_h1_no_compression", cuda, g, 16, 2, n_anchor=64, n_block=480, seed=5,
+                 gpu_scores=False)
+
+
+def test_c3_sim8_layer_vs_reference(cuda):
+    """C3 (131072 tokens, l_p=1024) on 8 simulated hosts: all 16 blocks' passing indices
+    and sampled rows of every block, host and the merged query."""
+    g = LR.geometry(131072 - 128, 128, 8, 2048, 1024)
+    assert g["l_b"] == 8056
+    _check_layer("c3_h8_exact", cuda, g, 16, 2, n_anchor=64, n_block=64, seed=77)
