@@ -139,8 +139,22 @@ __device__ __forceinline__ void cursor_next(const AttnProb& p, int imax, Cursor&
   }
 }
 
-template <int kEmu, int KS, bool kProf = false, bool kPipe = false, bool kSpec = true>
-__global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_constant__ AttnParams P) {
+// kPParts: P of a tile is committed to TMEM in kPParts key ranges, each signalled on its own
+// mbarrier, and the MMA warp issues the PV K-steps of a range as soon as it is in, so the
+// tensor pipe overlaps the tail of the softmax of the same tile (the per-tile loop
+// softmax -> PV -> QK shortens by (1 - 1/kPParts) of a PV).
+// kRegs > 0: 384 threads (3 warpgroups); the producer/MMA warpgroup gives registers back
+// (setmaxnreg.dec to 56) and the two softmax warpgroups take kRegs each (setmaxnreg.inc), so
+// a softmax thread holds its S row, packed P and a deeper software pipeline without spills.
+// kSeq: the exp phases of the two softmax warpgroups strictly alternate (named barriers 1/2),
+// so each runs with the SM's MUFU to itself and the two stay in anti-phase with the MMAs.
+// kLd2: S is read from TMEM in two halves, the max of the first overlapping the second load.
+template <int kEmu, int KS, bool kProf = false, bool kPipe = false, bool kSpec = true, int kPParts = 1,
+          int kRegs = 0, bool kSeq = false, bool kLd2 = false>
+__global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ AttnParams P) {
+  static_assert(kPParts == 1 || (kPipe && !kSpec && (kPParts == 2 || kPParts == 4)),
+                "split P needs the max-first pipelined softmax");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -152,8 +166,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   uint64_t* v_full = k_empty + kMaxKStages;   // [kVStages]
   uint64_t* v_empty = v_full + kVStages;      // [kVStages] freed once both PV completed
   uint64_t* s_full = v_empty + kVStages;      // [2] S_t ready in TMEM
-  uint64_t* p_full = s_full + 2;              // [2] P_t written (and O_t corrected)
-  uint64_t* o_full = p_full + 2;              // [2] PV_t complete
+  uint64_t* p_full = s_full + 2;              // [2][4] P_t key range written (O_t corrected)
+  uint64_t* o_full = p_full + 8;              // [2] PV_t complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
 
   const int warp = warp_id();
@@ -201,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(s_full + t, 1);
-      mbar_init(p_full + t, 128);
+      for (int pp = 0; pp < kPParts; ++pp) mbar_init(p_full + 4 * t + pp, 128);
       mbar_init(o_full + t, 1);
     }
     fence_barrier_init();
@@ -216,7 +230,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-
+  // Role branches: the register budget changes at the top of each warpgroup's branch and the
+  // branches only rejoin at the teardown, so ptxas allocates each role within its budget.
+  if (warp >= kProducerWarp) {
+  if constexpr (kRegs > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
   if (warp == kProducerWarp) {
     // ======================================================== TMA producer
     if (elect_one()) {
@@ -262,11 +279,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
           mma_ss(d, a, b, idesc_qk, kk > 0 ? 1u : 0u);
         }
       };
-      auto issue_pv = [&](int qt, int stage, bool acc) {
+      // PV K-steps [kk0, kk0 + n) (16 keys each; P of K-step kk at S columns 8kk..8kk+7)
+      auto issue_pv = [&](int qt, int stage, bool acc, int kk0, int n) {
         const uint32_t d = tmem + 256 + qt * 128;
         const uint32_t a = tmem + qt * 128;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
+        for (int k = 0; k < n; ++k) {
+          const int kk = kk0 + k;
           const uint64_t b = sdesc_sw128(sv + stage * kTileBytes + kk * 2048, kBoxBytes, 1024);
           mma_ts(d, a + kk * 8, b, idesc_pv, (acc || kk > 0) ? 1u : 0u);
         }
@@ -315,11 +334,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         tc_fence_after();
         for (int qt = 0; qt < 2; ++qt) {
           if (mode[qt] != kSkip) {
-            const long long tw = PROF_NOW();
-            mbar_wait(p_full + qt, p_cnt[qt] & 1);
-            if (kProf) pr[2] += PROF_NOW() - tw;
-            tc_fence_after();
-            issue_pv(qt, vs, o_acc[qt]);
+#pragma unroll
+            for (int pp = 0; pp < kPParts; ++pp) {
+              const long long tw = PROF_NOW();
+              mbar_wait(p_full + 4 * qt + pp, p_cnt[qt] & 1);
+              if (kProf) pr[2] += PROF_NOW() - tw;
+              tc_fence_after();
+              issue_pv(qt, vs, o_acc[qt], pp * (8 / kPParts), 8 / kPParts);
+            }
             o_acc[qt] = true;
             ++p_cnt[qt];
             tc_commit(o_full + qt);
@@ -337,7 +359,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
       }
       if (kProf) pr[3] += PROF_NOW() - tm0;
     }
-  } else if (warp < kProducerWarp) {
+  }
+  } else {
+    if constexpr (kRegs > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
     // ======================================================== softmax warpgroups
     const int qt = warp >> 2;
     const int quad = warp & 3;
@@ -350,6 +374,18 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
     float m_ref = -INFINITY;
     float l = 0.f;
     uint32_t cnt = 0;
+    // kSeq: tiles processed by this and by the other warpgroup (skipped tiles are the causal
+    // tail, so the k-th processed tiles of both line up); tokens only for k < n_min.
+    int n_ot = 0, n_min = 0;
+    if constexpr (kSeq) {
+      int n_me = 0;
+      Cursor c2 = cursor_at(prob, imax, t_begin);
+      for (int it = 0; it < ntiles; ++it, cursor_next(prob, imax, c2)) {
+        n_me += tile_mode(prob.seg[c2.seg], c2.kt, TILE_R0(qt), nq) != kSkip;
+        n_ot += tile_mode(prob.seg[c2.seg], c2.kt, TILE_R0(qt ^ 1), nq) != kSkip;
+      }
+      n_min = min(n_me, n_ot);
+    }
     Cursor cur = cursor_at(prob, imax, t_begin);
     for (int it = 0; it < ntiles; ++it, cursor_next(prob, imax, cur)) {
       const AttnSeg sg = prob.seg[cur.seg];
@@ -426,6 +462,36 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         for (int c = 0; c < 4; ++c) tmem_ld32(tS + 32 * c, sr[c]);
         tmem_wait_ld();
       };
+      auto mask_chunk = [&](int c) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (c * 32 + j >= lim) sr[c][j] = __float_as_uint(-INFINITY);
+      };
+      auto rescale_o = [&](float a) {
+        mbar_wait(o_full + qt, (cnt - 1) & 1);  // PV_{cnt-1} has landed in O
+        tc_fence_after();
+        if constexpr (kPParts > 1) {  // the S row is still live: 8 columns at a time
+#pragma unroll 1
+          for (int c = 0; c < 16; ++c) {
+            uint32_t o[8];
+            tmem_ld8(tO + 8 * c, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * a);
+            tmem_st8(tO + 8 * c, o);
+          }
+          return;
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          tmem_ld32(tO + 32 * c, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * a);
+          tmem_st32(tO + 32 * c, o);
+        }
+      };
       float mxp[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
@@ -433,7 +499,31 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 #pragma unroll
       for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
       bool done = false;
-      load_s();
+      if constexpr (kLd2) {
+        static_assert(!kSpec, "kLd2 is a max-first path");
+#pragma unroll
+        for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
+        tmem_ld32(tS, sr[0]);
+        tmem_ld32(tS + 32, sr[1]);
+        tmem_wait_ld();
+        tmem_ld32(tS + 64, sr[2]);
+        tmem_ld32(tS + 96, sr[3]);
+        if (mode == kPart) {
+          mask_chunk(0);
+          mask_chunk(1);
+        }
+        chunk_max(0, mxp);
+        chunk_max(1, mxp);
+        tmem_wait_ld();
+        if (mode == kPart) {
+          mask_chunk(2);
+          mask_chunk(3);
+        }
+        chunk_max(2, mxp);
+        chunk_max(3, mxp);
+      } else {
+        load_s();
+      }
       if (kProf) pr[9] += PROF_NOW() - tw1;
       if (kSpec && mode == kFull && m_ref != -INFINITY) {
         // (kSpec only -- measured 1.5 % slower than max-first at C1, so off in production)
@@ -467,20 +557,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
           for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
           load_s();
         }
-      } else if (mode == kPart) {
+      } else if (!kLd2 && mode == kPart) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c * 32 + j >= lim) sr[c][j] = __float_as_uint(-INFINITY);
+        for (int c = 0; c < 4; ++c) mask_chunk(c);
       }
       if (kProf) pr[8] += PROF_NOW() - tw1;
       if (!done) {
         // max first, lazy rescale (keep a stale max while p <= 2^8), then exps
+        if constexpr (!kLd2) {
 #pragma unroll
-        for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
+          for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) chunk_max(c, mxp);
+          for (int c = 0; c < 4; ++c) chunk_max(c, mxp);
+        }
         const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
                                fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
         const float m_new = fmaxf(m_ref, mx * sl2);
@@ -491,7 +580,40 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
         }
         const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
         const float2 negm = make_float2(-m_use, -m_use);
-        if constexpr (kPipe) {
+        if constexpr (kPParts > 1) {
+          // O is corrected before any P range is released (PV_{cnt-1} already landed: it
+          // was issued before the QK whose commit signalled s_full), then each key range
+          // of P is stored and signalled as soon as it is packed.
+          if (rescale && cnt > 0) rescale_o(alpha);
+          constexpr int kCpp = 4 / kPParts;  // 32-key chunks per range
+          const int k = static_cast<int>(cnt);
+          if constexpr (kSeq) {  // wait for the other warpgroup's exp phase of the turn before
+            if (qt == 0 ? (k >= 1 && k - 1 < n_min) : (k < n_min)) named_bar_sync(qt == 0 ? 2 : 1, 256);
+          }
+          const long long te0 = PROF_NOW();
+          chunk_exp_ip(0, negm, mode == kFull);
+#pragma unroll
+          for (int c = 1; c < 4; ++c) {
+            chunk_exp_ip(c, negm, mode == kFull);
+            if (kSeq && c == 3) {  // exps done: hand the MUFUs to the other warpgroup
+              // warpgroup 0's turn k is awaited by warpgroup 1 iff k < n_min; warpgroup 1's
+              // turn k by warpgroup 0 iff k < n_min and warpgroup 0 has a turn k + 1
+              if (qt == 0 ? (k < n_min) : (k < n_min && k + 1 < n_ot)) named_bar_arrive(qt == 0 ? 1 : 2, 256);
+            }
+            chunk_pack(c - 1, sacc);
+            tmem_st16(tS + 16 * (c - 1), pk[c - 1]);
+            if (c % kCpp == 0) {
+              const long long ts0 = PROF_NOW();
+              tmem_wait_st();
+              tc_fence_before();
+              mbar_arrive(p_full + 4 * qt + c / kCpp - 1);
+              if (kProf) pr[11] += PROF_NOW() - ts0;
+            }
+          }
+          chunk_pack(3, sacc);
+          tmem_st16(tS + 48, pk[3]);
+          if (kProf) pr[10] += PROF_NOW() - te0;
+        } else if constexpr (kPipe) {
           chunk_exp_ip(0, negm, mode == kFull);
 #pragma unroll
           for (int c = 1; c < 4; ++c) {
@@ -504,27 +626,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
           for (int c = 0; c < 4; ++c) chunk_exp(c, negm, mode == kFull, sacc);
         }
       }
+      if constexpr (kPParts == 1) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_st16(tS + 16 * c, pk[c]);
+        for (int c = 0; c < 4; ++c) tmem_st16(tS + 16 * c, pk[c]);
+      }
       sum2 = __fadd2_rn(__fadd2_rn(sacc[0], sacc[1]), __fadd2_rn(sacc[2], sacc[3]));
       const long long tp3 = PROF_NOW();
       l = l * alpha + (sum2.x + sum2.y);
-      if (rescale && cnt > 0) {
-        mbar_wait(o_full + qt, (cnt - 1) & 1);  // PV_{cnt-1} has landed in O
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t o[32];
-          tmem_ld32(tO + 32 * c, o);
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-          tmem_st32(tO + 32 * c, o);
-        }
-      }
+      if (kPParts == 1 && rescale && cnt > 0) rescale_o(alpha);
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(p_full + qt);
+      mbar_arrive(p_full + 4 * qt + kPParts - 1);
       if (kProf) {
         pr[12] += PROF_NOW() - tp3;
         pr[5] += PROF_NOW() - tw1;
@@ -594,1556 +706,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_fwd_kernel(const __grid_cons
 #undef TILE_HEAD
 }
 
-// ============================================================================ variant family 4
-// Ping-pong family with the score tile split across time: P is stored in the UPPER half of
-// the S columns (64..127) and QK(j+1) is issued as two N=64 halves.  Half A (keys 0-63 ->
-// S columns 0-63) is issued as soon as the softmax has pulled S(j) into registers (after
-// its row max), i.e. while tile j's exps still run; P(j) is committed in two halves so
-// PV(j) starts on keys 0-63 while the softmax is still on keys 64-127; half B of QK(j+1)
-// (columns 64-127) follows PV(j) in the in-order tensor pipe.  The softmax of tile j+1
-// then waits only for PV(j)_B + QK(j+1)_B after its last commit instead of a full PV+QK.
-// The MMA warp is a small scheduler polling both Q tiles' barriers (no head-of-line
-// blocking between the two softmax warpgroups).
-template <int kEmu>
-__global__ void __launch_bounds__(kThreads, 1) attn_fwd4_kernel(const __grid_constant__ AttnParams P) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
-  using SL = Smem<2>;
-  constexpr int KS = 2;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SL::bar);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;        // [2]
-  uint64_t* k_empty = k_full + 2;     // [2]
-  uint64_t* v_full = k_empty + 2;     // [2]
-  uint64_t* v_empty = v_full + 2;     // [2]
-  uint64_t* sA = v_empty + 2;         // [2 Q tiles] QK half A (S cols 0-63) landed
-  uint64_t* sB = sA + 2;              // [2] QK half B (S cols 64-127) landed
-  uint64_t* sfree = sB + 2;           // [2] softmax holds S(j) in registers (128 arrivals)
-  uint64_t* pA = sfree + 2;           // [2] P keys 0-63 stored (and O corrected)
-  uint64_t* pB = pA + 2;              // [2] P keys 64-127 stored
-  uint64_t* o_full = pB + 2;          // [2] PV half B of the tile complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
-
-  const int warp = warp_id();
-  const int lane = lane_id();
-
-  int pi = 0;
-  while (pi + 1 < P.nprob && static_cast<int>(blockIdx.x) >= P.prob[pi + 1].work_begin) ++pi;
-  const AttnProb& prob = P.prob[pi];
-  int local = static_cast<int>(blockIdx.x) - prob.work_begin;
-  const int split = local % prob.splits;
-  local /= prob.splits;
-  const int pair = prob.head_pair;
-  const int nheads = pair ? P.hq / 2 : P.hq;
-  const int head = pair ? 2 * (local % nheads) : local % nheads;
-  local /= nheads;
-  const int unit = prob.units - 1 - local;
-  const int i0 = pair ? 0 : unit * (kTilesPerCta * kBlockM);
-  const int nq = prob.nq;
-  const int imax = min(i0 + (pair ? kBlockM : kTilesPerCta * kBlockM), nq);
-  const int hk = head / (P.hq / P.hkv);
-#define TILE_R0(t) (pair ? 0 : i0 + (t) * kBlockM)
-#define TILE_HEAD(t) (head + pair * (t))
-
-  int T = 0;
-  for (int s = 0; s < prob.nseg; ++s) T += seg_tiles(prob.seg[s], imax);
-  const int t_begin = static_cast<int>(static_cast<long long>(T) * split / prob.splits);
-  const int t_end = static_cast<int>(static_cast<long long>(T) * (split + 1) / prob.splits);
-  const int ntiles = t_end - t_begin;
-  const CUtensorMap* tm = P.tmap[pi];
-  // Q tile t processes a prefix of the KV tiles (causal skips only trail the own segment)
-  int nt[2] = {0, 0};
-  {
-    Cursor c = cursor_at(prob, imax, t_begin);
-    for (int it = 0; it < ntiles; ++it, cursor_next(prob, imax, c))
-      for (int qt = 0; qt < 2; ++qt)
-        if (tile_mode(prob.seg[c.seg], c.kt, TILE_R0(qt), nq) != kSkip) nt[qt] = it + 1;
-  }
-
-  if (warp == kProducerWarp && elect_one()) {
-    mbar_init(q_full, 1);
-    for (int s = 0; s < KS; ++s) {
-      mbar_init(k_full + s, 1);
-      mbar_init(k_empty + s, 1);
-      mbar_init(v_full + s, 1);
-      mbar_init(v_empty + s, 1);
-    }
-    for (int t = 0; t < 2; ++t) {
-      mbar_init(sA + t, 1);
-      mbar_init(sB + t, 1);
-      mbar_init(sfree + t, 128);
-      mbar_init(pA + t, 128);
-      mbar_init(pB + t, 128);
-      mbar_init(o_full + t, 1);
-    }
-    fence_barrier_init();
-    tma_prefetch_desc(&tm[0]);
-    for (int s = 0; s < prob.nseg; ++s) {
-      tma_prefetch_desc(&tm[1 + 2 * s]);
-      tma_prefetch_desc(&tm[2 + 2 * s]);
-    }
-  }
-  if (warp == kMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == kProducerWarp) {
-    // ======================================================== TMA producer (as family 0)
-    if (elect_one()) {
-      const bool has1 = TILE_R0(1) < nq;
-      mbar_expect_tx(q_full, (has1 ? 2u : 1u) * kTileBytes);
-      for (int qt = 0; qt < (has1 ? 2 : 1); ++qt)
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + SL::q + qt * kTileBytes + c * kBoxBytes, &tm[0], q_full,
-                      TILE_HEAD(qt) * kHeadDim + c * 64, TILE_R0(qt));
-      Cursor cur = cursor_at(prob, imax, t_begin);
-      for (int it = 0; it < ntiles; ++it) {
-        const CUtensorMap* km = &tm[1 + 2 * cur.seg];
-        const CUtensorMap* vm = &tm[2 + 2 * cur.seg];
-        const int ks = it % KS, vs = it % kVStages;
-        if (it >= KS) mbar_wait(k_empty + ks, ((it / KS) - 1) & 1);
-        mbar_expect_tx(k_full + ks, kTileBytes);
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + SL::k + ks * kTileBytes + c * kBoxBytes, km, k_full + ks,
-                      hk * kHeadDim + c * 64, cur.kt * kBlockN);
-        if (it >= kVStages) mbar_wait(v_empty + vs, ((it / kVStages) - 1) & 1);
-        mbar_expect_tx(v_full + vs, kTileBytes);
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + SL::v + vs * kTileBytes + c * kBoxBytes, vm, v_full + vs,
-                      hk * kHeadDim + c * 64, cur.kt * kBlockN);
-        cursor_next(prob, imax, cur);
-      }
-    }
-  } else if (warp == kMmaWarp) {
-    // ======================================================== MMA scheduler
-    if (elect_one()) {
-      const uint32_t idesc_h = idesc_bf16_f32(128, 64, 0, 0);    // QK half: N = 64 keys
-      const uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);  // P (TMEM), V MN-major
-      const uint32_t sq = smem_u32(smem + SL::q);
-      const uint32_t sk = smem_u32(smem + SL::k);
-      const uint32_t sv = smem_u32(smem + SL::v);
-      // QK(j) half h of Q tile qt: S cols [64h, 64h+64) <- Q_qt x K(j) rows [64h, 64h+64)
-      auto issue_qk_half = [&](int qt, int j, int h) {
-        const int ks = j % KS;
-        const uint32_t d = tmem + qt * 128 + h * 64;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t koff = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
-          mma_ss(d, sdesc_sw128(sq + qt * kTileBytes + koff, 16, 1024),
-                 sdesc_sw128(sk + ks * kTileBytes + koff + h * 64 * 128, 16, 1024), idesc_h,
-                 kk > 0 ? 1u : 0u);
-        }
-      };
-      // PV(j) half h: O_qt += P[keys 64h..64h+63] x V(j) rows [64h, 64h+64)
-      auto issue_pv_half = [&](int qt, int j, int h) {
-        const int vs = j % kVStages;
-        const uint32_t d = tmem + 256 + qt * 128;
-        const uint32_t a = tmem + qt * 128 + 64;
-#pragma unroll
-        for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
-          mma_ts(d, a + kk * 8, sdesc_sw128(sv + vs * kTileBytes + kk * 2048, kBoxBytes, 1024), idesc_pv,
-                 (j > 0 || kk > 0) ? 1u : 0u);
-      };
-      // K(j) / V(j) are released once every Q tile that uses tile j has issued its last MMA on it
-      auto users = [&](int j) { return (nt[0] > j ? 1 : 0) + (nt[1] > j ? 1 : 0); };
-      int k_done[KS] = {0, 0}, v_done[kVStages] = {0, 0};
-      auto k_release = [&](int j) {
-        if (++k_done[j % KS] == users(j)) {
-          tc_commit(k_empty + j % KS);
-          k_done[j % KS] = 0;
-        }
-      };
-      auto v_release = [&](int j) {
-        if (++v_done[j % kVStages] == users(j)) {
-          tc_commit(v_empty + j % kVStages);
-          v_done[j % kVStages] = 0;
-        }
-      };
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      if (ntiles > 0) {
-        mbar_wait(k_full, 0);
-        tc_fence_after();
-        for (int qt = 0; qt < 2; ++qt)
-          if (nt[qt] > 0) {
-            issue_qk_half(qt, 0, 0);
-            tc_commit(sA + qt);
-            issue_qk_half(qt, 0, 1);
-            tc_commit(sB + qt);
-            k_release(0);
-          }
-      }
-      // per Q tile: current tile j and phase (0: QK_A(j+1) after sfree(j), 1: PV_A(j) after
-      // pA(j), 2: PV_B(j) + QK_B(j+1) after pB(j))
-      int j[2] = {0, 0}, ph[2] = {0, 0};
-      bool a_issued[2] = {false, false};  // QK_A(j+1) issued for the current j
-      auto finished = [&](int qt) { return j[qt] >= nt[qt]; };
-      while (!(finished(0) && finished(1))) {
-        for (int qt = 0; qt < 2; ++qt) {
-          if (finished(qt)) continue;
-          const int jj = j[qt];
-          const bool next = jj + 1 < nt[qt];
-          if (ph[qt] == 0) {
-            if (!next) {
-              ph[qt] = 1;
-            } else if (mbar_try(sfree + qt, jj & 1) && mbar_try(k_full + (jj + 1) % KS, ((jj + 1) / KS) & 1)) {
-              tc_fence_after();
-              issue_qk_half(qt, jj + 1, 0);
-              tc_commit(sA + qt);
-              a_issued[qt] = true;
-              ph[qt] = 1;
-            }
-          }
-          if (ph[qt] == 1) {
-            if (mbar_try(pA + qt, jj & 1) && mbar_try(v_full + jj % kVStages, (jj / kVStages) & 1)) {
-              tc_fence_after();
-              issue_pv_half(qt, jj, 0);
-              ph[qt] = 2;
-            }
-          }
-          if (ph[qt] == 2) {
-            if (mbar_try(pB + qt, jj & 1)) {
-              tc_fence_after();
-              issue_pv_half(qt, jj, 1);
-              tc_commit(o_full + qt);
-              v_release(jj);
-              if (next) {
-                issue_qk_half(qt, jj + 1, 1);
-                tc_commit(sB + qt);
-                k_release(jj + 1);
-              }
-              a_issued[qt] = false;
-              ph[qt] = 0;
-              ++j[qt];
-            }
-          }
-        }
-      }
-    }
-  } else if (warp < kProducerWarp) {
-    // ======================================================== softmax warpgroups
-    const int qt = warp >> 2;
-    const int quad = warp & 3;
-    const int row = TILE_R0(qt) + quad * 32 + lane;
-    const int qhead = TILE_HEAD(qt);
-    const uint32_t t_lane = static_cast<uint32_t>(quad * 32) << 16;
-    const uint32_t tS = tmem + t_lane + qt * 128;
-    const uint32_t tO = tmem + t_lane + 256 + qt * 128;
-    const float sl2 = P.scale_log2;
-    const float2 sl2v = make_float2(sl2, sl2);
-    float m_ref = -INFINITY;
-    float l = 0.f;
-    Cursor cur = cursor_at(prob, imax, t_begin);
-    uint32_t sr[4][32];
-    uint32_t pk[2][16];
-    for (int it = 0; it < nt[qt]; ++it, cursor_next(prob, imax, cur)) {
-      const AttnSeg sg = prob.seg[cur.seg];
-      const int mode = tile_mode(sg, cur.kt, TILE_R0(qt), nq);
-      mbar_wait(sA + qt, it & 1);
-      mbar_wait(sB + qt, it & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(tS + 32 * c, sr[c]);
-      tmem_wait_ld();
-      if (mode == kPart) {
-        const int k0 = cur.kt * kBlockN;
-        int lim = sg.len - k0;
-        if (sg.causal) lim = min(lim, row - k0 + 1);
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int jv = 0; jv < 32; ++jv)
-            if (c * 32 + jv >= lim) sr[c][jv] = __float_as_uint(-INFINITY);
-      }
-      float mxp[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int jv = 0; jv < 32; jv += 2) {
-          const int t = (jv / 2) & 7;
-          mxp[t] = fmaxf(mxp[t], fmaxf(__uint_as_float(sr[c][jv]), __uint_as_float(sr[c][jv + 1])));
-        }
-      // S is in registers: the next tile's QK half A may overwrite S columns 0-63 now
-      tc_fence_before();
-      mbar_arrive(sfree + qt);
-      const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
-                             fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
-      float alpha = 1.f;
-      bool rescale = false;
-      const float m_new = fmaxf(m_ref, mx * sl2);
-      if (m_new > m_ref + 8.f) {  // lazy rescale (P <= 2^8 otherwise)
-        alpha = exp2f(m_ref - m_new);
-        m_ref = m_new;
-        rescale = true;
-      }
-      const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
-      const float2 negm = make_float2(-m_use, -m_use);
-      float2 sacc[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const int c = 2 * h + cc;
-#pragma unroll
-          for (int jv = 0; jv < 16; ++jv) {
-            const float2 x2 = __ffma2_rn(make_float2(__uint_as_float(sr[c][2 * jv]),
-                                                     __uint_as_float(sr[c][2 * jv + 1])), sl2v, negm);
-            float2 p2;
-            if (kEmu > 0 && mode == kFull && emu_slot(jv, kEmu))
-              p2 = exp2_poly2(x2);
-            else
-              p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));
-            sacc[jv & 3] = __fadd2_rn(sacc[jv & 3], p2);
-            __nv_bfloat162 bb = __floats2bfloat162_rn(p2.x, p2.y);
-            pk[cc][jv] = *reinterpret_cast<uint32_t*>(&bb);
-          }
-        }
-        // P keys [64h, 64h+64) -> S columns 64 + 32h .. (packed bf16 pairs)
-        tmem_st16(tS + 64 + 32 * h, pk[0]);
-        tmem_st16(tS + 64 + 32 * h + 16, pk[1]);
-        if (h == 0 && rescale && it > 0) {
-          // PV(it-1) is complete: S(it) half B only landed after it in the tensor pipe
-          mbar_wait(o_full + qt, (it - 1) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t o[32];
-            tmem_ld32(tO + 32 * c, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int jv = 0; jv < 32; ++jv) o[jv] = __float_as_uint(__uint_as_float(o[jv]) * alpha);
-            tmem_st32(tO + 32 * c, o);
-          }
-        }
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(h == 0 ? pA + qt : pB + qt);
-      }
-      const float2 sum2 = __fadd2_rn(__fadd2_rn(sacc[0], sacc[1]), __fadd2_rn(sacc[2], sacc[3]));
-      l = l * alpha + (sum2.x + sum2.y);
-    }
-    // ---- epilogue: O / l, lse
-    const int cnt = nt[qt];
-    if (cnt > 0) {
-      mbar_wait(o_full + qt, (cnt - 1) & 1);  // only PV(cnt-1) can still be in flight
-      tc_fence_after();
-    }
-    const bool valid_row = row < nq;
-    const float inv = (l > 0.f) ? 1.f / l : 0.f;
-    const long long obase = static_cast<long long>(split) * prob.split_stride_out +
-                            static_cast<long long>(row) * prob.ldo + qhead * kHeadDim;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t o[32];
-      if (cnt > 0) {
-        tmem_ld32(tO + 32 * c, o);
-        tmem_wait_ld();
-      } else {
-#pragma unroll
-        for (int jv = 0; jv < 32; ++jv) o[jv] = 0u;
-      }
-      if (valid_row) {
-        if (prob.out_f32) {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(prob.out) + obase + 32 * c);
-#pragma unroll
-          for (int jv = 0; jv < 8; ++jv)
-            dst[jv] = make_float4(__uint_as_float(o[4 * jv]) * inv, __uint_as_float(o[4 * jv + 1]) * inv,
-                                  __uint_as_float(o[4 * jv + 2]) * inv, __uint_as_float(o[4 * jv + 3]) * inv);
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(prob.out) + obase + 32 * c);
-#pragma unroll
-          for (int jv = 0; jv < 4; ++jv) {
-            uint32_t w[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              __nv_bfloat162 bb = __floats2bfloat162_rn(__uint_as_float(o[8 * jv + 2 * e]) * inv,
-                                                        __uint_as_float(o[8 * jv + 2 * e + 1]) * inv);
-              w[e] = *reinterpret_cast<uint32_t*>(&bb);
-            }
-            dst[jv] = make_uint4(w[0], w[1], w[2], w[3]);
-          }
-        }
-      }
-    }
-    if (valid_row && prob.lse) {
-      const float lse = (l > 0.f) ? (m_ref + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
-      prob.lse[static_cast<long long>(split) * prob.split_stride_lse +
-               static_cast<long long>(row) * prob.ld_lse + qhead] = lse;
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == kMmaWarp) tmem_dealloc(tmem, kTmemCols);
-#undef TILE_R0
-#undef TILE_HEAD
-}
-
-// ============================================================================ variant family 1
-// One Q tile (128 rows of one q-head) per CTA with the score accumulator double-buffered
-// in TMEM: S_0 | S_1 | O (384 of 512 columns).  The MMA warp issues QK(j+2) into the buffer
-// of tile j right behind PV(j), so S(j+1) is already resident when the softmax finishes
-// tile j: the per-tile critical loop is the softmax body alone (not body + PV + QK as in
-// the ping-pong family, whose QK(j+1) must wait for PV(j) because P aliases S).
-//   warps 0-3  softmax (thread = TMEM lane = query row), epilogue
-//   warp 4     TMA producer (Q once, then K/V rings)
-//   warp 5     TMEM allocator + single-thread tcgen05.mma issuer
-constexpr int kThreads1 = 192;
-constexpr int kKS1 = 3, kVS1 = 2;
-struct Smem1 {
-  static constexpr uint32_t q = 0;
-  static constexpr uint32_t k = q + kTileBytes;
-  static constexpr uint32_t v = k + kKS1 * kTileBytes;
-  static constexpr uint32_t bar = v + kVS1 * kTileBytes;
-  static constexpr uint32_t total = bar + 256;
-  static constexpr uint32_t bytes = total + 1024;
-};
-
-template <int kEmu, bool kPipe>
-__global__ void __launch_bounds__(kThreads1, 1) attn_fwd1_kernel(const __grid_constant__ AttnParams P) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem1::bar);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;           // [kKS1]
-  uint64_t* k_empty = k_full + kKS1;     // [kKS1]
-  uint64_t* v_full = k_empty + kKS1;     // [kVS1]
-  uint64_t* v_empty = v_full + kVS1;     // [kVS1]
-  uint64_t* s_full = v_empty + kVS1;     // [2] S buffer b holds a fresh QK
-  uint64_t* p_full = s_full + 2;         // [2] P written into buffer b (O corrected)
-  uint64_t* o_full = p_full + 2;         // PV complete
-  uint64_t* o_done = o_full + 1;         // every MMA of the CTA complete (epilogue)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
-
-  const int warp = warp_id();
-  const int lane = lane_id();
-
-  int pi = 0;
-  while (pi + 1 < P.nprob && static_cast<int>(blockIdx.x) >= P.prob[pi + 1].work_begin) ++pi;
-  const AttnProb& prob = P.prob[pi];
-  int local = static_cast<int>(blockIdx.x) - prob.work_begin;
-  const int split = local % prob.splits;
-  local /= prob.splits;
-  const int head = local % P.hq;
-  local /= P.hq;
-  const int unit = prob.units - 1 - local;  // heaviest (latest causal rows) first
-  const int i0 = unit * kBlockM;
-  const int nq = prob.nq;
-  const int imax = min(i0 + kBlockM, nq);
-  const int hk = head / (P.hq / P.hkv);
-
-  int T = 0;
-  for (int s = 0; s < prob.nseg; ++s) T += seg_tiles(prob.seg[s], imax);
-  const int t_begin = static_cast<int>(static_cast<long long>(T) * split / prob.splits);
-  const int t_end = static_cast<int>(static_cast<long long>(T) * (split + 1) / prob.splits);
-  const int ntiles = t_end - t_begin;
-  const CUtensorMap* tm = P.tmap[pi];
-
-  if (warp == 4 && elect_one()) {
-    mbar_init(q_full, 1);
-    for (int s = 0; s < kKS1; ++s) {
-      mbar_init(k_full + s, 1);
-      mbar_init(k_empty + s, 1);
-    }
-    for (int s = 0; s < kVS1; ++s) {
-      mbar_init(v_full + s, 1);
-      mbar_init(v_empty + s, 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(s_full + b, 1);
-      mbar_init(p_full + b, 128);
-    }
-    mbar_init(o_full, 1);
-    mbar_init(o_done, 1);
-    fence_barrier_init();
-    tma_prefetch_desc(&tm[0]);
-    for (int s = 0; s < prob.nseg; ++s) {
-      tma_prefetch_desc(&tm[1 + 2 * s]);
-      tma_prefetch_desc(&tm[2 + 2 * s]);
-    }
-  }
-  if (warp == 5) tmem_alloc(tmem_slot, kTmemCols);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 4) {
-    // ======================================================== TMA producer
-    if (elect_one()) {
-      mbar_expect_tx(q_full, kTileBytes);
-      for (int c = 0; c < 2; ++c)
-        tma_load_2d(smem + Smem1::q + c * kBoxBytes, &tm[0], q_full, head * kHeadDim + c * 64, i0);
-      Cursor cur = cursor_at(prob, imax, t_begin);
-      for (int it = 0; it < ntiles; ++it) {
-        const CUtensorMap* km = &tm[1 + 2 * cur.seg];
-        const CUtensorMap* vm = &tm[2 + 2 * cur.seg];
-        const int ks = it % kKS1, vs = it % kVS1;
-        if (it >= kKS1) mbar_wait(k_empty + ks, ((it / kKS1) - 1) & 1);
-        mbar_expect_tx(k_full + ks, kTileBytes);
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + Smem1::k + ks * kTileBytes + c * kBoxBytes, km, k_full + ks,
-                      hk * kHeadDim + c * 64, cur.kt * kBlockN);
-        if (it >= kVS1) mbar_wait(v_empty + vs, ((it / kVS1) - 1) & 1);
-        mbar_expect_tx(v_full + vs, kTileBytes);
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + Smem1::v + vs * kTileBytes + c * kBoxBytes, vm, v_full + vs,
-                      hk * kHeadDim + c * 64, cur.kt * kBlockN);
-        cursor_next(prob, imax, cur);
-      }
-    }
-  } else if (warp == 5) {
-    // ======================================================== MMA issuer
-    if (elect_one()) {
-      const uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
-      const uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
-      const uint32_t sq = smem_u32(smem + Smem1::q);
-      const uint32_t sk = smem_u32(smem + Smem1::k);
-      const uint32_t sv = smem_u32(smem + Smem1::v);
-      auto issue_qk = [&](int b, int it) {
-        const int ks = it % kKS1;
-        mbar_wait(k_full + ks, (it / kKS1) & 1);
-        tc_fence_after();
-        const uint32_t d = tmem + b * 128;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t koff = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
-          mma_ss(d, sdesc_sw128(sq + koff, 16, 1024), sdesc_sw128(sk + ks * kTileBytes + koff, 16, 1024),
-                 idesc_qk, kk > 0 ? 1u : 0u);
-        }
-        tc_commit(s_full + b);
-        tc_commit(k_empty + ks);
-      };
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      if (ntiles > 0) issue_qk(0, 0);
-      if (ntiles > 1) issue_qk(1, 1);
-      for (int it = 0; it < ntiles; ++it) {
-        const int b = it & 1, vs = it % kVS1;
-        mbar_wait(v_full + vs, (it / kVS1) & 1);
-        mbar_wait(p_full + b, (it >> 1) & 1);
-        tc_fence_after();
-        const uint32_t d = tmem + 256;
-        const uint32_t a = tmem + b * 128;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ts(d, a + kk * 8, sdesc_sw128(sv + vs * kTileBytes + kk * 2048, kBoxBytes, 1024), idesc_pv,
-                 (it > 0 || kk > 0) ? 1u : 0u);
-        tc_commit(o_full);
-        tc_commit(v_empty + vs);
-        // QK(it+2) reuses buffer b: issued behind PV(it), the in-order tensor pipe keeps
-        // P(it) intact until PV(it) has read it.
-        if (it + 2 < ntiles) issue_qk(b, it + 2);
-      }
-      tc_commit(o_done);
-    }
-  } else {
-    // ======================================================== softmax warpgroup
-    const int quad = warp;
-    const int row = i0 + quad * 32 + lane;
-    const uint32_t t_lane = static_cast<uint32_t>(quad * 32) << 16;
-    const uint32_t tO = tmem + t_lane + 256;
-    const float sl2 = P.scale_log2;
-    const float2 sl2v = make_float2(sl2, sl2);
-    float m_ref = -INFINITY;
-    float l = 0.f;
-    Cursor cur = cursor_at(prob, imax, t_begin);
-    uint32_t sr[4][32];
-    uint32_t pk[4][16];
-    for (int it = 0; it < ntiles; ++it, cursor_next(prob, imax, cur)) {
-      const int b = it & 1;
-      const uint32_t tS = tmem + t_lane + b * 128;
-      const AttnSeg sg = prob.seg[cur.seg];
-      const int mode = tile_mode(sg, cur.kt, i0, nq);
-      mbar_wait(s_full + b, (it >> 1) & 1);
-      tc_fence_after();
-      auto load_s = [&]() {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32(tS + 32 * c, sr[c]);
-        tmem_wait_ld();
-      };
-      auto chunk_max = [&](int c, float (&mxp)[8]) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          const int t = (j / 2) & 7;
-          mxp[t] = fmaxf(mxp[t], fmaxf(__uint_as_float(sr[c][j]), __uint_as_float(sr[c][j + 1])));
-        }
-      };
-      auto chunk_exp = [&](int c, float2 negm, bool emu) {  // in place: sr[c] := p
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float2 x2 = __ffma2_rn(
-              make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1])), sl2v, negm);
-          float2 p2;
-          if (kEmu > 0 && emu && emu_slot(j, kEmu))
-            p2 = exp2_poly2(x2);
-          else
-            p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));  // -inf -> 0
-          sr[c][2 * j] = __float_as_uint(p2.x);
-          sr[c][2 * j + 1] = __float_as_uint(p2.y);
-        }
-      };
-      auto chunk_pack = [&](int c, float2 (&sacc)[4]) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float2 p2 = make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1]));
-          sacc[j & 3] = __fadd2_rn(sacc[j & 3], p2);
-          __nv_bfloat162 bb = __floats2bfloat162_rn(p2.x, p2.y);
-          pk[c][j] = *reinterpret_cast<uint32_t*>(&bb);
-        }
-      };
-      auto exp_pack_all = [&](float2 negm, bool emu, float2 (&sacc)[4]) {
-        if constexpr (kPipe) {
-          chunk_exp(0, negm, emu);
-#pragma unroll
-          for (int c = 1; c < 4; ++c) {
-            chunk_exp(c, negm, emu);
-            chunk_pack(c - 1, sacc);
-          }
-          chunk_pack(3, sacc);
-        } else {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            chunk_exp(c, negm, emu);
-            chunk_pack(c, sacc);
-          }
-        }
-      };
-      float alpha = 1.f;
-      bool rescale = false;
-      float mxp[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
-      float2 sacc[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
-      bool done = false;
-      load_s();
-      if (mode == kFull && m_ref != -INFINITY) {
-        // speculative pass against the running max (see the ping-pong kernel)
-        const float2 negm = make_float2(-m_ref, -m_ref);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) chunk_max(c, mxp);
-        exp_pack_all(negm, true, sacc);
-        const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
-                               fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
-        done = !(mx * sl2 > m_ref + 8.f);
-        if (!done) {
-#pragma unroll
-          for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
-          load_s();
-        }
-      } else if (mode == kPart) {
-        const int k0 = cur.kt * kBlockN;
-        int lim = sg.len - k0;
-        if (sg.causal) lim = min(lim, row - k0 + 1);
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c * 32 + j >= lim) sr[c][j] = __float_as_uint(-INFINITY);
-      }
-      if (!done) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) chunk_max(c, mxp);
-        const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
-                               fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
-        const float m_new = fmaxf(m_ref, mx * sl2);
-        if (m_new > m_ref + 8.f) {
-          alpha = exp2f(m_ref - m_new);
-          m_ref = m_new;
-          rescale = true;
-        }
-        const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
-        exp_pack_all(make_float2(-m_use, -m_use), mode == kFull, sacc);
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_st16(tS + 16 * c, pk[c]);
-      const float2 sum2 = __fadd2_rn(__fadd2_rn(sacc[0], sacc[1]), __fadd2_rn(sacc[2], sacc[3]));
-      l = l * alpha + (sum2.x + sum2.y);
-      if (rescale && it > 0) {
-        mbar_wait(o_full, (it - 1) & 1);  // PV(it-1) has landed in O
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t o[32];
-          tmem_ld32(tO + 32 * c, o);
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-          tmem_st32(tO + 32 * c, o);
-        }
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(p_full + b);
-    }
-    // ---- epilogue: O / l, lse
-    // S double-buffered: PV(n-1) and PV(n) may both be in flight, which a parity wait on
-    // o_full cannot disambiguate -- wait for the MMA warp's final commit instead.
-    mbar_wait(o_done, 0);
-    tc_fence_after();
-    const bool valid_row = row < nq;
-    const float inv = (l > 0.f) ? 1.f / l : 0.f;
-    const long long obase = static_cast<long long>(split) * prob.split_stride_out +
-                            static_cast<long long>(row) * prob.ldo + head * kHeadDim;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t o[32];
-      if (ntiles > 0) {
-        tmem_ld32(tO + 32 * c, o);
-        tmem_wait_ld();
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) o[j] = 0u;
-      }
-      if (valid_row) {
-        if (prob.out_f32) {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(prob.out) + obase + 32 * c);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            dst[j] = make_float4(__uint_as_float(o[4 * j]) * inv, __uint_as_float(o[4 * j + 1]) * inv,
-                                 __uint_as_float(o[4 * j + 2]) * inv, __uint_as_float(o[4 * j + 3]) * inv);
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(prob.out) + obase + 32 * c);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            uint32_t w[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              __nv_bfloat162 bb = __floats2bfloat162_rn(__uint_as_float(o[8 * j + 2 * e]) * inv,
-                                                        __uint_as_float(o[8 * j + 2 * e + 1]) * inv);
-              w[e] = *reinterpret_cast<uint32_t*>(&bb);
-            }
-            dst[j] = make_uint4(w[0], w[1], w[2], w[3]);
-          }
-        }
-      }
-    }
-    if (valid_row && prob.lse) {
-      const float lse = (l > 0.f) ? (m_ref + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
-      prob.lse[static_cast<long long>(split) * prob.split_stride_lse +
-               static_cast<long long>(row) * prob.ld_lse + head] = lse;
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 5) tmem_dealloc(tmem, kTmemCols);
-}
-
-// ============================================================================ variant family 3
-// Family 1 (one Q tile per CTA, S double-buffered: S_0 | S_1 | O) with the softmax split by
-// COLUMNS over two warpgroups: warps 0-3 take keys 0-63 of every tile, warps 4-7 keys
-// 64-127 of the same rows (a warp and its partner share TMEM lanes).  Each SMSP then holds
-// two softmax warps working on the same tile with half the exps each, so one warp's MUFU
-// stream fills the other's issue gaps, and the double-buffered S keeps the next tile's QK
-// off the critical path.  The halves agree on the running max through a per-tile exchange
-// in shared memory (named barrier of the 256 softmax threads); the row sum is combined in
-// the epilogue.
-constexpr int kThreads3 = 320;  // warps 0-7 softmax (2 column halves), 8 TMA, 9 MMA
-struct Smem3 {
-  static constexpr uint32_t q = 0;
-  static constexpr uint32_t k = q + kTileBytes;
-  static constexpr uint32_t v = k + kKS1 * kTileBytes;
-  static constexpr uint32_t xch = v + kVS1 * kTileBytes;        // [2 buf][2 half][128] f32
-  static constexpr uint32_t bar = xch + 2 * 2 * 128 * 4;
-  static constexpr uint32_t total = bar + 256;
-  static constexpr uint32_t bytes = total + 1024;
-};
-
-__device__ __forceinline__ void named_bar_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
-template <int kEmu>
-__global__ void __launch_bounds__(kThreads3, 1) attn_fwd3_kernel(const __grid_constant__ AttnParams P) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem3::bar);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;           // [kKS1]
-  uint64_t* k_empty = k_full + kKS1;     // [kKS1]
-  uint64_t* v_full = k_empty + kKS1;     // [kVS1]
-  uint64_t* v_empty = v_full + kVS1;     // [kVS1]
-  uint64_t* s_full = v_empty + kVS1;     // [2]
-  uint64_t* p_full = s_full + 2;         // [2] both halves' P written (256 arrivals)
-  uint64_t* o_full = p_full + 2;         // PV complete
-  uint64_t* o_done = o_full + 1;         // every MMA complete (epilogue)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
-  float* xch = reinterpret_cast<float*>(smem + Smem3::xch);
-
-  const int warp = warp_id();
-  const int lane = lane_id();
-
-  int pi = 0;
-  while (pi + 1 < P.nprob && static_cast<int>(blockIdx.x) >= P.prob[pi + 1].work_begin) ++pi;
-  const AttnProb& prob = P.prob[pi];
-  int local = static_cast<int>(blockIdx.x) - prob.work_begin;
-  const int split = local % prob.splits;
-  local /= prob.splits;
-  const int head = local % P.hq;
-  local /= P.hq;
-  const int unit = prob.units - 1 - local;
-  const int i0 = unit * kBlockM;
-  const int nq = prob.nq;
-  const int imax = min(i0 + kBlockM, nq);
-  const int hk = head / (P.hq / P.hkv);
-
-  int T = 0;
-  for (int s = 0; s < prob.nseg; ++s) T += seg_tiles(prob.seg[s], imax);
-  const int t_begin = static_cast<int>(static_cast<long long>(T) * split / prob.splits);
-  const int t_end = static_cast<int>(static_cast<long long>(T) * (split + 1) / prob.splits);
-  const int ntiles = t_end - t_begin;
-  const CUtensorMap* tm = P.tmap[pi];
-
-  if (warp == 8 && elect_one()) {
-    mbar_init(q_full, 1);
-    for (int s = 0; s < kKS1; ++s) {
-      mbar_init(k_full + s, 1);
-      mbar_init(k_empty + s, 1);
-    }
-    for (int s = 0; s < kVS1; ++s) {
-      mbar_init(v_full + s, 1);
-      mbar_init(v_empty + s, 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(s_full + b, 1);
-      mbar_init(p_full + b, 256);
-    }
-    mbar_init(o_full, 1);
-    mbar_init(o_done, 1);
-    fence_barrier_init();
-    tma_prefetch_desc(&tm[0]);
-    for (int s = 0; s < prob.nseg; ++s) {
-      tma_prefetch_desc(&tm[1 + 2 * s]);
-      tma_prefetch_desc(&tm[2 + 2 * s]);
-    }
-  }
-  if (warp == 9) tmem_alloc(tmem_slot, kTmemCols);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 8) {
-    // ======================================================== TMA producer
-    if (elect_one()) {
-      mbar_expect_tx(q_full, kTileBytes);
-      for (int c = 0; c < 2; ++c)
-        tma_load_2d(smem + Smem3::q + c * kBoxBytes, &tm[0], q_full, head * kHeadDim + c * 64, i0);
-      Cursor cur = cursor_at(prob, imax, t_begin);
-      for (int it = 0; it < ntiles; ++it) {
-        const CUtensorMap* km = &tm[1 + 2 * cur.seg];
-        const CUtensorMap* vm = &tm[2 + 2 * cur.seg];
-        const int ks = it % kKS1, vs = it % kVS1;
-        if (it >= kKS1) mbar_wait(k_empty + ks, ((it / kKS1) - 1) & 1);
-        mbar_expect_tx(k_full + ks, kTileBytes);
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + Smem3::k + ks * kTileBytes + c * kBoxBytes, km, k_full + ks,
-                      hk * kHeadDim + c * 64, cur.kt * kBlockN);
-        if (it >= kVS1) mbar_wait(v_empty + vs, ((it / kVS1) - 1) & 1);
-        mbar_expect_tx(v_full + vs, kTileBytes);
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + Smem3::v + vs * kTileBytes + c * kBoxBytes, vm, v_full + vs,
-                      hk * kHeadDim + c * 64, cur.kt * kBlockN);
-        cursor_next(prob, imax, cur);
-      }
-    }
-  } else if (warp == 9) {
-    // ======================================================== MMA issuer (as family 1)
-    if (elect_one()) {
-      const uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);
-      const uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);
-      const uint32_t sq = smem_u32(smem + Smem3::q);
-      const uint32_t sk = smem_u32(smem + Smem3::k);
-      const uint32_t sv = smem_u32(smem + Smem3::v);
-      auto issue_qk = [&](int b, int it) {
-        const int ks = it % kKS1;
-        mbar_wait(k_full + ks, (it / kKS1) & 1);
-        tc_fence_after();
-        const uint32_t d = tmem + b * 128;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t koff = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
-          mma_ss(d, sdesc_sw128(sq + koff, 16, 1024), sdesc_sw128(sk + ks * kTileBytes + koff, 16, 1024),
-                 idesc_qk, kk > 0 ? 1u : 0u);
-        }
-        tc_commit(s_full + b);
-        tc_commit(k_empty + ks);
-      };
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      if (ntiles > 0) issue_qk(0, 0);
-      if (ntiles > 1) issue_qk(1, 1);
-      for (int it = 0; it < ntiles; ++it) {
-        const int b = it & 1, vs = it % kVS1;
-        mbar_wait(v_full + vs, (it / kVS1) & 1);
-        mbar_wait(p_full + b, (it >> 1) & 1);
-        tc_fence_after();
-        const uint32_t d = tmem + 256;
-        const uint32_t a = tmem + b * 128;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ts(d, a + kk * 8, sdesc_sw128(sv + vs * kTileBytes + kk * 2048, kBoxBytes, 1024), idesc_pv,
-                 (it > 0 || kk > 0) ? 1u : 0u);
-        tc_commit(o_full);
-        tc_commit(v_empty + vs);
-        if (it + 2 < ntiles) issue_qk(b, it + 2);
-      }
-      tc_commit(o_done);
-    }
-  } else {
-    // ======================================================== softmax: 2 column halves
-    const int half = warp >> 2;   // 0: keys 0-63 of each tile, 1: keys 64-127
-    const int quad = warp & 3;
-    const int rloc = quad * 32 + lane;
-    const int row = i0 + rloc;
-    const uint32_t t_lane = static_cast<uint32_t>(quad * 32) << 16;
-    const uint32_t tO = tmem + t_lane + 256 + half * 64;  // this half rescales/stores O cols
-    const float sl2 = P.scale_log2;
-    const float2 sl2v = make_float2(sl2, sl2);
-    float m_ref = -INFINITY;
-    float l = 0.f;
-    int xc = 0;  // exchange counter (identical in both halves: same decisions)
-    // max of this half's 64 scores, combined with the partner half through smem
-    auto exchange_max = [&](float mine) {
-      float* buf = xch + (xc & 1) * 256;
-      buf[half * 128 + rloc] = mine;
-      named_bar_sync(1, 256);
-      const float other = buf[(half ^ 1) * 128 + rloc];
-      ++xc;
-      return fmaxf(mine, other);
-    };
-    Cursor cur = cursor_at(prob, imax, t_begin);
-    uint32_t sr[2][32];
-    uint32_t pk[2][16];
-    for (int it = 0; it < ntiles; ++it, cursor_next(prob, imax, cur)) {
-      const int b = it & 1;
-      const uint32_t tS = tmem + t_lane + b * 128;
-      const AttnSeg sg = prob.seg[cur.seg];
-      const int mode = tile_mode(sg, cur.kt, i0, nq);
-      mbar_wait(s_full + b, (it >> 1) & 1);
-      tc_fence_after();
-      auto load_s = [&]() {
-        tmem_ld32(tS + half * 64, sr[0]);
-        tmem_ld32(tS + half * 64 + 32, sr[1]);
-        tmem_wait_ld();
-      };
-      auto chunk_max = [&](int c, float (&mxp)[8]) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          const int t = (j / 2) & 7;
-          mxp[t] = fmaxf(mxp[t], fmaxf(__uint_as_float(sr[c][j]), __uint_as_float(sr[c][j + 1])));
-        }
-      };
-      auto chunk_exp = [&](int c, float2 negm, bool emu) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float2 x2 = __ffma2_rn(
-              make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1])), sl2v, negm);
-          float2 p2;
-          if (kEmu > 0 && emu && emu_slot(j, kEmu))
-            p2 = exp2_poly2(x2);
-          else
-            p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));
-          sr[c][2 * j] = __float_as_uint(p2.x);
-          sr[c][2 * j + 1] = __float_as_uint(p2.y);
-        }
-      };
-      auto chunk_pack = [&](int c, float2 (&sacc)[4]) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float2 p2 = make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1]));
-          sacc[j & 3] = __fadd2_rn(sacc[j & 3], p2);
-          __nv_bfloat162 bb = __floats2bfloat162_rn(p2.x, p2.y);
-          pk[c][j] = *reinterpret_cast<uint32_t*>(&bb);
-        }
-      };
-      auto exp_pack_all = [&](float2 negm, bool emu, float2 (&sacc)[4]) {
-        chunk_exp(0, negm, emu);
-        chunk_exp(1, negm, emu);
-        chunk_pack(0, sacc);
-        chunk_pack(1, sacc);
-      };
-      auto max8 = [](const float (&m)[8]) {
-        return fmaxf(fmaxf(fmaxf(m[0], m[1]), fmaxf(m[2], m[3])), fmaxf(fmaxf(m[4], m[5]), fmaxf(m[6], m[7])));
-      };
-      float alpha = 1.f;
-      bool rescale = false;
-      float mxp[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
-      float2 sacc[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
-      bool done = false;
-      load_s();
-      if (mode == kFull && m_ref != -INFINITY) {
-        const float2 negm = make_float2(-m_ref, -m_ref);
-        chunk_max(0, mxp);
-        chunk_max(1, mxp);
-        exp_pack_all(negm, true, sacc);
-        const float mx = exchange_max(max8(mxp));
-        done = !(mx * sl2 > m_ref + 8.f);
-        if (!done) {
-#pragma unroll
-          for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
-          load_s();
-        }
-      } else if (mode == kPart) {
-        const int k0 = cur.kt * kBlockN + half * 64;
-        int lim = sg.len - k0;
-        if (sg.causal) lim = min(lim, row - k0 + 1);
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c * 32 + j >= lim) sr[c][j] = __float_as_uint(-INFINITY);
-      }
-      if (!done) {
-        chunk_max(0, mxp);
-        chunk_max(1, mxp);
-        const float mx = exchange_max(max8(mxp));
-        const float m_new = fmaxf(m_ref, mx * sl2);
-        if (m_new > m_ref + 8.f) {
-          alpha = exp2f(m_ref - m_new);
-          m_ref = m_new;
-          rescale = true;
-        }
-        const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
-        exp_pack_all(make_float2(-m_use, -m_use), mode == kFull, sacc);
-      }
-      tmem_st16(tS + half * 32, pk[0]);
-      tmem_st16(tS + half * 32 + 16, pk[1]);
-      const float2 sum2 = __fadd2_rn(__fadd2_rn(sacc[0], sacc[1]), __fadd2_rn(sacc[2], sacc[3]));
-      l = l * alpha + (sum2.x + sum2.y);  // this half's share of the row sum
-      if (rescale && it > 0) {
-        mbar_wait(o_full, (it - 1) & 1);  // PV(it-1) has landed in O
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t o[32];
-          tmem_ld32(tO + 32 * c, o);
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-          tmem_st32(tO + 32 * c, o);
-        }
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(p_full + b);
-    }
-    // ---- epilogue: the row sum of both halves, O / l (this half's 64 columns), lse
-    {
-      float* buf = xch + (xc & 1) * 256;
-      buf[half * 128 + rloc] = l;
-      named_bar_sync(1, 256);
-      l += buf[(half ^ 1) * 128 + rloc];
-    }
-    mbar_wait(o_done, 0);
-    tc_fence_after();
-    const bool valid_row = row < nq;
-    const float inv = (l > 0.f) ? 1.f / l : 0.f;
-    const long long obase = static_cast<long long>(split) * prob.split_stride_out +
-                            static_cast<long long>(row) * prob.ldo + head * kHeadDim + half * 64;
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      uint32_t o[32];
-      if (ntiles > 0) {
-        tmem_ld32(tO + 32 * c, o);
-        tmem_wait_ld();
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) o[j] = 0u;
-      }
-      if (valid_row) {
-        if (prob.out_f32) {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(prob.out) + obase + 32 * c);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            dst[j] = make_float4(__uint_as_float(o[4 * j]) * inv, __uint_as_float(o[4 * j + 1]) * inv,
-                                 __uint_as_float(o[4 * j + 2]) * inv, __uint_as_float(o[4 * j + 3]) * inv);
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(prob.out) + obase + 32 * c);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            uint32_t w[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              __nv_bfloat162 bb = __floats2bfloat162_rn(__uint_as_float(o[8 * j + 2 * e]) * inv,
-                                                        __uint_as_float(o[8 * j + 2 * e + 1]) * inv);
-              w[e] = *reinterpret_cast<uint32_t*>(&bb);
-            }
-            dst[j] = make_uint4(w[0], w[1], w[2], w[3]);
-          }
-        }
-      }
-    }
-    if (valid_row && prob.lse && half == 0) {
-      const float lse = (l > 0.f) ? (m_ref + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
-      prob.lse[static_cast<long long>(split) * prob.split_stride_lse +
-               static_cast<long long>(row) * prob.ld_lse + head] = lse;
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 9) tmem_dealloc(tmem, kTmemCols);
-}
-
-// ============================================================================ variant family 2
-// Two Q tiles (256 rows, or two q-heads of one GQA group) per CTA as in the ping-pong
-// family, but with 64-key KV tiles so each Q tile's score accumulator fits TMEM twice:
-// S_0[2] | S_1[2] (64 columns each) | O_0 | O_1 = 512 columns.  QK_t(j+2) is issued right
-// behind PV_t(j) into the buffer PV_t(j) just drained, so S_t(j+1) is resident when softmax
-// t finishes tile j: the two softmax warpgroups (one warp of each per SMSP) run back to back
-// and interleave their MUFU streams instead of each waiting one PV+QK per tile.
-constexpr int kBN2 = 64;
-constexpr int kKS2 = 4, kVS2 = 4;
-constexpr uint32_t kKvBox2 = kBN2 * 64 * 2;     // 64 rows x 64 bf16 (SW128 box)
-constexpr uint32_t kKvTile2 = 2 * kKvBox2;      // 64 keys x 128 dh
-struct Smem2 {
-  static constexpr uint32_t q = 0;
-  static constexpr uint32_t k = q + kTilesPerCta * kTileBytes;
-  static constexpr uint32_t v = k + kKS2 * kKvTile2;
-  static constexpr uint32_t bar = v + kVS2 * kKvTile2;
-  static constexpr uint32_t total = bar + 256;
-  static constexpr uint32_t bytes = total + 1024;
-};
-
-__device__ __forceinline__ int seg_tiles2(const AttnSeg& s, int imax) {
-  const int klen = s.causal ? min(s.len, imax) : s.len;
-  return klen > 0 ? (klen + kBN2 - 1) / kBN2 : 0;
-}
-__device__ __forceinline__ int tile_mode2(const AttnSeg& s, int kt, int r0, int nq) {
-  if (r0 >= nq) return kSkip;
-  const int k0 = kt * kBN2;
-  const bool tail = k0 + kBN2 > s.len;
-  if (s.causal) {
-    const int rlast = min(r0 + kBlockM, nq) - 1;
-    if (k0 > rlast) return kSkip;
-    return (k0 + kBN2 - 1 > r0 || tail) ? kPart : kFull;
-  }
-  return tail ? kPart : kFull;
-}
-__device__ __forceinline__ Cursor cursor_at2(const AttnProb& p, int imax, int t) {
-  for (int s = 0; s < p.nseg; ++s) {
-    const int n = seg_tiles2(p.seg[s], imax);
-    if (t < n) return {s, t};
-    t -= n;
-  }
-  return {p.nseg, 0};
-}
-__device__ __forceinline__ void cursor_next2(const AttnProb& p, int imax, Cursor& c) {
-  ++c.kt;
-  while (c.seg < p.nseg && c.kt >= seg_tiles2(p.seg[c.seg], imax)) {
-    ++c.seg;
-    c.kt = 0;
-  }
-}
-
-template <int kEmu>
-__global__ void __launch_bounds__(kThreads, 1) attn_fwd2_kernel(const __grid_constant__ AttnParams P) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem2::bar);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;          // [kKS2]
-  uint64_t* k_empty = k_full + kKS2;    // [kKS2]
-  uint64_t* v_full = k_empty + kKS2;    // [kVS2]
-  uint64_t* v_empty = v_full + kVS2;    // [kVS2]
-  uint64_t* s_full = v_empty + kVS2;    // [2 tiles][2 buffers]
-  uint64_t* p_full = s_full + 4;        // [2][2]
-  uint64_t* o_full = p_full + 4;        // [2] PV_t complete
-  uint64_t* o_done = o_full + 2;        // every MMA of the CTA complete (epilogue)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
-
-  const int warp = warp_id();
-  const int lane = lane_id();
-
-  int pi = 0;
-  while (pi + 1 < P.nprob && static_cast<int>(blockIdx.x) >= P.prob[pi + 1].work_begin) ++pi;
-  const AttnProb& prob = P.prob[pi];
-  int local = static_cast<int>(blockIdx.x) - prob.work_begin;
-  const int split = local % prob.splits;
-  local /= prob.splits;
-  const int pair = prob.head_pair;
-  const int nheads = pair ? P.hq / 2 : P.hq;
-  const int head = pair ? 2 * (local % nheads) : local % nheads;
-  local /= nheads;
-  const int unit = prob.units - 1 - local;
-  const int i0 = pair ? 0 : unit * (kTilesPerCta * kBlockM);
-  const int nq = prob.nq;
-  const int imax = min(i0 + (pair ? kBlockM : kTilesPerCta * kBlockM), nq);
-  const int hk = head / (P.hq / P.hkv);
-#define TILE_R0(t) (pair ? 0 : i0 + (t) * kBlockM)
-#define TILE_HEAD(t) (head + pair * (t))
-
-  int T = 0;
-  for (int s = 0; s < prob.nseg; ++s) T += seg_tiles2(prob.seg[s], imax);
-  const int t_begin = static_cast<int>(static_cast<long long>(T) * split / prob.splits);
-  const int t_end = static_cast<int>(static_cast<long long>(T) * (split + 1) / prob.splits);
-  const int ntiles = t_end - t_begin;
-  const CUtensorMap* tm = P.tmap[pi];
-
-  if (warp == kProducerWarp && elect_one()) {
-    mbar_init(q_full, 1);
-    for (int s = 0; s < kKS2; ++s) {
-      mbar_init(k_full + s, 1);
-      mbar_init(k_empty + s, 1);
-    }
-    for (int s = 0; s < kVS2; ++s) {
-      mbar_init(v_full + s, 1);
-      mbar_init(v_empty + s, 1);
-    }
-    for (int i = 0; i < 4; ++i) {
-      mbar_init(s_full + i, 1);
-      mbar_init(p_full + i, 128);
-    }
-    mbar_init(o_full + 0, 1);
-    mbar_init(o_full + 1, 1);
-    mbar_init(o_done, 1);
-    fence_barrier_init();
-    tma_prefetch_desc(&tm[0]);
-    for (int s = 0; s < prob.nseg; ++s) {
-      tma_prefetch_desc(&tm[1 + 2 * s]);
-      tma_prefetch_desc(&tm[2 + 2 * s]);
-    }
-  }
-  if (warp == kMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == kProducerWarp) {
-    // ======================================================== TMA producer
-    if (elect_one()) {
-      const bool has1 = TILE_R0(1) < nq;
-      mbar_expect_tx(q_full, (has1 ? 2u : 1u) * kTileBytes);
-      for (int qt = 0; qt < (has1 ? 2 : 1); ++qt)
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + Smem2::q + qt * kTileBytes + c * kBoxBytes, &tm[0], q_full,
-                      TILE_HEAD(qt) * kHeadDim + c * 64, TILE_R0(qt));
-      Cursor cur = cursor_at2(prob, imax, t_begin);
-      for (int it = 0; it < ntiles; ++it) {
-        const CUtensorMap* km = &tm[1 + 2 * cur.seg];
-        const CUtensorMap* vm = &tm[2 + 2 * cur.seg];
-        const int ks = it % kKS2, vs = it % kVS2;
-        if (it >= kKS2) mbar_wait(k_empty + ks, ((it / kKS2) - 1) & 1);
-        mbar_expect_tx(k_full + ks, kKvTile2);
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + Smem2::k + ks * kKvTile2 + c * kKvBox2, km, k_full + ks,
-                      hk * kHeadDim + c * 64, cur.kt * kBN2);
-        if (it >= kVS2) mbar_wait(v_empty + vs, ((it / kVS2) - 1) & 1);
-        mbar_expect_tx(v_full + vs, kKvTile2);
-        for (int c = 0; c < 2; ++c)
-          tma_load_2d(smem + Smem2::v + vs * kKvTile2 + c * kKvBox2, vm, v_full + vs,
-                      hk * kHeadDim + c * 64, cur.kt * kBN2);
-        cursor_next2(prob, imax, cur);
-      }
-    }
-  } else if (warp == kMmaWarp) {
-    // ======================================================== MMA issuer
-    if (elect_one()) {
-      const uint32_t idesc_qk = idesc_bf16_f32(128, kBN2, 0, 0);  // Q, K both K-major
-      const uint32_t idesc_pv = idesc_bf16_f32(128, 128, 0, 1);   // P (TMEM), V MN-major
-      const uint32_t sq = smem_u32(smem + Smem2::q);
-      const uint32_t sk = smem_u32(smem + Smem2::k);
-      const uint32_t sv = smem_u32(smem + Smem2::v);
-      // per (tile, buffer) use counters -> mbarrier parities
-      uint32_t s_cnt[2][2] = {{0, 0}, {0, 0}}, p_cnt[2][2] = {{0, 0}, {0, 0}};
-      bool o_acc[2] = {false, false};
-      auto issue_qk = [&](int qt, int b, int ks) {
-        const uint32_t d = tmem + (qt * 2 + b) * kBN2;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t qoff = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
-          const uint32_t koff = (kk >> 2) * kKvBox2 + (kk & 3) * 32;
-          mma_ss(d, sdesc_sw128(sq + qt * kTileBytes + qoff, 16, 1024),
-                 sdesc_sw128(sk + ks * kKvTile2 + koff, 16, 1024), idesc_qk, kk > 0 ? 1u : 0u);
-        }
-        tc_commit(s_full + qt * 2 + b);
-        ++s_cnt[qt][b];
-      };
-      auto issue_pv = [&](int qt, int b, int vs) {
-        const uint32_t d = tmem + 256 + qt * 128;
-        const uint32_t a = tmem + (qt * 2 + b) * kBN2;
-#pragma unroll
-        for (int kk = 0; kk < kBN2 / 16; ++kk)
-          mma_ts(d, a + kk * 8, sdesc_sw128(sv + vs * kKvTile2 + kk * 2048, kKvBox2, 1024), idesc_pv,
-                 (o_acc[qt] || kk > 0) ? 1u : 0u);
-        o_acc[qt] = true;
-        tc_commit(o_full + qt);
-      };
-      auto modes_at = [&](const Cursor& c, int (&m)[2]) {
-        for (int qt = 0; qt < 2; ++qt) m[qt] = tile_mode2(prob.seg[c.seg], c.kt, TILE_R0(qt), nq);
-      };
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      // prologue: QK of tiles 0 and 1 into buffers 0 and 1
-      Cursor cq = cursor_at2(prob, imax, t_begin);  // cursor of the next QK tile
-      for (int it = 0; it < 2 && it < ntiles; ++it) {
-        int m[2];
-        modes_at(cq, m);
-        const int ks = it % kKS2;
-        mbar_wait(k_full + ks, (it / kKS2) & 1);
-        tc_fence_after();
-        for (int qt = 0; qt < 2; ++qt)
-          if (m[qt] != kSkip) issue_qk(qt, it & 1, ks);
-        tc_commit(k_empty + ks);
-        cursor_next2(prob, imax, cq);
-      }
-      Cursor cp = cursor_at2(prob, imax, t_begin);  // cursor of the PV tile
-      for (int it = 0; it < ntiles; ++it) {
-        const int b = it & 1, vs = it % kVS2;
-        int m[2], mn[2] = {kSkip, kSkip};
-        modes_at(cp, m);
-        const bool has_next = it + 2 < ntiles;
-        const int ksn = (it + 2) % kKS2;
-        if (has_next) modes_at(cq, mn);
-        mbar_wait(v_full + vs, (it / kVS2) & 1);
-        bool k_ready = false;
-        for (int qt = 0; qt < 2; ++qt) {
-          if (m[qt] != kSkip) {
-            mbar_wait(p_full + qt * 2 + b, p_cnt[qt][b] & 1);
-            ++p_cnt[qt][b];
-            tc_fence_after();
-            issue_pv(qt, b, vs);
-          }
-          if (qt == 1) tc_commit(v_empty + vs);
-          // QK_t(it+2) into the buffer PV_t(it) just drained (in-order tensor pipe)
-          if (has_next && mn[qt] != kSkip) {
-            if (!k_ready) {
-              mbar_wait(k_full + ksn, ((it + 2) / kKS2) & 1);
-              tc_fence_after();
-              k_ready = true;
-            }
-            issue_qk(qt, b, ksn);
-          }
-        }
-        if (has_next) {
-          tc_commit(k_empty + ksn);
-          cursor_next2(prob, imax, cq);
-        }
-        cursor_next2(prob, imax, cp);
-      }
-      tc_commit(o_done);
-    }
-  } else if (warp < kProducerWarp) {
-    // ======================================================== softmax warpgroups
-    const int qt = warp >> 2;
-    const int quad = warp & 3;
-    const int row = TILE_R0(qt) + quad * 32 + lane;
-    const int qhead = TILE_HEAD(qt);
-    const uint32_t t_lane = static_cast<uint32_t>(quad * 32) << 16;
-    const uint32_t tO = tmem + t_lane + 256 + qt * 128;
-    const float sl2 = P.scale_log2;
-    const float2 sl2v = make_float2(sl2, sl2);
-    float m_ref = -INFINITY;
-    float l = 0.f;
-    uint32_t cnt = 0;                 // PV_t issued so far (o_full parity)
-    uint32_t bcnt[2] = {0, 0};        // uses of S buffer b (s_full parity)
-    Cursor cur = cursor_at2(prob, imax, t_begin);
-    uint32_t sr[2][32];
-    uint32_t pk[2][16];
-    for (int it = 0; it < ntiles; ++it, cursor_next2(prob, imax, cur)) {
-      const AttnSeg sg = prob.seg[cur.seg];
-      const int mode = tile_mode2(sg, cur.kt, TILE_R0(qt), nq);
-      if (mode == kSkip) continue;
-      const int b = it & 1;
-      const uint32_t tS = tmem + t_lane + (qt * 2 + b) * kBN2;
-      mbar_wait(s_full + qt * 2 + b, bcnt[b] & 1);
-      ++bcnt[b];
-      tc_fence_after();
-      auto load_s = [&]() {
-        tmem_ld32(tS, sr[0]);
-        tmem_ld32(tS + 32, sr[1]);
-        tmem_wait_ld();
-      };
-      auto chunk_max = [&](int c, float (&mxp)[8]) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          const int t = (j / 2) & 7;
-          mxp[t] = fmaxf(mxp[t], fmaxf(__uint_as_float(sr[c][j]), __uint_as_float(sr[c][j + 1])));
-        }
-      };
-      auto chunk_exp = [&](int c, float2 negm, bool emu) {  // in place: sr[c] := p
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float2 x2 = __ffma2_rn(
-              make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1])), sl2v, negm);
-          float2 p2;
-          if (kEmu > 0 && emu && emu_slot(j, kEmu))
-            p2 = exp2_poly2(x2);
-          else
-            p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));  // -inf -> 0
-          sr[c][2 * j] = __float_as_uint(p2.x);
-          sr[c][2 * j + 1] = __float_as_uint(p2.y);
-        }
-      };
-      auto chunk_pack = [&](int c, float2 (&sacc)[4]) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float2 p2 = make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1]));
-          sacc[j & 3] = __fadd2_rn(sacc[j & 3], p2);
-          __nv_bfloat162 bb = __floats2bfloat162_rn(p2.x, p2.y);
-          pk[c][j] = *reinterpret_cast<uint32_t*>(&bb);
-        }
-      };
-      auto exp_pack_all = [&](float2 negm, bool emu, float2 (&sacc)[4]) {
-        chunk_exp(0, negm, emu);
-        chunk_exp(1, negm, emu);
-        chunk_pack(0, sacc);
-        chunk_pack(1, sacc);
-      };
-      float alpha = 1.f;
-      bool rescale = false;
-      float mxp[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
-      float2 sacc[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
-      bool done = false;
-      load_s();
-      if (mode == kFull && m_ref != -INFINITY) {
-        const float2 negm = make_float2(-m_ref, -m_ref);
-        chunk_max(0, mxp);
-        chunk_max(1, mxp);
-        exp_pack_all(negm, true, sacc);
-        const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
-                               fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
-        done = !(mx * sl2 > m_ref + 8.f);
-        if (!done) {
-#pragma unroll
-          for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
-          load_s();
-        }
-      } else if (mode == kPart) {
-        const int k0 = cur.kt * kBN2;
-        int lim = sg.len - k0;
-        if (sg.causal) lim = min(lim, row - k0 + 1);
-#pragma unroll
-        for (int c = 0; c < 2; ++c)
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (c * 32 + j >= lim) sr[c][j] = __float_as_uint(-INFINITY);
-      }
-      if (!done) {
-        chunk_max(0, mxp);
-        chunk_max(1, mxp);
-        const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
-                               fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
-        const float m_new = fmaxf(m_ref, mx * sl2);
-        if (m_new > m_ref + 8.f) {
-          alpha = exp2f(m_ref - m_new);
-          m_ref = m_new;
-          rescale = true;
-        }
-        const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
-        exp_pack_all(make_float2(-m_use, -m_use), mode == kFull, sacc);
-      }
-      tmem_st16(tS, pk[0]);
-      tmem_st16(tS + 16, pk[1]);
-      const float2 sum2 = __fadd2_rn(__fadd2_rn(sacc[0], sacc[1]), __fadd2_rn(sacc[2], sacc[3]));
-      l = l * alpha + (sum2.x + sum2.y);
-      if (rescale && cnt > 0) {
-        mbar_wait(o_full + qt, (cnt - 1) & 1);  // PV_t of the previous tile has landed
-        tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t o[32];
-          tmem_ld32(tO + 32 * c, o);
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-          tmem_st32(tO + 32 * c, o);
-        }
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(p_full + qt * 2 + b);
-      ++cnt;
-    }
-    // ---- epilogue: O / l, lse.  With S double-buffered, PV(n-1) and PV(n) may both be in
-    // flight here, which a parity wait on o_full cannot disambiguate: wait for the one-shot
-    // barrier the MMA warp commits after its last instruction instead.
-    mbar_wait(o_done, 0);
-    tc_fence_after();
-    const bool valid_row = row < nq;
-    const float inv = (l > 0.f) ? 1.f / l : 0.f;
-    const long long obase = static_cast<long long>(split) * prob.split_stride_out +
-                            static_cast<long long>(row) * prob.ldo + qhead * kHeadDim;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t o[32];
-      if (cnt > 0) {
-        tmem_ld32(tO + 32 * c, o);
-        tmem_wait_ld();
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) o[j] = 0u;
-      }
-      if (valid_row) {
-        if (prob.out_f32) {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(prob.out) + obase + 32 * c);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            dst[j] = make_float4(__uint_as_float(o[4 * j]) * inv, __uint_as_float(o[4 * j + 1]) * inv,
-                                 __uint_as_float(o[4 * j + 2]) * inv, __uint_as_float(o[4 * j + 3]) * inv);
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(prob.out) + obase + 32 * c);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            uint32_t w[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              __nv_bfloat162 bb = __floats2bfloat162_rn(__uint_as_float(o[8 * j + 2 * e]) * inv,
-                                                        __uint_as_float(o[8 * j + 2 * e + 1]) * inv);
-              w[e] = *reinterpret_cast<uint32_t*>(&bb);
-            }
-            dst[j] = make_uint4(w[0], w[1], w[2], w[3]);
-          }
-        }
-      }
-    }
-    if (valid_row && prob.lse) {
-      const float lse = (l > 0.f) ? (m_ref + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
-      prob.lse[static_cast<long long>(split) * prob.split_stride_lse +
-               static_cast<long long>(row) * prob.ld_lse + qhead] = lse;
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == kMmaWarp) tmem_dealloc(tmem, kTmemCols);
-#undef TILE_R0
-#undef TILE_HEAD
-}
-
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -2200,36 +762,35 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
     if (err) *err = "attention: bad problem count or head counts";
     return cudaErrorInvalidValue;
   }
-  static AttnParams P;  // large; filled per launch (launch copies params)
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
+  // Per call (reentrant: the reference's operators are called from H host threads at once,
+  // simhost.cpp:458-470); the launch copies the parameter block.
+  AttnParams P;
   std::memset(&P, 0, sizeof(P));
   P.hq = hq;
   P.hkv = hkv;
   P.scale_log2 = (1.0f / sqrtf(static_cast<float>(dh))) * 1.4426950408889634f;
-  // kernel variants (SPAVA_ATTN_VARIANT): family 0 = ping-pong (2 Q tiles per CTA, 320
-  // threads), family 1 = one Q tile per CTA with double-buffered S (192 threads).
+  // kernel variants (spava_debug_attn_variant / SPAVA_ATTN_VARIANT, dev A/B only): all are
+  // the ping-pong kernel (2 Q tiles per CTA, 320 threads) with different template switches.
   using KFn = void (*)(AttnParams);
-  struct Var { KFn fn; uint32_t smem; int threads; int family; };
+  struct Var { KFn fn; uint32_t smem; int threads = kThreads; };
   static const Var variants[] = {
-      {attn_fwd_kernel<0, 2, false, true, false>, Smem<2>::bytes, kThreads, 0},  // 0 production
-      {attn_fwd1_kernel<0, true>, Smem1::bytes, kThreads1, 1},            // 1 single tile, S x2
-      {attn_fwd_kernel<0, 2, true, true>, Smem<2>::bytes, kThreads, 0},   // 2 14 + cycle counters
-      {attn_fwd1_kernel<4, true>, Smem1::bytes, kThreads1, 1},            // 3 1 + 25% FMA exp2
-      {attn_fwd_kernel<4, 2, false, true>, Smem<2>::bytes, kThreads, 0},  // 4 14 + 25% FMA exp2
-      {attn_fwd1_kernel<2, true>, Smem1::bytes, kThreads1, 1},            // 5 1 + 12.5% FMA exp2
-      {attn_fwd_kernel<0, 2>, Smem<2>::bytes, kThreads, 0},               // 6 14 without the
-                                                                          //   one-chunk-behind pack
-      {attn_fwd2_kernel<0>, Smem2::bytes, kThreads, 2},                   // 7 64-key tiles, S x2
-      {attn_fwd2_kernel<2>, Smem2::bytes, kThreads, 2},                   // 8 7 + 25% FMA exp2
-      {attn_fwd2_kernel<1>, Smem2::bytes, kThreads, 2},                   // 9 7 + 12.5% FMA exp2
-      {attn_fwd3_kernel<0>, Smem3::bytes, kThreads3, 1},                  // 10 1 + column-split softmax
-      {attn_fwd3_kernel<4>, Smem3::bytes, kThreads3, 1},                  // 11 10 + 25% FMA exp2
-      {attn_fwd4_kernel<0>, Smem<2>::bytes, kThreads, 0},                 // 12 0 + split QK / P halves
-      {attn_fwd4_kernel<4>, Smem<2>::bytes, kThreads, 0},                 // 13 12 + 25% FMA exp2
-      {attn_fwd_kernel<0, 2, false, true, true>, Smem<2>::bytes, kThreads, 0}};   // 14 0 + speculative
-                                                                                  //  stale-max pass
+      {attn_fwd_kernel<0, 2, false, true, false, 4>, Smem<2>::bytes},  // 0 production: P in 4 key ranges
+      {attn_fwd_kernel<0, 2, true, true, false, 4>, Smem<2>::bytes},   // 1 0 + cycle counters
+      {attn_fwd_kernel<0, 2, false, true, false, 1>, Smem<2>::bytes},  // 2 round-1 kernel (P whole)
+      {attn_fwd_kernel<0, 2, false, true, false, 2>, Smem<2>::bytes},  // 3 P in 2 key ranges
+      {attn_fwd_kernel<4, 2, false, true, false, 4>, Smem<2>::bytes},  // 4 0 + 25% FMA exp2
+      {attn_fwd_kernel<2, 2, false, true, false, 4>, Smem<2>::bytes},  // 5 0 + 12.5% FMA exp2
+      {attn_fwd_kernel<0, 3, false, true, false, 4>, Smem<3>::bytes},  // 6 0 + 3-deep K ring
+      {attn_fwd_kernel<0, 2, false, true, true, 1>, Smem<2>::bytes},   // 7 speculative stale max
+      {attn_fwd_kernel<0, 2, false, true, false, 4, 224>, Smem<2>::bytes, 384},  // 8 0 + setmaxnreg
+      {attn_fwd_kernel<4, 2, false, true, false, 4, 224>, Smem<2>::bytes, 384},  // 9 8 + 25% FMA exp2
+      {attn_fwd_kernel<2, 2, false, true, false, 4, 224>, Smem<2>::bytes, 384},  // 10 8 + 12.5% FMA exp2
+      {attn_fwd_kernel<0, 2, false, true, false, 4, 0, true>, Smem<2>::bytes},    // 11 0 + exp phases alternate
+      {attn_fwd_kernel<0, 2, false, true, false, 4, 0, false, true>, Smem<2>::bytes},  // 12 0 + split S load
+      {attn_fwd_kernel<0, 2, false, true, false, 4, 0, true, true>, Smem<2>::bytes},   // 13 11 + 12
+      {attn_fwd_kernel<4, 2, false, true, false, 4, 224, true, true>, Smem<2>::bytes, 384}};  // 14 13 + setmaxnreg + 25% FMA exp2
   constexpr int kNumVar = sizeof(variants) / sizeof(variants[0]);
+  static_assert(kNumVar <= 32, "attr mask");
   static const int env_sel = [] {
     const char* e = getenv("SPAVA_ATTN_VARIANT");
     const int v = e ? atoi(e) : 0;
@@ -2238,7 +799,7 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
   const int forced = g_attn_variant.load();
   const int vsel = (forced >= 0 && forced < kNumVar) ? forced : env_sel;
   const Var& var = variants[vsel];
-  const int rows_per_cta = var.family == 1 ? kBlockM : kTilesPerCta * kBlockM;
+  constexpr int rows_per_cta = kTilesPerCta * kBlockM;
   int work = 0;
   int np = 0;
   for (int i = 0; i < nprob; ++i) {
@@ -2251,7 +812,7 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
     AttnProb& p = P.prob[np];
     p.nq = v.nq;
     p.nseg = v.nseg;
-    p.head_pair = (var.family != 1 && v.nq <= kBlockM && (hq / hkv) % 2 == 0) ? 1 : 0;
+    p.head_pair = (v.nq <= kBlockM && (hq / hkv) % 2 == 0) ? 1 : 0;
     p.units = p.head_pair ? 1 : (v.nq + rows_per_cta - 1) / rows_per_cta;
     p.splits = v.splits;
     p.work_begin = work;
@@ -2271,11 +832,10 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
         if (err) *err = "attention: causal segment longer than the query";
         return cudaErrorInvalidValue;
       }
-      const int kv_box = var.family == 2 ? kBN2 : kBlockN;
       if (!make_tmap(&P.tmap[np][1 + 2 * s], v.seg[s].k, v.seg[s].len,
-                     static_cast<long long>(hkv) * dh, v.seg[s].ld, err, kv_box) ||
+                     static_cast<long long>(hkv) * dh, v.seg[s].ld, err, kBlockN) ||
           !make_tmap(&P.tmap[np][2 + 2 * s], v.seg[s].v, v.seg[s].len,
-                     static_cast<long long>(hkv) * dh, v.seg[s].ld, err, kv_box))
+                     static_cast<long long>(hkv) * dh, v.seg[s].ld, err, kBlockN))
         return cudaErrorInvalidValue;
     }
     work += p.units * (p.head_pair ? hq / 2 : hq) * p.splits;
@@ -2284,15 +844,12 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
   P.nprob = np;
   P.total_work = work;
   if (work == 0) return cudaSuccess;
-  static bool attr_set[kNumVar] = {};
+  static std::atomic<uint32_t> attr_set[kMaxDevices] = {};
   const KFn fn = var.fn;
   const uint32_t smem_bytes = var.smem;
-  if (!attr_set[vsel]) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem_bytes));
-    if (e != cudaSuccess) return e;
-    attr_set[vsel] = true;
-  }
+  if (cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), static_cast<int>(smem_bytes), attr_set, vsel);
+      e != cudaSuccess)
+    return e;
   fn<<<work, var.threads, smem_bytes, stream>>>(P);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess && err) {

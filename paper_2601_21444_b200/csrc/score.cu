@@ -576,13 +576,10 @@ cudaError_t launch_score_exact2(int nblk, const void* q, long long ldq, int n_t,
   }
   const size_t stat_smem = static_cast<size_t>(kColStatBytes) * hq * n_t;
   if (softmax && stat_smem <= 96 * 1024) {
-    static size_t attr = 0;
-    if (stat_smem > attr) {
-      cudaError_t e = cudaFuncSetAttribute(colsum_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(96 * 1024));
-      if (e != cudaSuccess) return e;
-      attr = 96 * 1024;
-    }
+    static std::atomic<uint32_t> attr[kMaxDevices] = {};
+    if (cudaError_t e = smem_optin(reinterpret_cast<const void*>(colsum_kernel<true>), 96 * 1024, attr, 0);
+        e != cudaSuccess)
+      return e;
     colsum_kernel<true><<<dim3((l_b + 31) / 32, nblk), kColWarps * 32, stat_smem, stream>>>(a);
   } else {
     colsum_kernel<false><<<dim3((l_b + 31) / 32, nblk), kColWarps * 32, 0, stream>>>(a);

@@ -277,14 +277,11 @@ cudaError_t launch_score_fast2(int nblk, const void* q, long long ldq, int n_t,
   a.part = static_cast<float2*>(ws);
   a.lse2 = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) +
                                     ((2ull * hq * n_t * a.ntiles * sizeof(float2) + 255) & ~255ull));
-  static bool attr = false;
-  if (!attr) {
-    for (auto fn : {score_fast_kernel<0>, score_fast_kernel<1>}) {
-      cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(FSmem::bytes));
-      if (e != cudaSuccess) return e;
-    }
-    attr = true;
+  static std::atomic<uint32_t> attr[kMaxDevices] = {};
+  for (int v = 0; v < 2; ++v) {
+    const void* fn = v ? reinterpret_cast<const void*>(score_fast_kernel<1>)
+                       : reinterpret_cast<const void*>(score_fast_kernel<0>);
+    if (cudaError_t e = smem_optin(fn, static_cast<int>(FSmem::bytes), attr, v); e != cudaSuccess) return e;
   }
   const dim3 grid(a.ntiles, nblk);
   score_fast_kernel<0><<<grid, kFThreads, FSmem::bytes, stream>>>(a);

@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -14,6 +15,7 @@ constexpr int kHeadDim = 128;       // dh (Qwen2.5-VL 3B/7B)
 constexpr int kBlockM = 128;        // query rows per Q tile (TMEM lanes)
 constexpr int kBlockN = 128;        // keys per KV tile
 constexpr int kTilesPerCta = 2;     // two Q tiles share every K/V tile (ping-pong softmax)
+constexpr int kMaxDevices = 64;    // per-device caches of kernel attributes
 constexpr int kMaxSegs = 5;         // [anchor | passing lo-round | passing hi-round | own]
                                      // (+1: a row chunk splits own into visible prefix + causal)
 constexpr int kMaxProbs = 3;        // attention problems fused into one launch
@@ -49,6 +51,19 @@ struct __align__(64) AttnParams {
   int total_work;
   float scale_log2;  // (1/sqrt(dh)) * log2(e)
 };
+
+// Opt kernel `fn` into `bytes` of dynamic shared memory on the current device, once per
+// (device, bit of `mask`): the attribute is per device context.  Thread-safe (a race only
+// repeats the idempotent call).
+inline cudaError_t smem_optin(const void* fn, int bytes, std::atomic<uint32_t>* mask, uint32_t bit) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const bool cached = dev >= 0 && dev < kMaxDevices;
+  if (cached && (mask[dev].load(std::memory_order_acquire) & (1u << bit))) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && cached) mask[dev].fetch_or(1u << bit, std::memory_order_release);
+  return e;
+}
 
 // Host launch helpers (attention.cu)
 struct SegView {

@@ -29,8 +29,8 @@ fl2 = 2.0*n*n*hq*128
 # fully visible (non-causal) 16K x 16K
 ms3 = t(lambda: spava.attention(q, [dict(k=k, v=v)], hq, hkv), 5)
 fl3 = 4.0*lb*lb*hq*128
-print(f"variant {os.environ.get('SPAVA_ATTN_VARIANT','2')}: block {ms:.3f} ms {fl/ms/1e9:.0f} TF/s | dense causal {ms2:.3f} ms {fl2/ms2/1e9:.0f} TF/s | full {ms3:.3f} ms {fl3/ms3/1e9:.0f} TF/s")
-if os.environ.get('SPAVA_ATTN_VARIANT') == '2':
+print(f"variant {os.environ.get('SPAVA_ATTN_VARIANT','0')}: block {ms:.3f} ms {fl/ms/1e9:.0f} TF/s | dense causal {ms2:.3f} ms {fl2/ms2/1e9:.0f} TF/s | full {ms3:.3f} ms {fl3/ms3/1e9:.0f} TF/s")
+if os.environ.get('SPAVA_ATTN_VARIANT') == '1':
     import ctypes as C
     L = spava.lib()
     buf = (C.c_uint64 * 16)()
@@ -43,4 +43,4 @@ if os.environ.get('SPAVA_ATTN_VARIANT') == '2':
     print({k: v for k, v in d.items()})
     print('per softmax warp-tile: wait_s %.0f  body %.0f cycles; mma per tile-pair total %.0f, wait_p %.0f wait_k %.0f wait_v %.0f' % (
         d['sm_wait_s']/tiles, d['sm_body']/tiles, d['mma_total']/(tiles/8), d['mma_wait_p']/(tiles/8), d['mma_wait_k']/(tiles/8), d['mma_wait_v']/(tiles/8)))
-    print('softmax phases per warp-tile: ld %.0f  max %.0f  exp+st %.0f  (rescale+)wait_st/arrive %.0f' % (buf[8]/tiles, buf[9]/tiles, buf[11]/tiles, buf[12]/tiles))
+    print('softmax phases per warp-tile: ld %.0f  ld+mask+max %.0f  exp+pack+st %.0f (of which mid-tile wait_st/arrive %.0f)  tail wait_st/arrive %.0f' % (buf[9]/tiles, buf[8]/tiles, buf[10]/tiles, buf[11]/tiles, buf[12]/tiles))
