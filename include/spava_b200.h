@@ -344,6 +344,10 @@ int spava_debug_attn_prof(uint64_t* out16);
 /* Development: force an attention kernel variant for this process (-1 = default or the
  * SPAVA_ATTN_VARIANT environment variable); lets the tests cover every variant.        */
 int spava_debug_attn_variant(int variant);
+/* Development: 1 = the final query merge runs as trailing CTAs of the last stage launch
+ * (default; peer fabric: they wait for the peers' qpartial flags in-kernel), 0 = a separate
+ * merge launch after a stream wait, -1 = default / SPAVA_FUSED_MERGE.                     */
+int spava_debug_fused_merge(int on);
 
 /* Number of kernels the library launched since process start (for bench's
  * gpu_launches claim). */

@@ -32,6 +32,7 @@
 #include <cstring>
 #include <mutex>
 
+#include "fabric_dev.cuh"
 #include "ptx.cuh"
 #include "spava_internal.h"
 
@@ -170,6 +171,11 @@ __global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
   uint64_t* o_full = p_full + 8;              // [2] PV_t complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
 
+  // trailing CTAs of a stage launch (peer fabric): the receive-side query merge
+  if (P.job.ctas > 0 && static_cast<int>(blockIdx.x) >= P.total_work) {
+    merge_job(P.job, static_cast<int>(blockIdx.x) - P.total_work, reinterpret_cast<float*>(smem));
+    return;
+  }
   const int warp = warp_id();
   const int lane = lane_id();
   long long pr[14] = {};
@@ -753,7 +759,7 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, long long rows, long long 
 std::atomic<int> g_attn_variant{-1};  // -1: SPAVA_ATTN_VARIANT / default
 
 cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, int dh,
-                             cudaStream_t stream, std::string* err) {
+                             cudaStream_t stream, std::string* err, const MergeJob* job) {
   if (dh != kHeadDim) {
     if (err) *err = "attention: only dh == 128 is implemented";
     return cudaErrorInvalidValue;
@@ -843,14 +849,23 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
   }
   P.nprob = np;
   P.total_work = work;
-  if (work == 0) return cudaSuccess;
+  if (job && job->ctas > 0) {
+    if (job->nwait < 0 || job->nwait > kMaxPeers || job->mp.nparts < 1 || job->mp.nparts > kMaxMergeParts ||
+        job->mp.dh > 1024 || job->ctas > 64) {
+      if (err) *err = "attention: bad merge job";
+      return cudaErrorInvalidValue;
+    }
+    P.job = *job;
+  }
+  const int grid = work + P.job.ctas;
+  if (grid == 0) return cudaSuccess;
   static std::atomic<uint32_t> attr_set[kMaxDevices] = {};
   const KFn fn = var.fn;
   const uint32_t smem_bytes = var.smem;
   if (cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), static_cast<int>(smem_bytes), attr_set, vsel);
       e != cudaSuccess)
     return e;
-  fn<<<work, var.threads, smem_bytes, stream>>>(P);
+  fn<<<grid, var.threads, smem_bytes, stream>>>(P);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess && err) {
     cudaFuncAttributes fa{};

@@ -207,6 +207,7 @@ struct spava_host {
   float* qsplit_out = nullptr;
   float* qsplit_lse = nullptr;
   int32_t* status = nullptr;
+  unsigned* ctr = nullptr;  // [4] zeroed device counters of the peer-flag raises (rounds 0..2)
   void* base = nullptr;
   cudaEvent_t ev[6] = {};  // pass1_ready, pass2_ready, q_ready, pass1_done, pass2_done, q_done
   // scoring runs on a high-priority side stream forked from the caller's stream, so the
@@ -336,10 +337,10 @@ int cfg_check(const spava_layer_cfg* c, spava_plan* plan) {
 
 // -------------------------------------------------------- op wrappers
 int attention_impl(const ProbView* pv, int np, int hq, int hkv, int dh, cudaStream_t st,
-                   spava_host* H = nullptr) {
+                   spava_host* H = nullptr, const MergeJob* job = nullptr) {
   std::string err;
   const size_t t0 = mark(H, st);
-  cudaError_t e = launch_attention(pv, np, hq, hkv, dh, st, &err);
+  cudaError_t e = launch_attention(pv, np, hq, hkv, dh, st, &err, job);
   if (e != cudaSuccess)
     return fail(e == cudaErrorInvalidValue ? SPAVA_EINVAL : SPAVA_ECUDA,
                 err.empty() ? std::string("attention: ") + cudaGetErrorString(e) : err);
@@ -398,6 +399,17 @@ int peer_signal(spava_fabric* F, cudaStream_t s, int round) {
   CU_TRY(peer_flags_store(s, F->flag_tmp, n, F->epoch));
   if (n > 0) ++g_launches;
   return SPAVA_OK;
+}
+
+// the producing kernel raises arrive[round][me] in every peer itself (last CTA, release)
+FlagRaise peer_raise(spava_host* H, int round) {
+  spava_fabric* F = H->fab;
+  FlagRaise f{};
+  for (int q = 0; q < F->world; ++q)
+    if (q != F->rank) f.addr[f.n++] = arrive_flag(F->at_peer(q, F->shared.flags), round, F->rank);
+  f.value = F->epoch;
+  f.counter = H->ctr + round;
+  return f;
 }
 
 // the stream waits until every peer's round-`round` slot of this epoch is here
@@ -485,9 +497,10 @@ int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record,
     // is read as exactly l_p rows, so a short selection is reported (status bit 2)
     jobs[r] = SelectPackJob{H->scores[r], p.l_a + vs[r] * p.l_b, row_ptr(b.k, krow, dk), row_ptr(b.v, krow, dk),
                             idx_out, k_out, v_out, cnt_out, &peers[r], vs[r] < p.virtual_hosts - 1};
+    if (F.peer && p.l_p > 0) jobs[r].fr = peer_raise(H, r);  // the gather's last CTA signals
   }
   auto finish = [&](int r) -> int {  // after round r's select + pack
-    if (F.peer) ST_TRY(peer_signal(H->fab, st, r));
+    if (F.peer && p.l_p == 0) ST_TRY(peer_signal(H->fab, st, r));
     if (b.sel && p.l_p > 0)
       CU_TRY(cudaMemcpyAsync(b.sel + r * p.l_p, jobs[r].idx, sizeof(int32_t) * p.l_p,
                              cudaMemcpyDeviceToDevice, st));
@@ -575,8 +588,8 @@ int phase_query(spava_host* H, const HostBufs& b, cudaStream_t st, bool record) 
           mp.peer_lse[mp.npeer] = F.at_peer(q, dst_lse);
           ++mp.npeer;
         }
+    if (F.peer) mp.fr = peer_raise(H, 2);  // the split merge's last CTA signals qpartial
     ST_TRY(merge_impl(mp, st, H));
-    if (F.peer) ST_TRY(peer_signal(H->fab, st, 2));
   }
   if (record) CU_TRY(cudaEventRecord(H->ev[2], st));
   return SPAVA_OK;
@@ -657,19 +670,52 @@ int phase_stage1(spava_host* H, const HostBufs& b, cudaStream_t st) {
   return attention_impl(pv, H->fab->plan.l_a > 0 ? 2 : 1, c.hq, c.hkv, c.dh, st, H);
 }
 
-int phase_stage2(spava_host* H, const HostBufs& b, cudaStream_t st) {
+MergeParams query_merge_params(spava_host* H, const HostBufs& b);
+
+// The final query merge (mha_merge over the H host partials, simhost.cpp:404-426) as the
+// trailing CTAs of the last stage launch: with peers (peer fabric) they first wait for
+// every peer's qpartial arrive flag, so no separate merge launch or stream wait remains.
+// Same arithmetic as merge_kernel (fabric_dev.cuh).  SPAVA_FUSED_MERGE=0: separate launch.
+std::atomic<int> g_fused_merge{-1};  // -1: SPAVA_FUSED_MERGE (default 1); dev override
+bool fused_merge_enabled() {
+  static const int v = [] {
+    const char* e = getenv("SPAVA_FUSED_MERGE");
+    return e ? atoi(e) : 1;
+  }();
+  const int o = g_fused_merge.load();
+  return (o >= 0 ? o : v) != 0;
+}
+
+MergeJob query_merge_job(spava_host* H, const HostBufs& b) {
+  spava_fabric* F = H->fab;
+  MergeJob job{};
+  job.mp = query_merge_params(H, b);
+  if (F->peer)
+    for (int q = 0; q < F->world; ++q)
+      if (q != F->rank) job.wait[job.nwait++] = arrive_flag(F->shared.flags, 2, q);
+  job.epoch = F->epoch;
+  job.ctas = 64;  // fills SMs as the last attention wave drains
+  return job;
+}
+
+int phase_stage2(spava_host* H, const HostBufs& b, cudaStream_t st, bool with_merge = false) {
   const spava_layer_cfg& c = H->fab->cfg;
   ProbView pv = block_problem(H, b, 1);
-  return attention_impl(&pv, 1, c.hq, c.hkv, c.dh, st, H);
+  if (!with_merge) return attention_impl(&pv, 1, c.hq, c.hkv, c.dh, st, H);
+  const MergeJob job = query_merge_job(H, b);
+  return attention_impl(&pv, 1, c.hq, c.hkv, c.dh, st, H, &job);
 }
 
 // stage 1 and stage 2 in ONE launch (block hi, block lo, anchor): once both passing rounds
 // are in, the two block problems fill the GPU together -- at H > 1 a block has only
 // l_b / 256 row units per head, and separate launches leave most SMs idle in the tail.
-int phase_stage12(spava_host* H, const HostBufs& b, cudaStream_t st) {
+int phase_stage12(spava_host* H, const HostBufs& b, cudaStream_t st, bool with_merge = false) {
   const spava_layer_cfg& c = H->fab->cfg;
   ProbView pv[3] = {block_problem(H, b, 1), block_problem(H, b, 0), anchor_problem(H, b)};
-  return attention_impl(pv, H->fab->plan.l_a > 0 ? 3 : 2, c.hq, c.hkv, c.dh, st, H);
+  const int np = H->fab->plan.l_a > 0 ? 3 : 2;
+  if (!with_merge) return attention_impl(pv, np, c.hq, c.hkv, c.dh, st, H);
+  const MergeJob job = query_merge_job(H, b);
+  return attention_impl(pv, np, c.hq, c.hkv, c.dh, st, H, &job);
 }
 
 // H > 1 runs the merged launch (measured on one B200, C1 sim: 0.365 -> 0.334 ms per host at
@@ -682,7 +728,7 @@ bool merged_stages() {
   return v != 0;
 }
 
-int phase_merge(spava_host* H, const HostBufs& b, cudaStream_t st) {
+MergeParams query_merge_params(spava_host* H, const HostBufs& b) {
   const spava_layer_cfg& c = H->fab->cfg;
   const spava_plan& p = H->fab->plan;
   const long long dq = static_cast<long long>(c.hq) * c.dh;
@@ -701,7 +747,11 @@ int phase_merge(spava_host* H, const HostBufs& b, cudaStream_t st) {
   mp.ld_dst = dq;
   mp.dst_f32 = 0;
   mp.status = H->status;
-  return merge_impl(mp, st, H);
+  return mp;
+}
+
+int phase_merge(spava_host* H, const HostBufs& b, cudaStream_t st) {
+  return merge_impl(query_merge_params(H, b), st, H);
 }
 
 int nccl_round(spava_fabric* F, Exchange* ex, int r) {
@@ -747,6 +797,11 @@ uint64_t spava_kernel_launches(void) { return g_launches.load(); }
 
 int spava_debug_attn_prof(uint64_t* out16) {
   attn_prof_read(reinterpret_cast<unsigned long long*>(out16));
+  return SPAVA_OK;
+}
+
+int spava_debug_fused_merge(int on) {
+  g_fused_merge.store(on < 0 ? -1 : (on ? 1 : 0));
   return SPAVA_OK;
 }
 
@@ -1304,6 +1359,7 @@ int spava_host_create(spava_fabric* F, int h, spava_host** out) {
   H->qsplit_out = reinterpret_cast<float*>(b); b += qo;
   H->qsplit_lse = reinterpret_cast<float*>(b); b += ql;
   H->status = reinterpret_cast<int32_t*>(b);
+  H->ctr = reinterpret_cast<unsigned*>(b + 64);
   const int rc = host_init_streams(H);
   if (rc != SPAVA_OK) {
     spava_host_destroy(H);  // releases whatever was created before the failure
@@ -1383,8 +1439,9 @@ inline int chunk_of(int which, int k) { return which == 0 ? k : spava_host::kCop
 
 // stage 1 / stage 2 as row chunks (copy pipeline) or whole blocks; events are indexed by
 // processing position
-int stage_chunks(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdges& cp, int which) {
-  if (!cp.on) return which == 0 ? phase_stage1(H, b, st) : phase_stage2(H, b, st);
+int stage_chunks(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdges& cp, int which,
+                 bool with_merge = false) {
+  if (!cp.on) return which == 0 ? phase_stage1(H, b, st) : phase_stage2(H, b, st, with_merge);
   const spava_layer_cfg& c = H->fab->cfg;
   const int n = spava_host::kCopyChunks;
   for (int k = 0; k < n; ++k) {
@@ -1448,13 +1505,15 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     T(st, kCommWaitStart, "pass2", true);
     CU_TRY(cudaStreamWaitEvent(st, H->ev_sel, 0));
     T(st, kCommCompleted, "pass2", true);
+    // the merge of the query partial(s) rides in the stage-2 launch (trailing CTAs)
+    const bool fused = !cp.on && fused_merge_enabled();
     T(st, kComputeBegin, "stage2");
-    ST_TRY(stage_chunks(H, b, st, cp, 1));
+    ST_TRY(stage_chunks(H, b, st, cp, 1, fused));
     T(st, kComputeEnd, "stage2");
     T(st, kCommWaitStart, "qpartial", true);
     T(st, kCommCompleted, "qpartial", true);
     T(st, kComputeBegin, "merge");
-    ST_TRY(phase_merge(H, b, st));
+    if (!fused) ST_TRY(phase_merge(H, b, st));
     T(st, kComputeEnd, "merge");
     if (H->trace) ++H->trace_layer;
     return merged(st) == cudaSuccess ? SPAVA_OK : fail(SPAVA_ECUDA, "event record");
@@ -1484,6 +1543,8 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     ST_TRY(nccl_round(F, H->ex, 1));
     CU_TRY(cudaEventRecord(H->ev[4], cs));
   }
+  // peer fabric: the final query merge rides in the merged stage launch (receive side)
+  const bool fused_merge = F->peer && !cp.on && merged_stages() && fused_merge_enabled();
   auto query = [&]() -> int {
     T(st, kComputeBegin, "query_attn");
     if (cp.on) CU_TRY(cudaStreamWaitEvent(st, H->ev_vhi, 0));
@@ -1528,7 +1589,7 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     CU_TRY(cudaStreamWaitEvent(st, H->ev_sel, 0));
     T(st, kComputeBegin, "stage1");
     T(st, kComputeBegin, "stage2");
-    ST_TRY(phase_stage12(H, b, st));
+    ST_TRY(phase_stage12(H, b, st, fused_merge));
     T(st, kComputeEnd, "stage1");
     T(st, kComputeEnd, "stage2");
   } else {
@@ -1547,10 +1608,10 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     T(st, kComputeEnd, "stage2");
   }
   T(st, kCommWaitStart, "qpartial", true);
-  ST_TRY(wait_round(2));
+  if (!fused_merge) ST_TRY(wait_round(2));  // else: the stage launch's merge CTAs waited
   T(st, kCommCompleted, "qpartial", true);
   T(st, kComputeBegin, "merge");
-  ST_TRY(phase_merge(H, b, st));
+  if (!fused_merge) ST_TRY(phase_merge(H, b, st));
   T(st, kComputeEnd, "merge");
   if (F->peer) ST_TRY(peer_release(F, st));  // the exchange buffer of this epoch is read
   if (H->trace) ++H->trace_layer;

@@ -12,6 +12,7 @@
 // thread produces one output column.
 #include <cuda_bf16.h>
 
+#include "fabric_dev.cuh"
 #include "spava_internal.h"
 
 namespace spava {
@@ -24,58 +25,23 @@ __global__ void merge_kernel(const __grid_constant__ MergeParams p) {
   __shared__ float lse_sh;
   const int i = blockIdx.x, h = blockIdx.y, c = threadIdx.x;
   if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    // lanes own parts lane, lane+32 (kMaxMergeParts = 64)
-    float l0 = -INFINITY, l1 = -INFINITY;
-    if (lane < p.nparts) l0 = p.lse[lane][static_cast<long long>(i) * p.ld_lse + h];
-    if (lane + 32 < p.nparts) l1 = p.lse[lane + 32][static_cast<long long>(i) * p.ld_lse + h];
-    double mx = -INFINITY;
-    if (isfinite(l0)) mx = static_cast<double>(l0);
-    if (isfinite(l1)) mx = fmax(mx, static_cast<double>(l1));
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const bool ok = isfinite(mx);
-    double e0 = 0.0, e1 = 0.0;
-    if (ok) {
-      if (isfinite(l0)) e0 = exp(__dsub_rn(static_cast<double>(l0), mx));
-      if (isfinite(l1)) e1 = exp(__dsub_rn(static_cast<double>(l1), mx));
-    }
-    // denominator in part order (reference adds parts sequentially)
-    double denom = 0.0;
-    for (int q = 0; q < p.nparts; ++q) {
-      const double eq = __shfl_sync(0xffffffffu, q < 32 ? e0 : e1, q & 31);
-      denom = __dadd_rn(denom, eq);
-    }
-    if (lane < p.nparts) w[lane] = ok && isfinite(l0) ? __double2float_rn(__ddiv_rn(e0, denom)) : 0.f;
-    if (lane + 32 < p.nparts) w[lane + 32] = ok && isfinite(l1) ? __double2float_rn(__ddiv_rn(e1, denom)) : 0.f;
-    if (lane == 0) {
-      ok_sh = ok;
-      lse_sh = ok ? __double2float_rn(mx + log(denom)) : -INFINITY;
-      if (!ok && p.status) atomicOr(p.status, 4);
-    }
+    merge_weights_warp(p, i, h, w, &ok_sh, &lse_sh);
+    if (threadIdx.x == 0 && !ok_sh && p.status) atomicOr(p.status, 4);
   }
   __syncthreads();
   const long long col = static_cast<long long>(h) * p.dh + c;
-  float acc = 0.f;
-  if (ok_sh) {
-    for (int q = 0; q < p.nparts; ++q) {
-      const float wq = w[q];
-      if (wq == 0.f) continue;  // invalid part (weights of valid parts are > 0 or underflow)
-      acc = __fadd_rn(acc, __fmul_rn(wq, p.out[q][static_cast<long long>(i) * p.ld_part + col]));
-    }
-  }
-  const long long d = static_cast<long long>(i) * p.ld_dst + col;
-  if (p.dst_f32)
-    static_cast<float*>(p.dst)[d] = acc;
-  else
-    static_cast<__nv_bfloat16*>(p.dst)[d] = __float2bfloat16_rn(acc);
+  const float acc = ok_sh ? merge_column(p, w, i, col) : 0.f;
+  merge_store(p, i, col, acc);
   if (p.dst_lse && c == 0) p.dst_lse[static_cast<long long>(i) * p.hq + h] = lse_sh;
   // peer fabric: the qpartial round is this kernel's epilogue (NVLink stores into every
-  // peer's slot); only the f32 slot layout is ever published
+  // peer's slot, then the last CTA raises the round's arrive flags); only the f32 slot
+  // layout is ever published
+  const long long d = static_cast<long long>(i) * p.ld_dst + col;
   for (int q = 0; q < p.npeer; ++q) {
     static_cast<float*>(p.peer_dst[q])[d] = acc;
     if (c == 0) p.peer_lse[q][static_cast<long long>(i) * p.hq + h] = lse_sh;
   }
+  raise_when_done(p.fr, gridDim.x * gridDim.y);
 }
 
 }  // namespace
@@ -83,6 +49,8 @@ __global__ void merge_kernel(const __grid_constant__ MergeParams p) {
 cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream) {
   if (p.nparts < 1 || p.nparts > kMaxMergeParts || p.dh < 32 || p.dh > 1024) return cudaErrorInvalidValue;
   if (p.npeer < 0 || p.npeer > kMaxPeers || (p.npeer > 0 && (!p.dst_f32 || !p.dst_lse)))
+    return cudaErrorInvalidValue;
+  if (p.fr.n < 0 || p.fr.n > kMaxPeers || (p.fr.n > 0 && (!p.fr.counter || p.rows == 0)))
     return cudaErrorInvalidValue;
   if (p.rows == 0) return cudaSuccess;
   merge_kernel<<<dim3(p.rows, p.hq), p.dh, 0, stream>>>(p);

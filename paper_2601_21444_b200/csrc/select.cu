@@ -16,6 +16,7 @@
 // straight into this host's slot of the exchange buffer.
 #include <cuda_bf16.h>
 
+#include "fabric_dev.cuh"
 #include "spava_internal.h"
 
 namespace spava {
@@ -91,6 +92,7 @@ struct SelJob {
   uint4* k_out;
   uint4* v_out;
   PeerSlots peers;
+  FlagRaise fr;
   int require_full;  // a passing source: fewer than l_p keys is reported (status bit 2)
 };
 struct SelJobs {
@@ -245,27 +247,30 @@ __global__ void gather_kernel(const __grid_constant__ SelJobs J) {
   const SelJob& jb = J.j[blockIdx.y];
   const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
-  if (r >= J.l_p) return;
-  const int n = *jb.count;
-  const int32_t* idx = jb.idx;
-  const PeerSlots& peers = jb.peers;
-  const long long o = r * J.ld_out16;
-  if (lane == 0)
-    for (int q = 0; q < peers.n; ++q) {
-      static_cast<int32_t*>(peers.idx[q])[r] = idx[r];
-      if (r == 0) *static_cast<int32_t*>(peers.cnt[q]) = n;
-    }
-  const long long src = r < n ? static_cast<long long>(idx[r] - jb.global_offset) * J.ld16 : 0;
-  for (int c = lane; c < J.w16; c += 32) {
-    const uint4 kx = r < n ? jb.k[src + c] : make_uint4(0, 0, 0, 0);
-    const uint4 vx = r < n ? jb.v[src + c] : make_uint4(0, 0, 0, 0);
-    jb.k_out[o + c] = kx;
-    jb.v_out[o + c] = vx;
-    for (int q = 0; q < peers.n; ++q) {
-      static_cast<uint4*>(peers.k[q])[o + c] = kx;
-      static_cast<uint4*>(peers.v[q])[o + c] = vx;
+  if (r < J.l_p) {  // (no early exit: the peer flag raise below synchronises the CTA)
+    const int n = *jb.count;
+    const int32_t* idx = jb.idx;
+    const PeerSlots& peers = jb.peers;
+    const long long o = r * J.ld_out16;
+    if (lane == 0)
+      for (int q = 0; q < peers.n; ++q) {
+        static_cast<int32_t*>(peers.idx[q])[r] = idx[r];
+        if (r == 0) *static_cast<int32_t*>(peers.cnt[q]) = n;
+      }
+    const long long src = r < n ? static_cast<long long>(idx[r] - jb.global_offset) * J.ld16 : 0;
+    for (int c = lane; c < J.w16; c += 32) {
+      const uint4 kx = r < n ? jb.k[src + c] : make_uint4(0, 0, 0, 0);
+      const uint4 vx = r < n ? jb.v[src + c] : make_uint4(0, 0, 0, 0);
+      jb.k_out[o + c] = kx;
+      jb.v_out[o + c] = vx;
+      for (int q = 0; q < peers.n; ++q) {
+        static_cast<uint4*>(peers.k[q])[o + c] = kx;
+        static_cast<uint4*>(peers.v[q])[o + c] = vx;
+      }
     }
   }
+  // peer fabric: the last CTA of this block's round raises arrive[round][me] in every peer
+  raise_when_done(jb.fr, gridDim.x);
 }
 
 }  // namespace
@@ -295,10 +300,12 @@ cudaError_t launch_select_pack_n(const SelectPackJob* jobs, int n, int l_b, int 
     j.k_out = static_cast<uint4*>(s.k_out);
     j.v_out = static_cast<uint4*>(s.v_out);
     if (s.peers) j.peers = *s.peers;
+    j.fr = s.fr;
     j.require_full = s.require_full;
     gather = gather && s.k_out && s.v_out;
-    if (!(l_p > 0 && s.k_out && s.v_out) && j.peers.n > 0)
+    if (!(l_p > 0 && s.k_out && s.v_out) && (j.peers.n > 0 || j.fr.n > 0))
       return cudaErrorInvalidValue;  // a peer slot is only published through the gather
+    if (j.fr.n < 0 || j.fr.n > kMaxPeers || (j.fr.n > 0 && !j.fr.counter)) return cudaErrorInvalidValue;
   }
   if (l_b <= kSelSmall * kItems)
     select_kernel<kSelSmall><<<n, kSelSmall, 0, stream>>>(J);

@@ -42,6 +42,46 @@ struct AttnProb {
   long long split_stride_lse;
 };
 
+// ---------------------------------------------------------------- peer fabric / merge
+constexpr int kMaxPeers = 7;  // peers of one rank (8 GPUs per box)
+// Producer epilogue (peer fabric): once every CTA of a group has stored its part of a slot
+// into the peers' buffers, the last one raises these flags (fabric_dev.cuh).
+struct FlagRaise {
+  uint32_t* addr[kMaxPeers];
+  int n;  // 0 = nothing to raise
+  uint32_t value;
+  unsigned* counter;  // zeroed device counter, reset by the last CTA
+};
+
+constexpr int kMaxMergeParts = 64;
+struct MergeParams {
+  const float* out[kMaxMergeParts];  // [rows][ld_part]
+  const float* lse[kMaxMergeParts];  // [rows][ld_lse]
+  int nparts;
+  int rows, hq, dh;
+  long long ld_part;
+  int ld_lse;
+  void* dst;
+  long long ld_dst;
+  int dst_f32;
+  float* dst_lse;  // nullable [rows][hq]
+  int32_t* status; // nullable; set to 1 if a row is invalid in every part
+  // peer fabric: the merged rows / lse are also stored into these peers' slots (same layout)
+  int npeer;
+  void* peer_dst[kMaxPeers];
+  float* peer_lse[kMaxPeers];
+  FlagRaise fr;  // peer fabric: raise the qpartial arrive flags once every CTA has stored
+};
+// Receive-side merge run by the trailing CTAs of a stage attention launch (peer fabric):
+// wait until every peer's qpartial flag reached `epoch`, then merge into mp.dst.
+struct MergeJob {
+  MergeParams mp;
+  const uint32_t* wait[kMaxPeers];
+  int nwait;
+  uint32_t epoch;
+  int ctas;  // 0 = no job
+};
+
 struct __align__(64) AttnParams {
   // per problem: [0] = Q, [1+2s] = K of segment s, [2+2s] = V of segment s
   CUtensorMap tmap[kMaxProbs][1 + 2 * kMaxSegs];
@@ -50,6 +90,7 @@ struct __align__(64) AttnParams {
   int hq, hkv;
   int total_work;
   float scale_log2;  // (1/sqrt(dh)) * log2(e)
+  MergeJob job;      // job.ctas trailing CTAs run the receive-side query merge
 };
 
 // Opt kernel `fn` into `bytes` of dynamic shared memory on the current device, once per
@@ -91,7 +132,7 @@ struct ProbView {
 void attn_prof_read(unsigned long long* out16);  // dev: cycle counters of variant 2
 int attn_set_variant(int v);                     // dev: -1 = env/default, else variant id
 cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, int dh,
-                             cudaStream_t stream, std::string* err);
+                             cudaStream_t stream, std::string* err, const MergeJob* job = nullptr);
 
 // 2D bf16 [rows x cols] tensor map, box 64 cols x box_rows rows, 128B swizzle
 bool make_tmap_bf16(CUtensorMap* m, const void* base, long long rows, long long cols, long long ld,
@@ -120,7 +161,6 @@ cudaError_t launch_score_fast2(int nblk, const void* q, long long ldq, int n_t,
 
 // ---------------------------------------------------------------- selection
 // peer fabric: the same slot in up to kMaxPeers other GPUs' exchange buffers (IPC-mapped)
-constexpr int kMaxPeers = 7;
 struct PeerSlots {
   void* k[kMaxPeers];
   void* v[kMaxPeers];
@@ -139,6 +179,7 @@ struct SelectPackJob {
   int32_t* count;
   const PeerSlots* peers;  // nullable
   int require_full = 0;    // passing source: count < l_p sets status bit 2
+  FlagRaise fr = {};       // peer fabric: this round's arrive flags, raised by the gather
 };
 // select + pack of 1 or 2 blocks (same l_b / l_p / widths) in one select and one gather launch
 cudaError_t launch_select_pack_n(const SelectPackJob* jobs, int n, int l_b, int l_p, long long ld, int width,
@@ -178,24 +219,6 @@ void* gemm_handle_create();
 void gemm_handle_destroy(void* h);
 
 // ---------------------------------------------------------------- merge
-constexpr int kMaxMergeParts = 64;
-struct MergeParams {
-  const float* out[kMaxMergeParts];  // [rows][ld_part]
-  const float* lse[kMaxMergeParts];  // [rows][ld_lse]
-  int nparts;
-  int rows, hq, dh;
-  long long ld_part;
-  int ld_lse;
-  void* dst;
-  long long ld_dst;
-  int dst_f32;
-  float* dst_lse;  // nullable [rows][hq]
-  int32_t* status; // nullable; set to 1 if a row is invalid in every part
-  // peer fabric: the merged rows / lse are also stored into these peers' slots (same layout)
-  int npeer;
-  void* peer_dst[kMaxPeers];
-  float* peer_lse[kMaxPeers];
-};
 cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream);
 cudaError_t launch_delay(unsigned long long ns, cudaStream_t stream);  // test: stream delay
 

@@ -370,3 +370,36 @@ def test_decoder_layer_matches_reference_math(cuda, norm):
     assert rl2 < 1.5e-2, rl2
     host.close()
     fab.close()
+
+
+def test_fused_query_merge_matches_separate_launch(cuda):
+    """f1: the final query merge rides in the stage-2 launch (trailing CTAs) -- outputs and
+    indices bit-identical to the separate merge launch, with one launch fewer per layer."""
+    import torch
+
+    from paper_2601_21444_b200 import spava
+
+    n_v, n_t, l_a, l_p, hq, hkv = 3000, 96, 40, 128, 16, 2
+    cfg = spava.LayerConfig.make(n_v, n_t, 1, l_a, l_p, hq, hkv)
+    fab = spava.Fabric(cfg, 0)
+    H = fab.host(0)
+    g = torch.Generator(device=cuda).manual_seed(7)
+    q = torch.randn(H.rows, hq * 128, device=cuda, generator=g).to(torch.bfloat16)
+    k = torch.randn(H.rows, hkv * 128, device=cuda, generator=g).to(torch.bfloat16)
+    v = torch.randn(H.rows, hkv * 128, device=cuda, generator=g).to(torch.bfloat16)
+    res = {}
+    try:
+        for fused in (0, 1):
+            spava._check(spava.lib().spava_debug_fused_merge(fused))
+            out = torch.zeros(H.rows, hq * 128, dtype=torch.bfloat16, device=cuda)
+            sel = torch.zeros(2, l_p, dtype=torch.int32, device=cuda)
+            H.layer(q, k, v, out, sel)  # warm (lazy module loads)
+            torch.cuda.synchronize()
+            n0 = spava.kernel_launches()
+            H.layer(q, k, v, out, sel)
+            torch.cuda.synchronize()
+            res[fused] = (out.clone(), sel.clone(), spava.kernel_launches() - n0)
+    finally:
+        spava._check(spava.lib().spava_debug_fused_merge(-1))
+    assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
+    assert res[1][2] == res[0][2] - 1, (res[0][2], res[1][2])

@@ -41,10 +41,15 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("world,zigzag", [(2, True), (4, True), (3, False)])
-def test_peer_fabric_inprocess_matches_local(cuda, world, zigzag):
+@pytest.mark.parametrize("world,zigzag,fused", [(2, True, "1"), (4, True, "1"), (3, False, "1"), (2, True, "0"),
+                                                (4, True, "0")])
+def test_peer_fabric_inprocess_matches_local(cuda, world, zigzag, fused):
+    """fused=1 (default): the final query merge runs as trailing CTAs of the merged stage
+    launch, waiting for the peers' qpartial flags in-kernel (receive-side merge); fused=0:
+    separate merge launch after a stream wait.  Both bit-identical to the local fabric."""
     env = _env()
     env["PEER_ZIGZAG"] = "1" if zigzag else "0"
+    env["SPAVA_FUSED_MERGE"] = fused
     r = subprocess.run([sys.executable, "-m", "tests.peer_worker", "inproc", str(world), "3"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=240)
     assert r.returncode == 0 and "PEER_OK all 3" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
