@@ -348,6 +348,10 @@ int spava_debug_attn_variant(int variant);
  * (default; peer fabric: they wait for the peers' qpartial flags in-kernel), 0 = a separate
  * merge launch after a stream wait, -1 = default / SPAVA_FUSED_MERGE.                     */
 int spava_debug_fused_merge(int on);
+/* Development: 1 = fast-mode scoring (score_mode 1) rides in the query attention launch
+ * (default: row statistics from its softmax + trailing column-sum CTAs), 0 = the standalone
+ * three-launch tensor-core scorer, -1 = default / SPAVA_FUSED_SCORE.                     */
+int spava_debug_fused_score(int on);
 
 /* Number of kernels the library launched since process start (for bench's
  * gpu_launches claim). */

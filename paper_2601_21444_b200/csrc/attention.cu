@@ -34,6 +34,7 @@
 
 #include "fabric_dev.cuh"
 #include "ptx.cuh"
+#include "score_fast_dev.cuh"
 #include "spava_internal.h"
 
 namespace spava {
@@ -172,8 +173,17 @@ __global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
 
   // trailing CTAs of a stage launch (peer fabric): the receive-side query merge
-  if (P.job.ctas > 0 && static_cast<int>(blockIdx.x) >= P.total_work) {
+  if (P.job.ctas > 0 && static_cast<int>(blockIdx.x) >= P.total_work &&
+      static_cast<int>(blockIdx.x) < P.total_work + P.job.ctas) {
     merge_job(P.job, static_cast<int>(blockIdx.x) - P.total_work, reinterpret_cast<float*>(smem));
+    return;
+  }
+  // trailing CTAs of a query launch (fast scoring fused, N1): the column-sum pass of the
+  // tensor-core scorer over (block, 128-key tile), once this launch's attention CTAs have
+  // produced the lo / hi row statistics (K tiles of the blocks are L2-resident by then)
+  if (P.sj.ctas > 0 && static_cast<int>(blockIdx.x) >= P.total_work + P.job.ctas) {
+    const int t = static_cast<int>(blockIdx.x) - P.total_work - P.job.ctas;
+    score_fast_cta<1>(P.sj.fa, t % P.sj.fa.ntiles, t / P.sj.fa.ntiles, smem);
     return;
   }
   const int warp = warp_id();
@@ -378,6 +388,10 @@ __global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
     const uint32_t tO = tmem + t_lane + 256 + qt * 128;
     const float sl2 = P.scale_log2;
     float m_ref = -INFINITY;
+    // fused fast scorer: sum of 2^(x - m_ref) over the keys of block lo / hi alone (same
+    // reference max and lazy rescale as l), i.e. the scorer's per-row softmax statistics
+    const bool seg_stats = prob.seg_lse2 != nullptr;
+    float l_seg[2] = {0.f, 0.f};
     float l = 0.f;
     uint32_t cnt = 0;
     // kSeq: tiles processed by this and by the other warpgroup (skipped tiles are the causal
@@ -639,6 +653,12 @@ __global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
       sum2 = __fadd2_rn(__fadd2_rn(sacc[0], sacc[1]), __fadd2_rn(sacc[2], sacc[3]));
       const long long tp3 = PROF_NOW();
       l = l * alpha + (sum2.x + sum2.y);
+      if (seg_stats) {
+        l_seg[0] *= alpha;
+        l_seg[1] *= alpha;
+        if (cur.seg == prob.stat_seg[0]) l_seg[0] += sum2.x + sum2.y;
+        if (cur.seg == prob.stat_seg[1]) l_seg[1] += sum2.x + sum2.y;
+      }
       if (kPParts == 1 && rescale && cnt > 0) rescale_o(alpha);
       tmem_wait_st();
       tc_fence_before();
@@ -699,11 +719,76 @@ __global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
       prob.lse[static_cast<long long>(split) * prob.split_stride_lse +
                static_cast<long long>(row) * prob.ld_lse + qhead] = lse;
     }
+    if (valid_row && seg_stats) {
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2)
+        if (prob.stat_seg[s2] >= 0)
+          prob.seg_lse2[((static_cast<long long>(s2) * prob.splits + split) * nq + row) * P.hq + qhead] =
+              l_seg[s2] > 0.f ? m_ref + __log2f(l_seg[s2]) : -INFINITY;
+    }
   }
 
+  if (P.sj.ctas > 0) __threadfence();  // seg_lse2 stores, before this CTA is counted
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (P.sj.ctas > 0) {
+    // the last split CTA of each head group combines that group's per-split statistics into
+    // lse2[blk][h][i]; the last group to finish releases the column-sum CTAs
+    // (counter[g]: splits done of group g; counter[ngroups]: groups done)
+    const AttnProb& q0 = P.prob[0];
+    const int grp = (static_cast<int>(blockIdx.x) - q0.work_begin) / q0.splits;
+    const int ngroups = P.total_work / q0.splits;
+    __shared__ int last_sh;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last_sh = atomicAdd(P.sj.counter + grp, 1u) == static_cast<unsigned>(q0.splits) - 1;
+    }
+    __syncthreads();
+    if (last_sh) {
+      __threadfence();
+      const FastArgs& fa = P.sj.fa;
+      const int nh = q0.head_pair ? 2 : 1;
+      const int h0 = q0.head_pair ? 2 * grp : grp;
+      for (int e = threadIdx.x; e < 2 * nh * fa.n_t; e += blockDim.x) {
+        const int b2 = e / (nh * fa.n_t), h2 = h0 + (e / fa.n_t) % nh, i2 = e % fa.n_t;
+        float* dst = fa.lse2 + (static_cast<long long>(b2) * fa.hq + h2) * fa.n_t + i2;
+        if (q0.stat_seg[b2] < 0) {  // block without visible keys: every score is a pad (-inf)
+          *dst = -INFINITY;
+          continue;
+        }
+        const float* src = q0.seg_lse2 + (static_cast<long long>(b2) * q0.splits * q0.nq + i2) * fa.hq + h2;
+        const long long sstride = static_cast<long long>(q0.nq) * fa.hq;
+        float M = -INFINITY, S = 0.f;  // online log2-sum-exp over the splits
+        for (int sp = 0; sp < q0.splits; sp += 8) {
+          float v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = sp + u < q0.splits ? __ldcg(src + (sp + u) * sstride) : -INFINITY;
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (v[u] == -INFINITY) continue;
+            if (v[u] > M) {
+              S = S * exp2f(M - v[u]) + 1.f;
+              M = v[u];
+            } else {
+              S += exp2f(v[u] - M);
+            }
+          }
+        }
+        *dst = M + __log2f(S);  // -inf for a row without visible keys
+      }
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        atomicExch(P.sj.counter + grp, 0u);
+        if (atomicAdd(P.sj.counter + ngroups, 1u) == static_cast<unsigned>(ngroups) - 1) {
+          __threadfence();
+          atomicExch(P.sj.counter + ngroups, 0u);
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.sj.ready), "r"(fa.epoch) : "memory");
+        }
+      }
+    }
+  }
   if (kProf && (warp == kMmaWarp || (warp < kProducerWarp && lane == 0)))
     for (int i = 0; i < 14; ++i)
       if (pr[i]) atomicAdd(&g_attn_prof[i], static_cast<unsigned long long>(pr[i]));
@@ -759,7 +844,7 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, long long rows, long long 
 std::atomic<int> g_attn_variant{-1};  // -1: SPAVA_ATTN_VARIANT / default
 
 cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, int dh,
-                             cudaStream_t stream, std::string* err, const MergeJob* job) {
+                             cudaStream_t stream, std::string* err, const MergeJob* job, const ScoreJob* sj) {
   if (dh != kHeadDim) {
     if (err) *err = "attention: only dh == 128 is implemented";
     return cudaErrorInvalidValue;
@@ -828,6 +913,9 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
     p.split_stride_out = v.split_stride_out;
     p.lse = v.lse;
     p.ld_lse = v.ld_lse;
+    p.stat_seg[0] = v.stat_seg[0];
+    p.stat_seg[1] = v.stat_seg[1];
+    p.seg_lse2 = v.seg_lse2;
     p.split_stride_lse = v.split_stride_lse;
     if (!make_tmap(&P.tmap[np][0], v.q, v.nq, static_cast<long long>(hq) * dh, v.ldq, err))
       return cudaErrorInvalidValue;
@@ -857,12 +945,25 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
     }
     P.job = *job;
   }
-  const int grid = work + P.job.ctas;
+  uint32_t smem_need = var.smem;
+  if (sj && sj->ctas > 0) {
+    if (np != 1 || !P.prob[0].seg_lse2 || !sj->counter || !sj->ready || sj->fa.ready != sj->ready ||
+        P.prob[0].units != 1 || work / P.prob[0].splits > 32 ||
+        sj->ctas != 2 * sj->fa.ntiles || sj->fa.hq != hq || sj->fa.hkv != hkv || sj->fa.n_t != P.prob[0].nq) {
+      if (err) *err = "attention: bad fused score job";
+      return cudaErrorInvalidValue;
+    }
+    P.sj = *sj;
+    smem_need = std::max(smem_need, FSmem(hkv, hq).bytes());
+  }
+  const int grid = work + P.job.ctas + P.sj.ctas;
   if (grid == 0) return cudaSuccess;
   static std::atomic<uint32_t> attr_set[kMaxDevices] = {};
   const KFn fn = var.fn;
-  const uint32_t smem_bytes = var.smem;
-  if (cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn), static_cast<int>(smem_bytes), attr_set, vsel);
+  const uint32_t smem_bytes = smem_need;
+  // opted in at the larger of the kernel's and a fused scorer CTA's need (same for every call)
+  if (cudaError_t e = smem_optin(reinterpret_cast<const void*>(fn),
+                                 static_cast<int>(std::max(var.smem, kFSmemMaxBytes)), attr_set, vsel);
       e != cudaSuccess)
     return e;
   fn<<<grid, var.threads, smem_bytes, stream>>>(P);

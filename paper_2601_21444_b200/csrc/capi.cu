@@ -207,7 +207,10 @@ struct spava_host {
   float* qsplit_out = nullptr;
   float* qsplit_lse = nullptr;
   int32_t* status = nullptr;
-  unsigned* ctr = nullptr;  // [4] zeroed device counters of the peer-flag raises (rounds 0..2)
+  unsigned* ctr = nullptr;  // [48] zeroed device words: peer-flag raise counters (rounds 0..2),
+                            // [4] fused-scorer ready flag, [8..41) fused-scorer CTA counters
+  uint32_t score_epoch = 0;  // fused fast scorer: value released into ctr[4] per layer
+  cudaEvent_t ev_score = nullptr;  // fused fast scorer: scores ready (recorded after the query launch)
   void* base = nullptr;
   cudaEvent_t ev[6] = {};  // pass1_ready, pass2_ready, q_ready, pass1_done, pass2_done, q_done
   // scoring runs on a high-priority side stream forked from the caller's stream, so the
@@ -337,10 +340,10 @@ int cfg_check(const spava_layer_cfg* c, spava_plan* plan) {
 
 // -------------------------------------------------------- op wrappers
 int attention_impl(const ProbView* pv, int np, int hq, int hkv, int dh, cudaStream_t st,
-                   spava_host* H = nullptr, const MergeJob* job = nullptr) {
+                   spava_host* H = nullptr, const MergeJob* job = nullptr, const ScoreJob* sj = nullptr) {
   std::string err;
   const size_t t0 = mark(H, st);
-  cudaError_t e = launch_attention(pv, np, hq, hkv, dh, st, &err, job);
+  cudaError_t e = launch_attention(pv, np, hq, hkv, dh, st, &err, job, sj);
   if (e != cudaSuccess)
     return fail(e == cudaErrorInvalidValue ? SPAVA_EINVAL : SPAVA_ECUDA,
                 err.empty() ? std::string("attention: ") + cudaGetErrorString(e) : err);
@@ -442,8 +445,24 @@ int peer_release(spava_fabric* F, cudaStream_t s) {
   return SPAVA_OK;
 }
 
+// N1 (fast scoring): the tensor-core scorer rides in the query attention launch -- the
+// attention's online softmax yields the scorer's row statistics of blocks lo / hi, and
+// trailing CTAs of the same launch run the column sums (K tiles L2-resident).  The
+// host-buffer pipeline (query attention after stage 1) keeps the standalone scorer.
+std::atomic<int> g_fused_score{-1};  // -1: SPAVA_FUSED_SCORE (default 1); dev override
+bool fused_score(const spava_host* H, bool cp_on) {
+  static const int v = [] {
+    const char* e = getenv("SPAVA_FUSED_SCORE");
+    return e ? atoi(e) : 1;
+  }();
+  const int o = g_fused_score.load();
+  return H->fab->cfg.score_mode == 1 && !cp_on && (o >= 0 ? o : v) != 0;
+}
+
+// scores: 0 = launch the scorer here; 1 = produced earlier on this stream (fused query
+// launch); 2 = produced on another stream, wait for H->ev_score
 int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record,
-                 cudaEvent_t before_hi = nullptr) {
+                 cudaEvent_t before_hi = nullptr, int scores = 0) {
   const spava_fabric& F = *H->fab;
   const spava_layer_cfg& c = F.cfg;
   const spava_plan& p = F.plan;
@@ -451,8 +470,9 @@ int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record,
   const long long qrow = p.l_a + 2LL * p.l_b;
   const int vs[2] = {H->v_lo, H->v_hi};
   trace_ev(H, st, kComputeBegin, "score", false);
+  if (scores == 2) CU_TRY(cudaStreamWaitEvent(st, H->ev_score, 0));
   // both blocks (lo, hi) scored in one launch of each scoring kernel
-  {
+  if (scores == 0) {
     const void* ks[2] = {row_ptr(b.k, p.l_a, dk), row_ptr(b.k, p.l_a + static_cast<long long>(p.l_b), dk)};
     const int nv[2] = {valid_rows(p, vs[0]), valid_rows(p, vs[1])};
     float* sc[2] = {H->scores[0], H->scores[1]};
@@ -522,7 +542,7 @@ int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record,
 }
 
 // per-host partial query attention (split-KV, merged over splits) into its qpartial slot
-int phase_query(spava_host* H, const HostBufs& b, cudaStream_t st, bool record) {
+int phase_query(spava_host* H, const HostBufs& b, cudaStream_t st, bool record, bool with_score = false) {
   const spava_fabric& F = *H->fab;
   const spava_layer_cfg& c = F.cfg;
   const spava_plan& p = F.plan;
@@ -535,11 +555,45 @@ int phase_query(spava_host* H, const HostBufs& b, cudaStream_t st, bool record) 
   int n = 0;
   if (H->a1 > H->a0)
     pv.seg[n++] = SegView{row_ptr(b.k, H->a0, dk), row_ptr(b.v, H->a0, dk), dk, H->a1 - H->a0, 0};
+  int nvs[2];
   for (int r = 0; r < 2; ++r) {
-    const int nv = valid_rows(p, r == 0 ? H->v_lo : H->v_hi);
+    const int nv = nvs[r] = valid_rows(p, r == 0 ? H->v_lo : H->v_hi);
     const long long krow = p.l_a + static_cast<long long>(r) * p.l_b;
-    if (nv > 0) pv.seg[n++] = SegView{row_ptr(b.k, krow, dk), row_ptr(b.v, krow, dk), dk, nv, 0};
+    if (nv > 0) {
+      pv.stat_seg[r] = n;
+      pv.seg[n++] = SegView{row_ptr(b.k, krow, dk), row_ptr(b.v, krow, dk), dk, nv, 0};
+    }
   }
+  // fused fast scorer (N1): statistics of the lo / hi segments + column-sum CTAs
+  ScoreJob sj{};
+  if (with_score) {
+    const int splits = (H->splits <= 1 && !F.peer) ? 1 : H->splits;
+    const size_t seg_bytes = (2ull * splits * p.n_t * c.hq * 4 + 255) / 256 * 256;
+    if (seg_bytes + 2ull * c.hq * p.n_t * 4 > H->score_ws_bytes) return fail(SPAVA_EINVAL, "fused score: workspace");
+    pv.seg_lse2 = static_cast<float*>(H->score_ws);
+    FastArgs& fa = sj.fa;
+    std::string err;
+    if (!make_tmap_bf16(&fa.tq, row_ptr(b.q, qrow, dq), p.n_t, dq, dq, 128, &err)) return fail(SPAVA_EINVAL, err);
+    for (int r = 0; r < 2; ++r) {
+      const long long krow = p.l_a + static_cast<long long>(r) * p.l_b;
+      if (!make_tmap_bf16(&fa.tk[r], row_ptr(b.k, krow, dk), p.l_b, dk, dk, 128, &err)) return fail(SPAVA_EINVAL, err);
+      fa.n_valid[r] = nvs[r];
+      fa.scores[r] = H->scores[r];
+    }
+    fa.lse2 = reinterpret_cast<float*>(static_cast<uint8_t*>(H->score_ws) + seg_bytes);
+    fa.n_t = p.n_t;
+    fa.l_b = p.l_b;
+    fa.hq = c.hq;
+    fa.hkv = c.hkv;
+    fa.ntiles = (p.l_b + 127) / 128;
+    fa.sl2 = (1.0f / sqrtf(128.f)) * 1.4426950408889634f;
+    fa.ready = reinterpret_cast<const uint32_t*>(H->ctr + 4);
+    fa.epoch = ++H->score_epoch;
+    sj.ctas = 2 * fa.ntiles;
+    sj.counter = H->ctr + 8;  // [ngroups + 1] (<= 33 words)
+    sj.ready = reinterpret_cast<uint32_t*>(H->ctr + 4);
+  }
+  const ScoreJob* sjp = with_score ? &sj : nullptr;
   if (H->self_keys)
     pv.seg[n++] = SegView{row_ptr(b.k, qrow, dk), row_ptr(b.v, qrow, dk), dk, p.n_t, 1};
   pv.nseg = n;
@@ -554,7 +608,7 @@ int phase_query(spava_host* H, const HostBufs& b, cudaStream_t st, bool record) 
     pv.lse = dst_lse;
     pv.ld_lse = c.hq;
     pv.splits = 1;
-    ST_TRY(attention_impl(&pv, 1, c.hq, c.hkv, c.dh, st, H));
+    ST_TRY(attention_impl(&pv, 1, c.hq, c.hkv, c.dh, st, H, nullptr, sjp));
   } else {
     pv.out = H->qsplit_out;
     pv.ldo = dq;
@@ -564,7 +618,7 @@ int phase_query(spava_host* H, const HostBufs& b, cudaStream_t st, bool record) 
     pv.splits = H->splits;
     pv.split_stride_out = static_cast<long long>(p.n_t) * dq;
     pv.split_stride_lse = static_cast<long long>(p.n_t) * c.hq;
-    ST_TRY(attention_impl(&pv, 1, c.hq, c.hkv, c.dh, st, H));
+    ST_TRY(attention_impl(&pv, 1, c.hq, c.hkv, c.dh, st, H, nullptr, sjp));
     MergeParams mp{};
     mp.nparts = H->splits;
     for (int s = 0; s < H->splits; ++s) {
@@ -591,6 +645,7 @@ int phase_query(spava_host* H, const HostBufs& b, cudaStream_t st, bool record) 
     if (F.peer) mp.fr = peer_raise(H, 2);  // the split merge's last CTA signals qpartial
     ST_TRY(merge_impl(mp, st, H));
   }
+  if (with_score) CU_TRY(cudaEventRecord(H->ev_score, st));
   if (record) CU_TRY(cudaEventRecord(H->ev[2], st));
   return SPAVA_OK;
 }
@@ -797,6 +852,11 @@ uint64_t spava_kernel_launches(void) { return g_launches.load(); }
 
 int spava_debug_attn_prof(uint64_t* out16) {
   attn_prof_read(reinterpret_cast<unsigned long long*>(out16));
+  return SPAVA_OK;
+}
+
+int spava_debug_fused_score(int on) {
+  g_fused_score.store(on < 0 ? -1 : (on ? 1 : 0));
   return SPAVA_OK;
 }
 
@@ -1298,6 +1358,7 @@ int host_init_streams(spava_host* H) {
   for (auto& e : H->ev) CU_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CU_TRY(cudaEventCreateWithFlags(&H->ev_fork, cudaEventDisableTiming));
   CU_TRY(cudaEventCreateWithFlags(&H->ev_sel, cudaEventDisableTiming));
+  CU_TRY(cudaEventCreateWithFlags(&H->ev_score, cudaEventDisableTiming));
   int prio_lo = 0, prio_hi = 0;
   CU_TRY(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   CU_TRY(cudaStreamCreateWithPriority(&H->side, cudaStreamNonBlocking, prio_hi));
@@ -1374,6 +1435,7 @@ int spava_host_destroy(spava_host* H) {
   for (auto& e : H->ev)
     if (e) cudaEventDestroy(e);
   if (H->ev_fork) cudaEventDestroy(H->ev_fork);
+  if (H->ev_score) cudaEventDestroy(H->ev_score);
   if (H->ev_sel) cudaEventDestroy(H->ev_sel);
   if (H->graph_exec) cudaGraphExecDestroy(H->graph_exec);
   if (H->graph) cudaGraphDestroy(H->graph);
@@ -1480,28 +1542,32 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
   if (cp.on) CU_TRY(cudaStreamWaitEvent(ss, H->ev_kvq, 0));
   CU_TRY(launch_delay(H->delay_ns[0], ss));
   CU_TRY(launch_delay(H->delay_ns[2], st));
+  const bool fscore = fused_score(H, cp.on);  // N1: scorer inside the query launch
   if (!F->nccl && !F->peer) {
     // H = 1: block lo (v = 0) has no passing segment, so only stage 2 waits for selection
-    ST_TRY(phase_select(H, b, ss, false, before_hi));
+    auto query = [&](cudaStream_t qs) -> int {
+      T(qs, kComputeBegin, "query_attn");
+      if (cp.on) CU_TRY(cudaStreamWaitEvent(qs, H->ev_vhi, 0));
+      ST_TRY(phase_query(H, b, qs, false, fscore));
+      T(qs, kComputeEnd, "query_attn");
+      T(qs, kCommIssued, "qpartial", true);
+      return SPAVA_OK;
+    };
+    // fused scorer: the query launch (which now also scores) goes on the side stream ahead
+    // of select, so stage 1 on the caller's stream overlaps it; stage 2 joins via ev_sel
+    if (fscore) ST_TRY(query(ss));
+    ST_TRY(phase_select(H, b, ss, false, before_hi, fscore ? 1 : 0));
     CU_TRY(cudaEventRecord(H->ev_sel, ss));
     T(ss, kCommIssued, "pass1", true);
     T(ss, kCommIssued, "pass2", true);
-    auto query = [&]() -> int {
-      T(st, kComputeBegin, "query_attn");
-      if (cp.on) CU_TRY(cudaStreamWaitEvent(st, H->ev_vhi, 0));
-      ST_TRY(phase_query(H, b, st, false));
-      T(st, kComputeEnd, "query_attn");
-      T(st, kCommIssued, "qpartial", true);
-      return SPAVA_OK;
-    };
-    if (!cp.on) ST_TRY(query());
+    if (!cp.on && !fscore) ST_TRY(query(st));
     T(st, kCommWaitStart, "pass1", true);
     T(st, kCommCompleted, "pass1", true);
     CU_TRY(launch_delay(H->delay_ns[3], st));
     T(st, kComputeBegin, "stage1");
     ST_TRY(stage_chunks(H, b, st, cp, 0));
     T(st, kComputeEnd, "stage1");
-    if (cp.on) ST_TRY(query());
+    if (cp.on) ST_TRY(query(st));
     T(st, kCommWaitStart, "pass2", true);
     CU_TRY(cudaStreamWaitEvent(st, H->ev_sel, 0));
     T(st, kCommCompleted, "pass2", true);
@@ -1527,7 +1593,25 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     ST_TRY(peer_wait_done(F, ss));  // peers have released the previous epoch's slots
     ST_TRY(peer_wait_done(F, st));
   }
-  ST_TRY(phase_select(H, b, ss, true, before_hi));  // records pass1_ready, pass2_ready on ss
+  // peer fabric: the final query merge rides in the merged stage launch (receive side)
+  const bool fused_merge = F->peer && !cp.on && merged_stages() && fused_merge_enabled();
+  auto query = [&]() -> int {
+    T(st, kComputeBegin, "query_attn");
+    if (cp.on) CU_TRY(cudaStreamWaitEvent(st, H->ev_vhi, 0));
+    ST_TRY(phase_query(H, b, st, true, fscore));  // overlaps scoring and the pass rounds
+    T(st, kComputeEnd, "query_attn");
+    if (F->peer) {
+      T(st, kCommIssued, "qpartial", true);
+    } else {
+      CU_TRY(cudaStreamWaitEvent(cs, H->ev[2], 0));
+      T(cs, kCommIssued, "qpartial", true);
+      ST_TRY(nccl_qround(F, H->ex));
+      CU_TRY(cudaEventRecord(H->ev[5], cs));
+    }
+    return SPAVA_OK;
+  };
+  if (fscore) ST_TRY(query());  // first: it produces the scores select waits for
+  ST_TRY(phase_select(H, b, ss, true, before_hi, fscore ? 2 : 0));  // records pass1_ready, pass2_ready on ss
   CU_TRY(cudaEventRecord(H->ev_sel, ss));
   if (F->peer) {
     T(ss, kCommIssued, "pass1", true);
@@ -1543,24 +1627,7 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     ST_TRY(nccl_round(F, H->ex, 1));
     CU_TRY(cudaEventRecord(H->ev[4], cs));
   }
-  // peer fabric: the final query merge rides in the merged stage launch (receive side)
-  const bool fused_merge = F->peer && !cp.on && merged_stages() && fused_merge_enabled();
-  auto query = [&]() -> int {
-    T(st, kComputeBegin, "query_attn");
-    if (cp.on) CU_TRY(cudaStreamWaitEvent(st, H->ev_vhi, 0));
-    ST_TRY(phase_query(H, b, st, true));  // overlaps scoring and the pass rounds
-    T(st, kComputeEnd, "query_attn");
-    if (F->peer) {
-      T(st, kCommIssued, "qpartial", true);
-    } else {
-      CU_TRY(cudaStreamWaitEvent(cs, H->ev[2], 0));
-      T(cs, kCommIssued, "qpartial", true);
-      ST_TRY(nccl_qround(F, H->ex));
-      CU_TRY(cudaEventRecord(H->ev[5], cs));
-    }
-    return SPAVA_OK;
-  };
-  if (!cp.on) ST_TRY(query());
+  if (!cp.on && !fscore) ST_TRY(query());
   // st waits for round k (0 pass1, 1 pass2, 2 qpartial) of every host
   auto wait_round = [&](int k) -> int {
     if (!F->peer) {
@@ -1777,12 +1844,20 @@ int spava_sim_layer(spava_fabric* F, spava_host* const* hosts, const void* const
   // records keep each host's run_host program order (simhost.cpp:343-426)
   for (int h = 0; h < H; ++h) {
     spava_host* X = hosts[h];
-    ST_TRY(phase_select(X, b[h], st, false));
+    const bool fs = fused_score(X, false);  // N1: the query launch also scores
+    if (fs) {
+      trace_ev(X, st, kComputeBegin, "query_attn", false);
+      ST_TRY(phase_query(X, b[h], st, false, true));
+      trace_ev(X, st, kComputeEnd, "query_attn", false);
+    }
+    ST_TRY(phase_select(X, b[h], st, false, nullptr, fs ? 1 : 0));
     trace_ev(X, st, kCommIssued, "pass1", true);
     trace_ev(X, st, kCommIssued, "pass2", true);
-    trace_ev(X, st, kComputeBegin, "query_attn", false);
-    ST_TRY(phase_query(X, b[h], st, false));
-    trace_ev(X, st, kComputeEnd, "query_attn", false);
+    if (!fs) {
+      trace_ev(X, st, kComputeBegin, "query_attn", false);
+      ST_TRY(phase_query(X, b[h], st, false));
+      trace_ev(X, st, kComputeEnd, "query_attn", false);
+    }
     trace_ev(X, st, kCommIssued, "qpartial", true);
   }
   for (int h = 0; h < H; ++h) {
@@ -1847,8 +1922,10 @@ int spava_sim_layer_timed(spava_fabric* F, spava_host* const* hosts, const void*
   int rc = SPAVA_OK;
   for (int h = 0; h < H && rc == SPAVA_OK; ++h) {
     cudaEventRecord(ev[4 * h], st);
-    rc = phase_select(hosts[h], b[h], st, false);
-    if (rc == SPAVA_OK) rc = phase_query(hosts[h], b[h], st, false);
+    const bool fs = fused_score(hosts[h], false);
+    if (fs) rc = phase_query(hosts[h], b[h], st, false, true);
+    if (rc == SPAVA_OK) rc = phase_select(hosts[h], b[h], st, false, nullptr, fs ? 1 : 0);
+    if (rc == SPAVA_OK && !fs) rc = phase_query(hosts[h], b[h], st, false);
     cudaEventRecord(ev[4 * h + 1], st);
   }
   for (int h = 0; h < H && rc == SPAVA_OK; ++h) {

@@ -38,6 +38,8 @@ struct AttnProb {
   long long ldo;             // row stride (elements)
   long long split_stride_out;
   float* lse;                // nullable; [splits][nq][ld_lse] natural-log lse per head
+  int stat_seg[2];           // fused fast scorer: segment index of block lo / hi (-1: none)
+  float* seg_lse2;           // nullable; [2][splits][nq][hq] log2-domain lse of those segments
   int ld_lse;
   long long split_stride_lse;
 };
@@ -82,6 +84,33 @@ struct MergeJob {
   int ctas;  // 0 = no job
 };
 
+// tensor-core scorer arguments (score_fast.cu / score_fast_dev.cuh)
+struct FastArgs {
+  CUtensorMap tq;        // Q_qr [n_t x hq*128]
+  CUtensorMap tk[2];     // K block [l_b x hkv*128], per block
+  int n_valid[2];
+  const uint8_t* pad[2];
+  float* scores[2];
+  float2* part;          // [blk][hq][n_t][ntiles] (tile max, tile sum), log2 domain
+  float* lse2;           // [blk][hq][n_t]
+  int n_t, l_b, hq, hkv, ntiles;
+  float sl2;             // (1/sqrt(dh)) * log2(e)
+  const uint32_t* ready; // pass 1 inside another launch: wait for *ready >= epoch first
+  uint32_t epoch;
+};
+
+// Fast-mode scorer fused into the query attention launch: the attention CTAs of the (single)
+// query problem emit per-split log2 row statistics of the lo / hi segments (AttnProb
+// seg_lse2); the last split of each head group combines them into fa.lse2, the last group
+// releases *fa.ready = epoch; then
+// `ctas` trailing CTAs (one per (block, 128-key tile)) run the column-sum pass.
+struct ScoreJob {
+  FastArgs fa;
+  int ctas;            // 0 = no job
+  unsigned* counter;   // [ngroups + 1] zeroed: finished splits per head group, groups done
+  uint32_t* ready;     // = fa.ready
+};
+
 struct __align__(64) AttnParams {
   // per problem: [0] = Q, [1+2s] = K of segment s, [2+2s] = V of segment s
   CUtensorMap tmap[kMaxProbs][1 + 2 * kMaxSegs];
@@ -91,6 +120,7 @@ struct __align__(64) AttnParams {
   int total_work;
   float scale_log2;  // (1/sqrt(dh)) * log2(e)
   MergeJob job;      // job.ctas trailing CTAs run the receive-side query merge
+  ScoreJob sj;       // sj.ctas trailing CTAs run the fast scorer's column sums
 };
 
 // Opt kernel `fn` into `bytes` of dynamic shared memory on the current device, once per
@@ -128,11 +158,14 @@ struct ProbView {
   int splits;
   long long split_stride_out;
   long long split_stride_lse;
+  int stat_seg[2] = {-1, -1};  // fused fast scorer (see AttnProb)
+  float* seg_lse2 = nullptr;
 };
 void attn_prof_read(unsigned long long* out16);  // dev: cycle counters of variant 2
 int attn_set_variant(int v);                     // dev: -1 = env/default, else variant id
 cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, int dh,
-                             cudaStream_t stream, std::string* err, const MergeJob* job = nullptr);
+                             cudaStream_t stream, std::string* err, const MergeJob* job = nullptr,
+                             const ScoreJob* sj = nullptr);
 
 // 2D bf16 [rows x cols] tensor map, box 64 cols x box_rows rows, 128B swizzle
 bool make_tmap_bf16(CUtensorMap* m, const void* base, long long rows, long long cols, long long ld,

@@ -46,7 +46,7 @@ EXPORTED_SYMBOLS = [
     "spava_decoder_workspace", "spava_host_decoder_layer",
     "spava_host_status",
     "spava_host_set_timing", "spava_host_timing", "spava_kernel_launches",
-    "spava_debug_attn_prof", "spava_debug_attn_variant", "spava_debug_fused_merge",
+    "spava_debug_attn_prof", "spava_debug_attn_variant", "spava_debug_fused_merge", "spava_debug_fused_score",
 ]
 
 
@@ -188,6 +188,7 @@ def lib():
                                                C.c_size_t, C.c_void_p]
         L.spava_debug_attn_variant.argtypes = [C.c_int]
         L.spava_debug_fused_merge.argtypes = [C.c_int]
+        L.spava_debug_fused_score.argtypes = [C.c_int]
         L.spava_split_rows.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                                        C.c_int, C.c_void_p]
         L.spava_merge_rows.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
