@@ -4,11 +4,14 @@
 //
 // Same names, argument meaning and error behaviour (std::invalid_argument /
 // std::out_of_range) as the reference, on host fp32 matrices: each call uploads its
-// operands as bf16, runs the sm_100a kernels, and returns host results.  Differences:
-//   * the GPU path computes in bf16 with fp32 accumulation (dh = 128 only); inputs that
-//     are not bf16-representable are rounded to nearest-even on upload;
-//   * every attention/score entry point takes an optional kv_heads (GQA) that defaults
-//     to `heads`, which is the reference's (MHA) behaviour;
+// operands as bf16, runs the sm_100a kernels, and returns host results.  Reference call
+// sites compile unchanged (CostCounters* in the reference's position).  Differences:
+//   * the GPU path computes in bf16 with fp32 accumulation; inputs that are not
+//     bf16-representable are rounded to nearest-even on upload; head widths up to 128
+//     (narrower heads, e.g. the acceptance suite's d = 64 / 4 heads, are zero-padded to
+//     the kernels' 128 columns -- exact for the scores, see spava_score_block_ex);
+//   * every attention/score entry point takes an optional trailing kv_heads (GQA) that
+//     defaults to `heads`, which is the reference's (MHA) behaviour;
 //   * pad masks passed to attention must be tail masks (the only kind split_context
 //     produces, partition.cpp:71-79).
 // The per-layer fast path (no host round trips) is spava_host_layer in spava_b200.h.
@@ -61,6 +64,31 @@ std::pair<BlockPlan, ContextSplit> split_context(const Matrix& e_v, const Matrix
                                                  int l_a, int l_p);
 std::pair<int, int> slice_anchor(int l_a, int hosts, int h);
 BlockPlan default_plan(int n, int hosts);
+// partition.hpp:45: floor(F/H) frames per host, one extra for the first F mod H hosts
+std::vector<int> frame_partition(int frames, int hosts);
+
+// ---- costs.hpp:9-54 (algorithmic FLOP tallies, same convention and buckets)
+enum class AttnSite { AnchorSelf, BlockAnchor, BlockPassing, BlockOwn, QueryAttn, EncodeAttn, Score, Other };
+struct CostCounters {
+  uint64_t anchor_self = 0, block_anchor = 0, block_passing = 0, block_own = 0, query_attn = 0,
+           encode_attn = 0, score = 0, other = 0;
+  void add(AttnSite site, uint64_t flops) {
+    switch (site) {
+      case AttnSite::AnchorSelf: anchor_self += flops; break;
+      case AttnSite::BlockAnchor: block_anchor += flops; break;
+      case AttnSite::BlockPassing: block_passing += flops; break;
+      case AttnSite::BlockOwn: block_own += flops; break;
+      case AttnSite::QueryAttn: query_attn += flops; break;
+      case AttnSite::EncodeAttn: encode_attn += flops; break;
+      case AttnSite::Score: score += flops; break;
+      case AttnSite::Other: other += flops; break;
+    }
+  }
+  uint64_t balanced_total() const { return anchor_self + block_passing + block_own; }
+  uint64_t attention_total() const {
+    return anchor_self + block_anchor + block_passing + block_own + query_attn;
+  }
+};
 
 // ---- attention.hpp:14-63
 enum class MaskKind { CausalWithin, FullyVisible };
@@ -69,13 +97,25 @@ struct KeySegment {
   const Matrix* v = nullptr;
   MaskKind mask = MaskKind::FullyVisible;
   const std::vector<uint8_t>* pad = nullptr;  // tail pads only
+  AttnSite site = AttnSite::Other;
 };
+// single-head attention output + per-row lse (-inf and a zero row: no visible key)
+struct AttnPartial {
+  Matrix out;
+  std::vector<float> lse;
+  bool row_valid(int r) const;
+};
+float invalid_lse();
+AttnPartial attention_lse(const Matrix& q, std::span<const KeySegment> segments, float scale,
+                          bool allow_invalid_rows = false, CostCounters* counters = nullptr);
+Matrix merge_partials(std::span<const AttnPartial> parts);
 struct MultiHeadPartial {
   Matrix out;  // n_q x heads*dh
   Matrix lse;  // n_q x heads
 };
 MultiHeadPartial mha_lse(const Matrix& q, std::span<const KeySegment> segments, int heads,
-                         bool allow_invalid_rows = false, int kv_heads = 0);
+                         bool allow_invalid_rows = false, CostCounters* counters = nullptr,
+                         int kv_heads = 0);
 Matrix mha_merge(std::span<const MultiHeadPartial> parts, int heads);
 
 // ---- approx.hpp:13-81
@@ -99,22 +139,28 @@ struct BlockQkv {
   int global_offset = 0;
 };
 
+// score_context (approx.hpp:38-41): one head, explicit scale
+ScoreVector score_context(const Matrix& q_qr, const Matrix& k_block, float scale,
+                          const std::vector<uint8_t>* pad_mask, int source = 0,
+                          bool softmax_aggregation = true, CostCounters* counters = nullptr);
 // score_block (simhost.cpp:209-224): per-head score_context summed over heads.
 ScoreVector score_block(const Matrix& q_qr, const Matrix& k_block, int heads,
                         const std::vector<uint8_t>* pad, int source = 0,
-                        bool softmax_scores = true, int kv_heads = 0);
+                        bool softmax_scores = true, CostCounters* counters = nullptr, int kv_heads = 0);
 PassingBlock select_essential(const Matrix& k_block, const Matrix& v_block,
                               const ScoreVector& scores, int l_p, int global_offset);
 PassingAssembly assemble_passing(int v, std::span<const PassingBlock> all_compressed);
 Matrix anchor_attention(const Matrix& q_a, const Matrix& k_a, const Matrix& v_a, int heads,
-                        int kv_heads = 0);
+                        CostCounters* counters = nullptr, int kv_heads = 0);
 Matrix block_attention(const BlockQkv& block, const Matrix& k_a, const Matrix& v_a,
-                       const PassingAssembly& passing, int heads, int kv_heads = 0);
+                       const PassingAssembly& passing, int heads, CostCounters* counters = nullptr,
+                       int kv_heads = 0);
 MultiHeadPartial query_attention(const Matrix& q_qr, const Matrix& anchor_k,
                                  const Matrix& anchor_v, std::pair<int, int> anchor_slice,
                                  const BlockQkv& block_lo, const BlockQkv& block_hi,
                                  const Matrix* query_k, const Matrix* query_v,
                                  bool include_query_self, int heads, int query_offset,
-                                 std::vector<int>* key_indices, int kv_heads = 0);
+                                 std::vector<int>* key_indices, CostCounters* counters = nullptr,
+                                 int kv_heads = 0);
 
 }  // namespace seqpar_b200

@@ -101,6 +101,14 @@ size_t spava_score_workspace(int n_t, int l_b, int hq);
 int spava_score_block(const void* q, int64_t ldq, int n_t, const void* k, int64_t ldk, int l_b,
                       const uint8_t* pad, int n_valid, int hq, int hkv, int dh, int softmax,
                       float* scores, void* workspace, size_t workspace_bytes, void* stream);
+/* score_context (approx.cpp:15-69, approx.hpp:38-41) with the caller's logit scale
+ * (scale == 0: 1/sqrtf(dh)).  Heads narrower than 128 are passed zero-padded to dh = 128
+ * columns (the padding adds exact zeros to the c-ascending fp32 dot products, so the
+ * scores are those of the narrow heads).                                               */
+int spava_score_block_ex(const void* q, int64_t ldq, int n_t, const void* k, int64_t ldk, int l_b,
+                         const uint8_t* pad, int n_valid, int hq, int hkv, int dh, int softmax,
+                         float* scores, void* workspace, size_t workspace_bytes, void* stream,
+                         float scale);
 /* Fast score_block on the tensor cores (score_fast.cu): same definition, logits from bf16
  * tcgen05 MMAs with fp32 accumulation, softmax via exp2 -- NOT bit-faithful (the exact
  * entry point above is); passing indices agree except where two scores tie within that
@@ -143,6 +151,12 @@ size_t spava_attention_workspace(int nq, int hq, int dh, int splits);
 int spava_attention(const void* q, int64_t ldq, int nq, const spava_segment* segs, int nseg,
                     int hq, int hkv, int dh, void* out, int64_t ldo, int out_f32, float* lse,
                     int splits, void* workspace, size_t workspace_bytes, void* stream);
+/* attention_lse's explicit logit scale (attention.hpp:40-41; scale == 0: 1/sqrtf(dh)).
+ * Narrower heads go zero-padded to dh = 128 columns (q, k and v); the padded output
+ * columns come out zero.                                                                */
+int spava_attention_ex(const void* q, int64_t ldq, int nq, const spava_segment* segs, int nseg,
+                       int hq, int hkv, int dh, void* out, int64_t ldo, int out_f32, float* lse,
+                       int splits, void* workspace, size_t workspace_bytes, void* stream, float scale);
 
 /* --------------------------------------------------------------- merge
  * mha_merge (attention.cpp:180-197) over nparts partials in host order.

@@ -844,7 +844,8 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, long long rows, long long 
 std::atomic<int> g_attn_variant{-1};  // -1: SPAVA_ATTN_VARIANT / default
 
 cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, int dh,
-                             cudaStream_t stream, std::string* err, const MergeJob* job, const ScoreJob* sj) {
+                             cudaStream_t stream, std::string* err, const MergeJob* job, const ScoreJob* sj,
+                             float scale) {
   if (dh != kHeadDim) {
     if (err) *err = "attention: only dh == 128 is implemented";
     return cudaErrorInvalidValue;
@@ -859,7 +860,9 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
   std::memset(&P, 0, sizeof(P));
   P.hq = hq;
   P.hkv = hkv;
-  P.scale_log2 = (1.0f / sqrtf(static_cast<float>(dh))) * 1.4426950408889634f;
+  // logit scale: 1/sqrt(dh) (mha_lse, attention.cpp:163-165) unless the caller passes one
+  // (attention_lse's explicit scale; heads narrower than 128 zero-padded to 128 columns)
+  P.scale_log2 = (scale > 0.f ? scale : 1.0f / sqrtf(static_cast<float>(dh))) * 1.4426950408889634f;
   // kernel variants (spava_debug_attn_variant / SPAVA_ATTN_VARIANT, dev A/B only): all are
   // the ping-pong kernel (2 Q tiles per CTA, 320 threads) with different template switches.
   using KFn = void (*)(AttnParams);

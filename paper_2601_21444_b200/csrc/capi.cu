@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstring>
 #include <cstdio>
 #include <string>
@@ -340,10 +341,11 @@ int cfg_check(const spava_layer_cfg* c, spava_plan* plan) {
 
 // -------------------------------------------------------- op wrappers
 int attention_impl(const ProbView* pv, int np, int hq, int hkv, int dh, cudaStream_t st,
-                   spava_host* H = nullptr, const MergeJob* job = nullptr, const ScoreJob* sj = nullptr) {
+                   spava_host* H = nullptr, const MergeJob* job = nullptr, const ScoreJob* sj = nullptr,
+                   float scale = 0.f) {
   std::string err;
   const size_t t0 = mark(H, st);
-  cudaError_t e = launch_attention(pv, np, hq, hkv, dh, st, &err, job, sj);
+  cudaError_t e = launch_attention(pv, np, hq, hkv, dh, st, &err, job, sj, scale);
   if (e != cudaSuccess)
     return fail(e == cudaErrorInvalidValue ? SPAVA_EINVAL : SPAVA_ECUDA,
                 err.empty() ? std::string("attention: ") + cudaGetErrorString(e) : err);
@@ -963,6 +965,13 @@ size_t spava_score_workspace(int n_t, int l_b, int hq) { return score_workspace_
 int spava_score_block(const void* q, int64_t ldq, int n_t, const void* k, int64_t ldk, int l_b,
                       const uint8_t* pad, int n_valid, int hq, int hkv, int dh, int softmax,
                       float* scores, void* ws, size_t ws_bytes, void* stream) {
+  return spava_score_block_ex(q, ldq, n_t, k, ldk, l_b, pad, n_valid, hq, hkv, dh, softmax, scores, ws,
+                              ws_bytes, stream, 0.f);
+}
+
+int spava_score_block_ex(const void* q, int64_t ldq, int n_t, const void* k, int64_t ldk, int l_b,
+                         const uint8_t* pad, int n_valid, int hq, int hkv, int dh, int softmax,
+                         float* scores, void* ws, size_t ws_bytes, void* stream, float scale) {
   if (n_t < 1) return fail(SPAVA_EINVAL, "score_context: empty query");
   if (dh != kHeadDim || hq < 1 || hkv < 1 || hq % hkv || hq > 32)
     return fail(SPAVA_EINVAL, "score_block: need dh == 128, hkv | hq, hq <= 32");
@@ -970,8 +979,9 @@ int spava_score_block(const void* q, int64_t ldq, int n_t, const void* k, int64_
   if (ws_bytes < score_workspace_bytes(n_t, l_b, hq))
     return fail(SPAVA_EINVAL, "score_block: workspace too small");
   ST_TRY(require_device());
+  if (!(scale >= 0.f) || std::isinf(scale)) return fail(SPAVA_EINVAL, "score_block: scale must be finite, >= 0");
   cudaError_t e = launch_score_exact(q, ldq, n_t, k, ldk, l_b, pad, n_valid, hq, hkv, dh, softmax,
-                                     scores, ws, ws_bytes, as_stream(stream));
+                                     scores, ws, ws_bytes, as_stream(stream), scale);
   if (e != cudaSuccess) return fail(SPAVA_ECUDA, std::string("score_block: ") + cudaGetErrorString(e));
   g_launches += softmax ? 3 : 2;
   return SPAVA_OK;
@@ -1022,6 +1032,14 @@ size_t spava_attention_workspace(int nq, int hq, int dh, int splits) {
 int spava_attention(const void* q, int64_t ldq, int nq, const spava_segment* segs, int nseg,
                     int hq, int hkv, int dh, void* out, int64_t ldo, int out_f32, float* lse,
                     int splits, void* ws, size_t ws_bytes, void* stream) {
+  return spava_attention_ex(q, ldq, nq, segs, nseg, hq, hkv, dh, out, ldo, out_f32, lse, splits, ws,
+                            ws_bytes, stream, 0.f);
+}
+
+int spava_attention_ex(const void* q, int64_t ldq, int nq, const spava_segment* segs, int nseg,
+                       int hq, int hkv, int dh, void* out, int64_t ldo, int out_f32, float* lse,
+                       int splits, void* ws, size_t ws_bytes, void* stream, float scale) {
+  if (!(scale >= 0.f) || std::isinf(scale)) return fail(SPAVA_EINVAL, "attention: scale must be finite, >= 0");
   if (nseg < 0 || nseg > kMaxSegs) return fail(SPAVA_EINVAL, "attention: at most 5 key segments");
   if (splits < 1) splits = 1;
   if (splits > kMaxMergeParts) return fail(SPAVA_EINVAL, "attention: too many splits");
@@ -1045,7 +1063,7 @@ int spava_attention(const void* q, int64_t ldq, int nq, const spava_segment* seg
     pv.lse = lse;
     pv.ld_lse = hq;
     pv.splits = 1;
-    return attention_impl(&pv, 1, hq, hkv, dh, st);
+    return attention_impl(&pv, 1, hq, hkv, dh, st, nullptr, nullptr, nullptr, scale);
   }
   if (ws_bytes < spava_attention_workspace(nq, hq, dh, splits))
     return fail(SPAVA_EINVAL, "attention: workspace too small for splits");
@@ -1059,7 +1077,7 @@ int spava_attention(const void* q, int64_t ldq, int nq, const spava_segment* seg
   pv.splits = splits;
   pv.split_stride_out = static_cast<long long>(nq) * dq;
   pv.split_stride_lse = static_cast<long long>(nq) * hq;
-  ST_TRY(attention_impl(&pv, 1, hq, hkv, dh, st));
+  ST_TRY(attention_impl(&pv, 1, hq, hkv, dh, st, nullptr, nullptr, nullptr, scale));
   MergeParams mp{};
   mp.nparts = splits;
   for (int s = 0; s < splits; ++s) {

@@ -526,7 +526,7 @@ cudaError_t launch_score_exact2(int nblk, const void* q, long long ldq, int n_t,
                                 const void* const* k, long long ldk, int l_b,
                                 const uint8_t* const* pad, const int* n_valid, int hq, int hkv,
                                 int dh, int softmax, float* const* scores, void* ws,
-                                size_t ws_bytes, cudaStream_t stream) {
+                                size_t ws_bytes, cudaStream_t stream, float scale) {
   if (dh != kDh || hq < 1 || hkv < 1 || hq % hkv || hq > 32 || n_t < 1 || nblk < 1 || nblk > 2)
     return cudaErrorInvalidValue;
   if (l_b <= 0) return cudaSuccess;
@@ -548,7 +548,7 @@ cudaError_t launch_score_exact2(int nblk, const void* q, long long ldq, int n_t,
   a.hq = hq;
   a.hkv = hkv;
   a.softmax = softmax;
-  a.scale = 1.0f / sqrtf(static_cast<float>(dh));
+  a.scale = scale > 0.f ? scale : 1.0f / sqrtf(static_cast<float>(dh));  // score_context's scale
   a.ldL = ld_logits(l_b);
   a.ntiles = n_ktiles(l_b);
   uint8_t* w = static_cast<uint8_t*>(ws);
@@ -590,13 +590,13 @@ cudaError_t launch_score_exact2(int nblk, const void* q, long long ldq, int n_t,
 cudaError_t launch_score_exact(const void* q, long long ldq, int n_t, const void* k,
                                long long ldk, int l_b, const uint8_t* pad, int n_valid, int hq,
                                int hkv, int dh, int softmax, float* scores, void* ws,
-                               size_t ws_bytes, cudaStream_t stream) {
+                               size_t ws_bytes, cudaStream_t stream, float scale) {
   const void* ks[1] = {k};
   const uint8_t* pads[1] = {pad};
   const int nv[1] = {n_valid};
   float* sc[1] = {scores};
   return launch_score_exact2(1, q, ldq, n_t, ks, ldk, l_b, pads, nv, hq, hkv, dh, softmax, sc, ws,
-                             ws_bytes, stream);
+                             ws_bytes, stream, scale);
 }
 
 }  // namespace spava

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -78,10 +79,55 @@ Matrix download_bf16(const void* d, int rows, int cols) {
 }
 
 int head_dim(int width, int heads, const char* what) {
-  if (heads < 1 || width % heads) throw std::invalid_argument(std::string(what) + ": width not divisible by heads");
-  if (width / heads != kDh)
-    throw std::invalid_argument(std::string(what) + ": the B200 path implements dh = 128");
-  return kDh;
+  if (heads < 1 || width % heads)
+    throw std::invalid_argument(std::string(what) + ": model width not divisible by head count");
+  if (width / heads < 1 || width / heads > kDh)
+    throw std::invalid_argument(std::string(what) + ": the B200 path implements head widths 1..128");
+  return width / heads;
+}
+
+// [rows x heads*dh] -> device bf16 [rows x heads*128]: each head zero-padded to the
+// kernels' 128 columns (zero products are exact, so narrow heads compute as themselves)
+Dev upload_heads_bf16(const Matrix& m, int heads, int dh) {
+  if (dh == kDh) return upload_bf16(m);
+  const size_t W = static_cast<size_t>(heads) * kDh;
+  std::vector<__nv_bfloat16> h(static_cast<size_t>(m.rows) * W, __float2bfloat16_rn(0.f));
+  for (int r = 0; r < m.rows; ++r)
+    for (int g = 0; g < heads; ++g)
+      for (int c = 0; c < dh; ++c) h[r * W + g * kDh + c] = __float2bfloat16_rn(m.at(r, g * dh + c));
+  Dev d(h.size() * sizeof(__nv_bfloat16));
+  cuda_check(cudaMemcpy(d.p, h.data(), h.size() * sizeof(__nv_bfloat16), cudaMemcpyHostToDevice), "H2D");
+  return d;
+}
+
+// device f32 [rows x heads*wp] -> [rows x heads*dh] (drops each head's padding columns)
+Matrix download_heads_f32(const void* d, int rows, int heads, int dh, int wp) {
+  if (dh == wp) return download_f32(d, rows, heads * dh);
+  Matrix full = download_f32(d, rows, heads * wp), m(rows, heads * dh);
+  for (int r = 0; r < rows; ++r)
+    for (int g = 0; g < heads; ++g)
+      for (int c = 0; c < dh; ++c) m.at(r, g * dh + c) = full.at(r, g * wp + c);
+  return m;
+}
+
+// host f32 [rows x heads*dh] -> device f32 [rows x heads*wp] (zero columns past dh)
+Dev upload_heads_f32(const Matrix& m, int heads, int dh, int wp) {
+  if (dh == wp) return upload_f32(m.data.data(), m.data.size());
+  std::vector<float> h(static_cast<size_t>(m.rows) * heads * wp, 0.f);
+  for (int r = 0; r < m.rows; ++r)
+    for (int g = 0; g < heads; ++g)
+      for (int c = 0; c < dh; ++c) h[(static_cast<size_t>(r) * heads + g) * wp + c] = m.at(r, g * dh + c);
+  return upload_f32(h.data(), h.size());
+}
+
+// reference FLOP convention (attention.cpp:33-36): per key segment 2 (causal) or 4 x
+// n_q x n_k x dh, per head
+void count_attention(CostCounters* counters, std::span<const KeySegment> segs, int n_q, int dh, int heads) {
+  if (!counters) return;
+  for (const KeySegment& s : segs) {
+    const uint64_t pair_cost = s.mask == MaskKind::CausalWithin ? 2u : 4u;
+    counters->add(s.site, pair_cost * static_cast<uint64_t>(n_q) * s.k->rows * dh * heads);
+  }
 }
 
 // tail pad mask -> number of valid keys; a non-tail mask is unsupported on the device path
@@ -157,6 +203,14 @@ std::pair<int, int> slice_anchor(int l_a, int hosts, int h) {
   return {b, e};
 }
 
+std::vector<int> frame_partition(int frames, int hosts) {
+  if (hosts < 1) throw std::invalid_argument("frame_partition: need at least one host");
+  if (frames < 0) throw std::invalid_argument("frame_partition: negative frame count");
+  std::vector<int> counts(hosts);
+  check(spava_frame_partition(frames, hosts, counts.data()), "frame_partition");
+  return counts;
+}
+
 BlockPlan default_plan(int n, int hosts) {
   spava_plan p{};
   check(spava_default_plan(n, hosts, &p), "default_plan");
@@ -164,30 +218,50 @@ BlockPlan default_plan(int n, int hosts) {
 }
 
 // ------------------------------------------------------------------- scoring
-ScoreVector score_block(const Matrix& q_qr, const Matrix& k_block, int heads,
-                        const std::vector<uint8_t>* pad, int source, bool softmax_scores,
-                        int kv_heads) {
-  if (kv_heads <= 0) kv_heads = heads;
+namespace {
+ScoreVector score_impl(const Matrix& q_qr, const Matrix& k_block, int heads, int kv_heads, float scale,
+                       const std::vector<uint8_t>* pad, int source, bool softmax, CostCounters* counters,
+                       const char* what) {
   if (q_qr.rows == 0) throw std::invalid_argument("score_context: empty query");
-  const int dh = head_dim(q_qr.cols, heads, "score_block");
+  const int dh = head_dim(q_qr.cols, heads, what);
   if (k_block.cols != kv_heads * dh) throw std::invalid_argument("score_context: width mismatch");
   if (pad && static_cast<int>(pad->size()) != k_block.rows)
     throw std::invalid_argument("score_context: pad mask length mismatch");
-  Dev q = upload_bf16(q_qr), k = upload_bf16(k_block);
+  if (counters) counters->add(AttnSite::Score, 2ull * q_qr.rows * k_block.rows * dh * heads);
+  Dev q = upload_heads_bf16(q_qr, heads, dh), k = upload_heads_bf16(k_block, kv_heads, dh);
   Dev pd(pad ? pad->size() : 1);
   if (pad) cuda_check(cudaMemcpy(pd.p, pad->data(), pad->size(), cudaMemcpyHostToDevice), "H2D");
   Dev sc(sizeof(float) * std::max(k_block.rows, 1));
   const size_t wsb = spava_score_workspace(q_qr.rows, k_block.rows, heads);
   Dev ws(wsb);
-  check(spava_score_block(q.p, q_qr.cols, q_qr.rows, k.p, k_block.cols, k_block.rows,
-                          pad ? pd.as<uint8_t>() : nullptr, k_block.rows, heads, kv_heads, dh,
-                          softmax_scores ? 1 : 0, sc.as<float>(), ws.p, wsb, nullptr),
-        "score_block");
+  check(spava_score_block_ex(q.p, heads * kDh, q_qr.rows, k.p, kv_heads * kDh, k_block.rows,
+                             pad ? pd.as<uint8_t>() : nullptr, k_block.rows, heads, kv_heads, kDh,
+                             softmax ? 1 : 0, sc.as<float>(), ws.p, wsb, nullptr, scale),
+        what);
   ScoreVector out;
   out.source = source;
   out.scores.resize(k_block.rows);
   cuda_check(cudaMemcpy(out.scores.data(), sc.p, sizeof(float) * k_block.rows, cudaMemcpyDeviceToHost), "D2H");
   return out;
+}
+}  // namespace
+
+ScoreVector score_context(const Matrix& q_qr, const Matrix& k_block, float scale,
+                          const std::vector<uint8_t>* pad_mask, int source, bool softmax_aggregation,
+                          CostCounters* counters) {
+  if (q_qr.rows == 0) throw std::invalid_argument("score_context: empty query");
+  if (q_qr.cols != k_block.cols) throw std::invalid_argument("score_context: width mismatch");
+  if (!(scale > 0.f) || !std::isfinite(scale)) throw std::invalid_argument("score_context: scale must be > 0");
+  return score_impl(q_qr, k_block, 1, 1, scale, pad_mask, source, softmax_aggregation, counters, "score_context");
+}
+
+ScoreVector score_block(const Matrix& q_qr, const Matrix& k_block, int heads,
+                        const std::vector<uint8_t>* pad, int source, bool softmax_scores,
+                        CostCounters* counters, int kv_heads) {
+  if (kv_heads <= 0) kv_heads = heads;
+  const int dh = head_dim(q_qr.cols, heads, "score_block");
+  return score_impl(q_qr, k_block, heads, kv_heads, 1.0f / std::sqrt(static_cast<float>(dh)), pad, source,
+                    softmax_scores, counters, "score_block");
 }
 
 PassingBlock select_essential(const Matrix& k_block, const Matrix& v_block,
@@ -255,91 +329,145 @@ PassingAssembly assemble_passing(int v, std::span<const PassingBlock> all) {
 }
 
 // ------------------------------------------------------------------ attention
-MultiHeadPartial mha_lse(const Matrix& q, std::span<const KeySegment> segments, int heads,
-                         bool allow_invalid_rows, int kv_heads) {
-  if (kv_heads <= 0) kv_heads = heads;
-  const int dh = head_dim(q.cols, heads, "mha_lse");
-  if (segments.size() > 4) throw std::invalid_argument("mha_lse: at most 4 key segments");
+namespace {
+MultiHeadPartial mha_impl(const Matrix& q, std::span<const KeySegment> segments, int heads, int kv_heads,
+                          float scale, bool allow_invalid_rows, CostCounters* counters, const char* what) {
+  const int dh = head_dim(q.cols, heads, what);
+  if (segments.size() > 4) throw std::invalid_argument(std::string(what) + ": at most 4 key segments");
   std::vector<std::unique_ptr<Dev>> keep;
   std::vector<spava_segment> segs;
   for (const KeySegment& s : segments) {
     if (s.k->cols != kv_heads * dh) throw std::invalid_argument("attention_lse: key width != query width");
     if (s.k->rows != s.v->rows) throw std::invalid_argument("attention_lse: K/V row mismatch");
+    if (s.v->cols != s.k->cols) throw std::invalid_argument("attention_lse: V width mismatch");
     if (s.mask == MaskKind::CausalWithin && s.k->rows != q.rows)
       throw std::invalid_argument("attention_lse: causal segment must match query rows");
     const int n = valid_len(s.pad, s.k->rows, "attention_lse");
-    keep.push_back(std::make_unique<Dev>(upload_bf16(*s.k)));
-    keep.push_back(std::make_unique<Dev>(upload_bf16(*s.v)));
-    segs.push_back(spava_segment{keep[keep.size() - 2]->p, keep.back()->p, s.k->cols, n,
+    keep.push_back(std::make_unique<Dev>(upload_heads_bf16(*s.k, kv_heads, dh)));
+    keep.push_back(std::make_unique<Dev>(upload_heads_bf16(*s.v, kv_heads, dh)));
+    segs.push_back(spava_segment{keep[keep.size() - 2]->p, keep.back()->p, static_cast<int64_t>(kv_heads) * kDh, n,
                                  s.mask == MaskKind::CausalWithin ? 1 : 0});
   }
+  count_attention(counters, segments, q.rows, dh, heads);
   MultiHeadPartial out;
   {
-    Dev dq = upload_bf16(q);
-    Dev o(sizeof(float) * std::max<size_t>(static_cast<size_t>(q.rows) * q.cols, 1));
+    const int64_t W = static_cast<int64_t>(heads) * kDh;
+    Dev dq = upload_heads_bf16(q, heads, dh);
+    Dev o(sizeof(float) * std::max<size_t>(static_cast<size_t>(q.rows) * W, 1));
     Dev l(sizeof(float) * std::max<size_t>(static_cast<size_t>(q.rows) * heads, 1));
-    check(spava_attention(dq.p, q.cols, q.rows, segs.data(), static_cast<int>(segs.size()), heads,
-                          kv_heads, dh, o.p, q.cols, 1, l.as<float>(), 1, nullptr, 0, nullptr),
-          "mha_lse");
-    out.out = download_f32(o.p, q.rows, q.cols);
+    check(spava_attention_ex(dq.p, W, q.rows, segs.data(), static_cast<int>(segs.size()), heads, kv_heads, kDh,
+                             o.p, W, 1, l.as<float>(), 1, nullptr, 0, nullptr, scale),
+          what);
+    out.out = download_heads_f32(o.p, q.rows, heads, dh, kDh);
     out.lse = download_f32(l.p, q.rows, heads);
   }
   if (!allow_invalid_rows)
     for (int i = 0; i < q.rows; ++i)
-      if (!std::isfinite(out.lse.at(i, 0)))
-        throw std::invalid_argument("attention_lse: query row " + std::to_string(i) + " has no visible keys");
+      for (int h = 0; h < heads; ++h)
+        if (!std::isfinite(out.lse.at(i, h)))
+          throw std::invalid_argument("attention_lse: query row " + std::to_string(i) + " has no visible keys");
   return out;
+}
+
+// merge over parts given as device f32 [rows x heads*wp] / [rows x heads] (wp >= 32)
+Matrix merge_impl(const std::vector<const float*>& po, const std::vector<const float*>& pl, int rows, int heads,
+                  int dh, int wp) {
+  Matrix out;
+  int status = 0;
+  {
+    const int64_t W = static_cast<int64_t>(heads) * wp;
+    Dev o(sizeof(float) * std::max<size_t>(static_cast<size_t>(rows) * W, 1)), st(4);
+    cuda_check(cudaMemset(st.p, 0, 4), "memset");
+    check(spava_mha_merge(static_cast<int>(po.size()), po.data(), pl.data(), rows, W, heads, wp, o.p, W, 1,
+                          nullptr, st.as<int32_t>(), nullptr),
+          "merge_partials");
+    out = download_heads_f32(o.p, rows, heads, dh, wp);
+    cuda_check(cudaMemcpy(&status, st.p, 4, cudaMemcpyDeviceToHost), "D2H");
+  }
+  if (status) throw std::invalid_argument("merge_partials: a row is invalid in every part");
+  return out;
+}
+}  // namespace
+
+float invalid_lse() { return -std::numeric_limits<float>::infinity(); }
+bool AttnPartial::row_valid(int r) const { return std::isfinite(lse[r]); }
+
+AttnPartial attention_lse(const Matrix& q, std::span<const KeySegment> segments, float scale,
+                          bool allow_invalid_rows, CostCounters* counters) {
+  if (!(scale > 0.f) || !std::isfinite(scale)) throw std::invalid_argument("attention_lse: scale must be > 0");
+  MultiHeadPartial m = mha_impl(q, segments, 1, 1, scale, allow_invalid_rows, counters, "attention_lse");
+  AttnPartial p;
+  p.out = std::move(m.out);
+  p.lse.assign(m.lse.data.begin(), m.lse.data.end());
+  return p;
+}
+
+Matrix merge_partials(std::span<const AttnPartial> parts) {
+  if (parts.empty()) throw std::invalid_argument("merge_partials: empty part list");
+  const int rows = parts.front().out.rows, d = parts.front().out.cols;
+  if (d < 1 || d > 1024) throw std::invalid_argument("merge_partials: width 1..1024");
+  const int wp = std::max(d, 32);  // the merge kernel's minimum row width
+  std::vector<std::unique_ptr<Dev>> keep;
+  std::vector<const float*> po, pl;
+  for (const AttnPartial& p : parts) {
+    if (p.out.rows != rows || p.out.cols != d || static_cast<int>(p.lse.size()) != rows)
+      throw std::invalid_argument("merge_partials: part shape mismatch");
+    keep.push_back(std::make_unique<Dev>(upload_heads_f32(p.out, 1, d, wp)));
+    po.push_back(keep.back()->as<float>());
+    keep.push_back(std::make_unique<Dev>(upload_f32(p.lse.data(), p.lse.size())));
+    pl.push_back(keep.back()->as<float>());
+  }
+  return merge_impl(po, pl, rows, 1, d, wp);
+}
+
+MultiHeadPartial mha_lse(const Matrix& q, std::span<const KeySegment> segments, int heads,
+                         bool allow_invalid_rows, CostCounters* counters, int kv_heads) {
+  if (kv_heads <= 0) kv_heads = heads;
+  const int dh = head_dim(q.cols, heads, "mha_lse");
+  return mha_impl(q, segments, heads, kv_heads, 1.0f / std::sqrt(static_cast<float>(dh)), allow_invalid_rows,
+                  counters, "mha_lse");
 }
 
 Matrix mha_merge(std::span<const MultiHeadPartial> parts, int heads) {
   if (parts.empty()) throw std::invalid_argument("mha_merge: empty part list");
   const int rows = parts.front().out.rows, d = parts.front().out.cols;
   const int dh = head_dim(d, heads, "mha_merge");
+  const int wp = std::max(dh, 32);
   std::vector<std::unique_ptr<Dev>> keep;
   std::vector<const float*> po, pl;
   for (const MultiHeadPartial& p : parts) {
     if (p.out.rows != rows || p.out.cols != d || p.lse.rows != rows || p.lse.cols != heads)
       throw std::invalid_argument("merge_partials: part shape mismatch");
-    keep.push_back(std::make_unique<Dev>(upload_f32(p.out.data.data(), p.out.data.size())));
+    keep.push_back(std::make_unique<Dev>(upload_heads_f32(p.out, heads, dh, wp)));
     po.push_back(keep.back()->as<float>());
     keep.push_back(std::make_unique<Dev>(upload_f32(p.lse.data.data(), p.lse.data.size())));
     pl.push_back(keep.back()->as<float>());
   }
-  Matrix out;
-  int status = 0;
-  {
-    Dev o(sizeof(float) * std::max<size_t>(static_cast<size_t>(rows) * d, 1)), st(4);
-    cuda_check(cudaMemset(st.p, 0, 4), "memset");
-    check(spava_mha_merge(static_cast<int>(parts.size()), po.data(), pl.data(), rows, d, heads, dh,
-                          o.p, d, 1, nullptr, st.as<int32_t>(), nullptr),
-          "mha_merge");
-    out = download_f32(o.p, rows, d);
-    cuda_check(cudaMemcpy(&status, st.p, 4, cudaMemcpyDeviceToHost), "D2H");
-  }
-  if (status) throw std::invalid_argument("merge_partials: a row is invalid in every part");
-  return out;
+  return merge_impl(po, pl, rows, heads, dh, wp);
 }
 
 Matrix anchor_attention(const Matrix& q_a, const Matrix& k_a, const Matrix& v_a, int heads,
-                        int kv_heads) {
-  const KeySegment seg{&k_a, &v_a, MaskKind::CausalWithin, nullptr};
-  return mha_lse(q_a, std::span<const KeySegment>(&seg, 1), heads, false, kv_heads).out;
+                        CostCounters* counters, int kv_heads) {
+  const KeySegment seg{&k_a, &v_a, MaskKind::CausalWithin, nullptr, AttnSite::AnchorSelf};
+  return mha_lse(q_a, std::span<const KeySegment>(&seg, 1), heads, false, counters, kv_heads).out;
 }
 
 Matrix block_attention(const BlockQkv& block, const Matrix& k_a, const Matrix& v_a,
-                       const PassingAssembly& passing, int heads, int kv_heads) {
+                       const PassingAssembly& passing, int heads, CostCounters* counters, int kv_heads) {
   std::vector<KeySegment> segs;
-  if (k_a.rows > 0) segs.push_back({&k_a, &v_a, MaskKind::FullyVisible, nullptr});
-  if (passing.k.rows > 0) segs.push_back({&passing.k, &passing.v, MaskKind::FullyVisible, nullptr});
-  segs.push_back({&block.k, &block.v, MaskKind::CausalWithin, block.pad});
-  return mha_lse(block.q, segs, heads, /*allow_invalid_rows=*/true, kv_heads).out;
+  if (k_a.rows > 0) segs.push_back({&k_a, &v_a, MaskKind::FullyVisible, nullptr, AttnSite::BlockAnchor});
+  if (passing.k.rows > 0)
+    segs.push_back({&passing.k, &passing.v, MaskKind::FullyVisible, nullptr, AttnSite::BlockPassing});
+  segs.push_back({&block.k, &block.v, MaskKind::CausalWithin, block.pad, AttnSite::BlockOwn});
+  return mha_lse(block.q, segs, heads, /*allow_invalid_rows=*/true, counters, kv_heads).out;
 }
 
 MultiHeadPartial query_attention(const Matrix& q_qr, const Matrix& anchor_k,
                                  const Matrix& anchor_v, std::pair<int, int> anchor_slice,
                                  const BlockQkv& lo, const BlockQkv& hi, const Matrix* query_k,
                                  const Matrix* query_v, bool include_query_self, int heads,
-                                 int query_offset, std::vector<int>* key_indices, int kv_heads) {
+                                 int query_offset, std::vector<int>* key_indices, CostCounters* counters,
+                                 int kv_heads) {
   const int a0 = anchor_slice.first, a1 = anchor_slice.second;
   if (a0 < 0 || a1 < a0 || a1 > anchor_k.rows) throw std::invalid_argument("slice_rows out of range");
   Matrix ka(a1 - a0, anchor_k.cols), va(a1 - a0, anchor_v.cols);
@@ -348,10 +476,10 @@ MultiHeadPartial query_attention(const Matrix& q_qr, const Matrix& anchor_k,
     std::memcpy(va.data.data(), anchor_v.row(a0), sizeof(float) * va.data.size());
   }
   std::vector<KeySegment> segs;
-  if (ka.rows > 0) segs.push_back({&ka, &va, MaskKind::FullyVisible, nullptr});
-  segs.push_back({&lo.k, &lo.v, MaskKind::FullyVisible, lo.pad});
-  segs.push_back({&hi.k, &hi.v, MaskKind::FullyVisible, hi.pad});
-  if (include_query_self) segs.push_back({query_k, query_v, MaskKind::CausalWithin, nullptr});
+  if (ka.rows > 0) segs.push_back({&ka, &va, MaskKind::FullyVisible, nullptr, AttnSite::QueryAttn});
+  segs.push_back({&lo.k, &lo.v, MaskKind::FullyVisible, lo.pad, AttnSite::QueryAttn});
+  segs.push_back({&hi.k, &hi.v, MaskKind::FullyVisible, hi.pad, AttnSite::QueryAttn});
+  if (include_query_self) segs.push_back({query_k, query_v, MaskKind::CausalWithin, nullptr, AttnSite::QueryAttn});
   if (key_indices) {  // approx.cpp:174-185
     for (int i = a0; i < a1; ++i) key_indices->push_back(i);
     for (const BlockQkv* b : {&lo, &hi})
@@ -360,7 +488,7 @@ MultiHeadPartial query_attention(const Matrix& q_qr, const Matrix& anchor_k,
     if (include_query_self)
       for (int i = 0; i < q_qr.rows; ++i) key_indices->push_back(query_offset + i);
   }
-  return mha_lse(q_qr, segs, heads, /*allow_invalid_rows=*/true, kv_heads);
+  return mha_lse(q_qr, segs, heads, /*allow_invalid_rows=*/true, counters, kv_heads);
 }
 
 }  // namespace seqpar_b200

@@ -165,7 +165,7 @@ void attn_prof_read(unsigned long long* out16);  // dev: cycle counters of varia
 int attn_set_variant(int v);                     // dev: -1 = env/default, else variant id
 cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, int dh,
                              cudaStream_t stream, std::string* err, const MergeJob* job = nullptr,
-                             const ScoreJob* sj = nullptr);
+                             const ScoreJob* sj = nullptr, float scale = 0.f);
 
 // 2D bf16 [rows x cols] tensor map, box 64 cols x box_rows rows, 128B swizzle
 bool make_tmap_bf16(CUtensorMap* m, const void* base, long long rows, long long cols, long long ld,
@@ -177,11 +177,11 @@ cudaError_t launch_score_exact2(int nblk, const void* q, long long ldq, int n_t,
                                 const void* const* k, long long ldk, int l_b,
                                 const uint8_t* const* pad, const int* n_valid, int hq, int hkv,
                                 int dh, int softmax, float* const* scores, void* ws,
-                                size_t ws_bytes, cudaStream_t stream);
+                                size_t ws_bytes, cudaStream_t stream, float scale = 0.f);
 cudaError_t launch_score_exact(const void* q, long long ldq, int n_t, const void* k,
                                long long ldk, int l_b, const uint8_t* pad, int n_valid, int hq,
                                int hkv, int dh, int softmax, float* scores, void* ws,
-                               size_t ws_bytes, cudaStream_t stream);
+                               size_t ws_bytes, cudaStream_t stream, float scale = 0.f);
 
 // fast (tensor-core) scoring: same definition as score_block, logits from tcgen05 bf16
 // MMAs with fp32 accumulation (not bit-faithful; see score_fast.cu)

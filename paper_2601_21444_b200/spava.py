@@ -32,9 +32,9 @@ EXPORTED_SYMBOLS = [
     "spava_default_plan", "spava_virtual_pair", "spava_physical_of", "spava_slice_anchor",
     "spava_block_offset", "spava_query_offset", "spava_pad_mask", "spava_block_valid_rows",
     "spava_passing_ranges", "spava_split_rows", "spava_merge_rows",
-    "spava_score_workspace", "spava_score_block", "spava_score_fast_workspace",
+    "spava_score_workspace", "spava_score_block", "spava_score_block_ex", "spava_score_fast_workspace",
     "spava_score_block_fast", "spava_select_pack",
-    "spava_attention_workspace", "spava_attention", "spava_mha_merge",
+    "spava_attention_workspace", "spava_attention", "spava_attention_ex", "spava_mha_merge",
     "spava_fabric_create_local", "spava_nccl_unique_id", "spava_fabric_create_nccl",
     "spava_fabric_create_peer", "spava_fabric_peer_handle", "spava_fabric_peer_open",
     "spava_fabric_peer_attach", "spava_frame_partition", "spava_gather_split_rows",

@@ -42,10 +42,10 @@ static Matrix rnd(int r, int c, std::mt19937_64& g) {
 
 // per-head dense attention in fp64 over an explicit visible-key list (test_tensor.cpp:24-45)
 static Matrix naive(const Matrix& q, const Matrix& k, const Matrix& v, int heads, int kv_heads,
-                    const std::vector<std::vector<int>>& vis) {
-  const int dh = 128, g = heads / kv_heads;
+                    const std::vector<std::vector<int>>& vis, double scale = 0.0) {
+  const int dh = q.cols / heads, g = heads / kv_heads;
   Matrix out(q.rows, q.cols);
-  const double sc = 1.0 / std::sqrt(128.0);
+  const double sc = scale > 0 ? scale : 1.0 / std::sqrt(double(float(dh)));
   for (int h = 0; h < heads; ++h)
     for (int i = 0; i < q.rows; ++i) {
       std::vector<double> l;
@@ -155,7 +155,7 @@ int main() {
     const int n = 200, heads = 4, kvh = 2;
     Matrix q = rnd(n, heads * 128, gen), k = rnd(n, kvh * 128, gen), v = rnd(n, kvh * 128, gen);
     KeySegment seg{&k, &v, MaskKind::CausalWithin, nullptr};
-    MultiHeadPartial p = mha_lse(q, std::span<const KeySegment>(&seg, 1), heads, false, kvh);
+    MultiHeadPartial p = mha_lse(q, std::span<const KeySegment>(&seg, 1), heads, false, nullptr, kvh);
     std::vector<std::vector<int>> vis(n);
     for (int i = 0; i < n; ++i)
       for (int j = 0; j <= i; ++j) vis[i].push_back(j);
@@ -239,6 +239,101 @@ int main() {
     bool t3 = false;
     try { assemble_passing(3, blocks); } catch (const std::invalid_argument&) { t3 = true; }
     CHECK(t3);
+  }
+  // ---- test_partition.cpp:23-40 frame_partition closed forms and law
+  {
+    CHECK((frame_partition(64, 8) == std::vector<int>{8, 8, 8, 8, 8, 8, 8, 8}));
+    CHECK((frame_partition(10, 3) == std::vector<int>{4, 3, 3}));
+    CHECK((frame_partition(7, 8) == std::vector<int>{1, 1, 1, 1, 1, 1, 1, 0}));
+    bool t4 = false;
+    try { frame_partition(4, 0); } catch (const std::invalid_argument&) { t4 = true; }
+    CHECK(t4);
+    for (int f = 0; f <= 200; f += 7)
+      for (int h = 1; h <= 16; ++h) {
+        std::vector<int> c = frame_partition(f, h);
+        const auto [mn, mx] = std::minmax_element(c.begin(), c.end());
+        CHECK(std::accumulate(c.begin(), c.end(), 0) == f && *mx - *mn <= 1 && std::is_sorted(c.rbegin(), c.rend()));
+      }
+  }
+  // ---- acceptance.cpp:91-127 (criterion 2) as written: single-head attention_lse with
+  // d in [2, 12] over random disjoint key partitions, merge_partials == dense attention
+  // (narrow heads run zero-padded to 128 columns; bf16 tolerance)
+  {
+    int bad = 0;
+    for (uint64_t seed = 0; seed < 100; ++seed) {
+      std::mt19937_64 g2(seed);
+      std::uniform_int_distribution<int> nk_dist(2, 32), nq_dist(1, 6), d_dist(2, 12);
+      const int n_k = nk_dist(g2), n_q = nq_dist(g2), d = d_dist(g2);
+      Matrix q = rnd(n_q, d, g2), k = rnd(n_k, d, g2), v = rnd(n_k, d, g2);
+      const float scale = 1.0f / std::sqrt(static_cast<float>(d));
+      std::uniform_int_distribution<int> seg_dist(1, std::min(8, n_k));
+      const int segments = seg_dist(g2);
+      std::uniform_int_distribution<int> pick(0, segments - 1);
+      std::vector<int> assign(n_k);
+      for (int j = 0; j < n_k; ++j) assign[j] = j < segments ? j : pick(g2);
+      std::shuffle(assign.begin(), assign.end(), g2);
+      std::vector<AttnPartial> parts;
+      std::vector<Matrix> kss, vss;
+      for (int s2 = 0; s2 < segments; ++s2) {
+        std::vector<int> members;
+        for (int j = 0; j < n_k; ++j)
+          if (assign[j] == s2) members.push_back(j);
+        Matrix ks(static_cast<int>(members.size()), d), vs(static_cast<int>(members.size()), d);
+        for (size_t t = 0; t < members.size(); ++t)
+          for (int c = 0; c < d; ++c) {
+            ks.at(static_cast<int>(t), c) = k.at(members[t], c);
+            vs.at(static_cast<int>(t), c) = v.at(members[t], c);
+          }
+        kss.push_back(ks);
+        vss.push_back(vs);
+      }
+      for (int s2 = 0; s2 < segments; ++s2) {
+        KeySegment seg{&kss[s2], &vss[s2], MaskKind::FullyVisible, nullptr, AttnSite::Other};
+        parts.push_back(attention_lse(q, std::span<const KeySegment>(&seg, 1), scale));
+      }
+      std::vector<std::vector<int>> vis(n_q);
+      for (int i = 0; i < n_q; ++i)
+        for (int j = 0; j < n_k; ++j) vis[i].push_back(j);
+      if (max_abs(merge_partials(parts), naive(q, k, v, 1, 1, vis, scale)) > 1.5e-2f) ++bad;
+    }
+    CHECK(bad == 0);
+  }
+  // ---- acceptance criterion 1's head shape (d = 64, 4 heads: dh = 16): causal mha_lse
+  // and per-site FLOP counters (costs.hpp; attention.cpp:33-36)
+  {
+    const int n = 96, heads = 4, d = 64;
+    Matrix q = rnd(n, d, gen), k = rnd(n, d, gen), v = rnd(n, d, gen);
+    CostCounters cc;
+    Matrix o = anchor_attention(q, k, v, heads, &cc);
+    std::vector<std::vector<int>> vis(n);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j <= i; ++j) vis[i].push_back(j);
+    CHECK(max_abs(o, naive(q, k, v, heads, heads, vis)) < 1.5e-2f);
+    CHECK(cc.anchor_self == 2ull * n * n * d && cc.attention_total() == cc.anchor_self);
+    BlockQkv blk;
+    blk.q = rnd(40, d, gen);
+    blk.k = rnd(40, d, gen);
+    blk.v = rnd(40, d, gen);
+    PassingAssembly pa;
+    pa.k = rnd(12, d, gen);
+    pa.v = rnd(12, d, gen);
+    CostCounters cb;
+    block_attention(blk, k, v, pa, heads, &cb);
+    CHECK(cb.block_anchor == 4ull * 40 * n * d && cb.block_passing == 4ull * 40 * 12 * d &&
+          cb.block_own == 2ull * 40 * 40 * d && cb.balanced_total() == cb.block_passing + cb.block_own);
+  }
+  // ---- score_context (approx.hpp:38-41) closed form at d = 16, explicit scale; equal to
+  // score_block of one 16-wide head (same scale 1/sqrt(16)); Score counter
+  {
+    Matrix q(1, 16), k(2, 16);
+    q.at(0, 0) = 1.f;
+    k.at(1, 0) = bf(std::log(3.0f) * 4.f);
+    CostCounters cs;
+    ScoreVector s = score_context(q, k, 0.25f, nullptr, 3, true, &cs);
+    CHECK(std::fabs(s.scores[0] - 0.25f) < 2e-3f && std::fabs(s.scores[1] - 0.75f) < 2e-3f && s.source == 3);
+    CHECK(cs.score == 2ull * 1 * 2 * 16);
+    Matrix q2 = rnd(7, 16, gen), k2 = rnd(50, 16, gen);
+    CHECK(score_context(q2, k2, 0.25f, nullptr).scores == score_block(q2, k2, 1, nullptr).scores);
   }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "all seqpar_b200 checks passed", failures);
   return failures;
