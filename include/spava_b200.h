@@ -295,6 +295,10 @@ typedef struct {
   const float* g_2;
   int d_model, ffn, norm;
 } spava_decoder_weights;
+/* The decoder layer's GEMM (tcgen05, gemm.cu): row-major bf16 C[M x N] = A[M x K] B[K x N]
+ * (+ beta * C) (ReLU if relu), fp32 accumulation; strides and N multiples of 8.          */
+int spava_gemm(int M, int N, int K, const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
+               int64_t ldc, float beta, int relu, void* stream);
 size_t spava_decoder_workspace(const spava_host* host, const spava_decoder_weights* w);
 int spava_host_decoder_layer(spava_host* host, const spava_decoder_weights* w, void* x, int64_t ldx,
                              void* ws, size_t ws_bytes, void* stream);

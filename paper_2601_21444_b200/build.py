@@ -69,7 +69,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++20", "--expt-relaxed-constexpr",
            "-Xcompiler", "-fPIC,-O2", "-shared", "-I", inc, "-I", os.path.join(ROOT, "include"),
            *sources(), *objs, "-o", LIB + ".tmp", "-L", libdir, "-l:libnccl.so.2",
-           "-L/usr/local/cuda/lib64", "-lcublasLt",
            "-Xlinker", f"-rpath,{libdir}"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")

@@ -249,7 +249,6 @@ struct spava_host {
   // DelayInjection analogue: ns of spin before a phase on its stream (0 score/select on the
   // side stream, 1 exchange rounds on the comm stream, 2 query attention, 3 stage 1)
   unsigned long long delay_ns[4] = {0, 0, 0, 0};
-  void* gemm = nullptr;  // cuBLASLt handle of the decoder-layer GEMMs (lazy)
   // one captured layer (CUDA graph over the caller's, side and comm streams)
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
@@ -1457,7 +1456,6 @@ int spava_host_destroy(spava_host* H) {
   if (H->ev_sel) cudaEventDestroy(H->ev_sel);
   if (H->graph_exec) cudaGraphExecDestroy(H->graph_exec);
   if (H->graph) cudaGraphDestroy(H->graph);
-  gemm_handle_destroy(H->gemm);
   if (H->side) cudaStreamDestroy(H->side);
   if (H->side_lo) cudaStreamDestroy(H->side_lo);
   if (H->h2d) cudaStreamDestroy(H->h2d);
@@ -2036,9 +2034,8 @@ int spava_host_timing(spava_host* H, double* ms_by_class, double* attn_flops,
 }
 
 namespace {
-constexpr size_t kGemmWs = 32ull << 20;
 struct DecoderWs {
-  size_t xn, q, k, v, a, h, gemm, total;
+  size_t xn, q, k, v, a, h, total;
 };
 DecoderWs decoder_ws(const spava_host* H, const spava_decoder_weights* w) {
   const spava_layer_cfg& c = H->fab->cfg;
@@ -2053,11 +2050,26 @@ DecoderWs decoder_ws(const spava_host* H, const spava_decoder_weights* w) {
   d.v = o; o += al(rows * c.hkv * c.dh * 2);
   d.a = o; o += al(rows * c.hq * c.dh * 2);
   d.h = o; o += al(rows * static_cast<size_t>(w->ffn) * 2);
-  d.gemm = o; o += kGemmWs;
   d.total = o;
   return d;
 }
 }  // namespace
+
+int spava_gemm(int M, int N, int K, const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
+               int64_t ldc, float beta, int relu, void* stream) {
+  if (!A || !B || !C) return fail(SPAVA_EINVAL, "gemm: null argument");
+  ST_TRY(require_device());
+  std::string err;
+  const int col0 = 0;
+  const long long ldo = ldc;
+  const cudaError_t e = launch_gemm_bf16(M, N, K, A, lda, B, ldb, 1, &col0, &C, &ldo, beta, relu != 0,
+                                         as_stream(stream), &err);
+  if (e != cudaSuccess)
+    return fail(e == cudaErrorInvalidValue ? SPAVA_EINVAL : SPAVA_ECUDA,
+                "gemm: " + (err.empty() ? std::string(cudaGetErrorString(e)) : err));
+  ++g_launches;
+  return SPAVA_OK;
+}
 
 size_t spava_decoder_workspace(const spava_host* H, const spava_decoder_weights* w) {
   return (H && w) ? decoder_ws(H, w).total : 0;
@@ -2076,7 +2088,6 @@ int spava_host_decoder_layer(spava_host* H, const spava_decoder_weights* w, void
   const DecoderWs d = decoder_ws(H, w);
   if (ws_bytes < d.total) return fail(SPAVA_EINVAL, "decoder_layer: workspace too small");
   CU_TRY(cudaSetDevice(F->device));
-  if (!H->gemm && !(H->gemm = gemm_handle_create())) return fail(SPAVA_ECUDA, "decoder_layer: cublasLtCreate");
   const spava_layer_cfg& c = F->cfg;
   const spava_plan& p = F->plan;
   const int rows = p.l_a + 2 * p.l_b + p.n_t;
@@ -2089,13 +2100,21 @@ int spava_host_decoder_layer(spava_host* H, const spava_decoder_weights* w, void
   void* v = base + d.v;
   void* a = base + d.a;
   void* hbuf = base + d.h;
-  void* gws = base + d.gemm;
   std::string err;
+  auto G3 = [&](int M, int N, int K, const void* A, long long lda, const void* B, long long ldb, int nout,
+                const int* col0, void* const* outs, const long long* ldo, float beta, bool relu) -> int {
+    const cudaError_t e = launch_gemm_bf16(M, N, K, A, lda, B, ldb, nout, col0, outs, ldo, beta, relu, st, &err);
+    if (e != cudaSuccess)
+      return fail(e == cudaErrorInvalidValue ? SPAVA_EINVAL : SPAVA_ECUDA,
+                  "decoder_layer: " + (err.empty() ? std::string(cudaGetErrorString(e)) : err));
+    ++g_launches;
+    return SPAVA_OK;
+  };
   auto G = [&](int M, int N, int K, const void* A, long long lda, const void* B, long long ldb, void* Cm,
                long long ldc, float beta, bool relu) -> int {
-    const cudaError_t e = gemm_bf16_rm(H->gemm, M, N, K, A, lda, B, ldb, Cm, ldc, beta, relu, gws, kGemmWs, st, &err);
-    if (e != cudaSuccess) return fail(SPAVA_ECUDA, "decoder_layer: " + (err.empty() ? std::string(cudaGetErrorString(e)) : err));
-    return SPAVA_OK;
+    const int col0 = 0;
+    const long long ldo = ldc;
+    return G3(M, N, K, A, lda, B, ldb, 1, &col0, &Cm, &ldo, beta, relu);
   };
   const uint8_t* wq = static_cast<const uint8_t*>(w->w_qkv);
   // project (simhost.cpp:196-199): xn = layer_norm(x, g1); q, k, v = xn [Wq | Wk | Wv]
@@ -2106,9 +2125,12 @@ int spava_host_decoder_layer(spava_host* H, const spava_decoder_weights* w, void
     xin = xn;
     ldin = D;
   }
-  ST_TRY(G(rows, dq, D, xin, ldin, wq, wqkv, q, dq, 0.f, false));
-  ST_TRY(G(rows, dk, D, xin, ldin, wq + dq * 2, wqkv, k, dk, 0.f, false));
-  ST_TRY(G(rows, dk, D, xin, ldin, wq + (dq + dk) * 2, wqkv, v, dk, 0.f, false));
+  {  // one GEMM against [Wq | Wk | Wv], its epilogue routes the column ranges to q, k, v
+    const int col0[3] = {0, dq, dq + dk};
+    void* outs[3] = {q, k, v};
+    const long long ldo[3] = {dq, dk, dk};
+    ST_TRY(G3(rows, wqkv, D, xin, ldin, wq, wqkv, 3, col0, outs, ldo, 0.f, false));
+  }
   // Spava attention (the hot path)
   HostBufs b{static_cast<const uint8_t*>(q), static_cast<const uint8_t*>(k), static_cast<const uint8_t*>(v),
              static_cast<uint8_t*>(a), nullptr};
@@ -2124,7 +2146,7 @@ int spava_host_decoder_layer(spava_host* H, const spava_decoder_weights* w, void
   }
   ST_TRY(G(rows, w->ffn, D, fin, ldf, w->w_1, w->ffn, hbuf, w->ffn, 0.f, true));
   ST_TRY(G(rows, D, w->ffn, hbuf, w->ffn, w->w_2, D, x, ldx, 1.f, false));
-  g_launches += 6 + (w->norm ? 2 : 0);
+  g_launches += w->norm ? 2 : 0;
   return SPAVA_OK;
 }
 

@@ -245,11 +245,11 @@ cudaError_t launch_split_rows(int l_a, int l_b, int n_t, int n_v, int lo, int hi
 // ---------------------------------------------------------------- decoder layer (f2)
 cudaError_t launch_layer_norm(const void* x, long long ldx, const float* g, int d, void* y,
                               long long ldy, int rows, cudaStream_t stream);
-cudaError_t gemm_bf16_rm(void* lt, int M, int N, int K, const void* A, long long lda, const void* B,
-                         long long ldb, void* C, long long ldc, float beta, bool relu, void* ws,
-                         size_t ws_bytes, cudaStream_t stream, std::string* err);
-void* gemm_handle_create();
-void gemm_handle_destroy(void* h);
+// tcgen05 GEMM (gemm.cu): C (+)= A B row-major bf16, fp32 accumulation; C's column ranges
+// [col0[r], col0[r+1]) go to out[r] (stride ldo[r]); beta * C residual and ReLU epilogue
+cudaError_t launch_gemm_bf16(int M, int N, int K, const void* A, long long lda, const void* B, long long ldb,
+                             int nout, const int* col0, void* const* out, const long long* ldo, float beta,
+                             bool relu, cudaStream_t stream, std::string* err);
 
 // ---------------------------------------------------------------- merge
 cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream);

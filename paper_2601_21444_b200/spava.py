@@ -22,7 +22,7 @@ __all__ = [
     "virtual_pair", "physical_of", "slice_anchor", "block_offset", "query_offset", "pad_mask",
     "block_valid_rows", "passing_ranges", "score_block", "select_pack", "select_essential", "attention",
     "mha_merge", "anchor_attention", "block_attention", "query_attention", "nccl_unique_id",
-    "kernel_launches", "device_ok", "EXPORTED_SYMBOLS",
+    "kernel_launches", "device_ok", "EXPORTED_SYMBOLS", "gemm",
 ]
 
 EINVAL, ERANGE, ERUNTIME, ECUDA, ENCCL = 1, 2, 3, 4, 5
@@ -43,7 +43,7 @@ EXPORTED_SYMBOLS = [
     "spava_host_rows", "spava_host_layer", "spava_host_layer_hostbuf", "spava_sim_layer",
     "spava_sim_layer_timed", "spava_host_set_trace", "spava_host_trace_read",
     "spava_host_capture_layer", "spava_host_replay_layer", "spava_host_set_delay",
-    "spava_decoder_workspace", "spava_host_decoder_layer",
+    "spava_decoder_workspace", "spava_host_decoder_layer", "spava_gemm",
     "spava_host_status",
     "spava_host_set_timing", "spava_host_timing", "spava_kernel_launches",
     "spava_debug_attn_prof", "spava_debug_attn_variant", "spava_debug_fused_merge", "spava_debug_fused_score",
@@ -161,6 +161,8 @@ def lib():
                                              C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
         L.spava_attention_workspace.restype = C.c_size_t
         L.spava_attention_workspace.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+        L.spava_gemm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                 C.c_void_p, C.c_int64, C.c_float, C.c_int, C.c_void_p]
         L.spava_kernel_launches.restype = C.c_uint64
         L.spava_score_block.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64,
                                         C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -437,6 +439,24 @@ def select_essential(scores, l_p, global_offset=0, k=None, v=None):
         raise SpavaError(EINVAL, "select_essential: NaN score")
     n = int(cnt.item())
     return idx[:n], (kc[:n] if kc is not None else None), (vc[:n] if vc is not None else None)
+
+
+def gemm(a, b, out=None, beta=0.0, relu=False, stream=None):
+    """out = a @ b (+ beta * out) (ReLU), bf16 row-major, fp32 accumulation (tcgen05 kernel)."""
+    import torch
+
+    _require(a, torch.bfloat16, "a")
+    _require(b, torch.bfloat16, "b")
+    M, K = a.shape
+    K2, N = b.shape
+    if K2 != K:
+        raise SpavaError(EINVAL, "gemm: inner dimensions differ")
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.bfloat16, device=a.device)
+    _require(out, torch.bfloat16, "out")
+    _check(lib().spava_gemm(M, N, K, _ptr(a), a.stride(0), _ptr(b), b.stride(0), _ptr(out), out.stride(0),
+                            float(beta), int(bool(relu)), _stream(stream)))
+    return out
 
 
 def attention(q, segments, hq, hkv, dh=128, out_f32=False, want_lse=False, splits=1, stream=None):

@@ -421,3 +421,31 @@ def test_needle_keys_are_selected(cuda, fast):
     if not fast:
         ref = O.score_block(q, k, hq, hkv, 128, None, True)
         assert idx == set(O.select_essential(ref, l_p, 0).tolist())
+
+
+@pytest.mark.parametrize("M,N,K,beta,relu", [
+    (1000, 2560, 512, 0.0, False),   # ragged rows, fused-QKV width
+    (384, 256, 1024, 1.0, False),    # residual epilogue (x += a Wo)
+    (300, 776, 200, 0.0, True),      # ragged N (last tile 8 wide) and K, ReLU
+    (4096, 2048, 2048, 0.5, True),   # multi-tile persistent schedule
+])
+def test_gemm_matches_fp32_reference(cuda, M, N, K, beta, relu):
+    """f2's tcgen05 GEMM against a plain PyTorch fp32 reference of the same op on the same
+    bf16 inputs: |err| <= 1 bf16 ulp of the output plus the fp32-accumulation slack."""
+    import torch
+
+    from paper_2601_21444_b200 import spava
+
+    g = torch.Generator(device=cuda).manual_seed(M + N + K)
+    a = torch.randn(M, K, device=cuda, generator=g).to(torch.bfloat16)
+    b = (torch.randn(K, N, device=cuda, generator=g) * K ** -0.5).to(torch.bfloat16)
+    c0 = torch.randn(M, N, device=cuda, generator=g).to(torch.bfloat16)
+    out = c0.clone()
+    spava.gemm(a, b, out, beta=beta, relu=relu)
+    torch.cuda.synchronize()
+    ref = a.float() @ b.float() + beta * c0.float()
+    if relu:
+        ref = ref.clamp_min(0)
+    err = (out.float() - ref).abs()
+    tol = 1e-2 + 2 ** -8 * ref.abs()
+    assert bool((err <= tol).all()), float(err.max())
