@@ -57,6 +57,30 @@ def test_score_block_matches_oracle(cuda, n_t, l_b, hq, hkv, n_valid, softmax):
         assert np.array_equal(idx.cpu().numpy(), want)
 
 
+def test_score_block_explicit_pad_mask(cuda):
+    """score_context's pad_mask (approx.cpp:32-66) as an explicit mask: scattered pads,
+    one logits tile entirely padded, the key holding a row's max padded."""
+    from paper_2601_21444_b200 import spava
+
+    n_t, l_b, hq, hkv = 64, 700, 8, 2
+    rng = np.random.default_rng(11)
+    q = randn(rng, n_t, hq * 128)
+    k = randn(rng, l_b, hkv * 128)
+    pad = (rng.random(l_b) < 0.2).astype(np.uint8)
+    pad[256:384] = 1  # the whole third 128-key tile
+    ref0 = O.score_block(q, k, hq, hkv, 128, None, True)
+    pad[int(np.argmax(ref0))] = 1
+    ref = O.score_block(q, k, hq, hkv, 128, pad, True)
+    got = host(spava.score_block(dev(q, cuda), dev(k, cuda), hq, hkv, 128, pad=pad, softmax=True))
+    assert np.array_equal(np.isinf(got), np.isinf(ref))
+    fin = np.isfinite(ref)
+    assert ulp_diff(got[fin], ref[fin]) <= 4
+    for l_p in (1, 50, int(fin.sum())):
+        want = O.select_essential(ref, l_p, 0)
+        idx, _, _ = spava.select_essential(spava_t(got, cuda), l_p, 0)
+        assert np.array_equal(idx.cpu().numpy(), want)
+
+
 @pytest.mark.parametrize("n_t,l_b,hq,hkv,n_valid", [
     (128, 1000, 16, 2, 1000),
     (128, 3000, 16, 2, 2950),   # padded tail, ragged last tile
