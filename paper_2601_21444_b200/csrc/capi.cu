@@ -226,7 +226,7 @@ struct spava_host {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   // row-chunk pipeline: q rows of block lo / hi arrive in kCopyChunks chunks each; the
   // stage-1/2 attention runs per chunk and each chunk's output leaves as soon as it is final
-  static constexpr int kCopyChunks = 5;
+  static constexpr int kCopyChunks = 16;  // capacity; copy_edges picks the count
   cudaEvent_t ev_kvq = nullptr;                  // all k and the query rows of q are on device (scorer)
   cudaEvent_t ev_vhi = nullptr;                  // v rows of block hi and the query are on device
   cudaEvent_t ev_qc[2 * kCopyChunks] = {};       // q rows of chunk c (chunk 0 of lo + anchor)
@@ -462,6 +462,41 @@ bool fused_score(const spava_host* H, bool cp_on) {
 
 // scores: 0 = launch the scorer here; 1 = produced earlier on this stream (fused query
 // launch); 2 = produced on another stream, wait for H->ev_score
+// dev: SPAVA_HOSTBUF_TIMELINE=1 prints when each copy / chunk of one host-buffer layer ends
+// (ms after the fork point; synchronises -- never set while timing)
+struct Timeline {
+  bool on = false;
+  std::vector<std::pair<std::string, cudaEvent_t>> ev;
+  void mark(const std::string& name, cudaStream_t s) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.emplace_back(name, e);
+  }
+  void dump() {
+    if (!on || ev.empty()) return;
+    cudaDeviceSynchronize();
+    for (auto& [n, e] : ev) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[0].second, e);
+      fprintf(stderr, "timeline %-14s %8.3f ms\n", n.c_str(), ms);
+    }
+    for (auto& pe : ev) cudaEventDestroy(pe.second);
+    ev.clear();
+  }
+};
+Timeline& timeline() {
+  static Timeline t;
+  static bool init = [] {
+    const char* e = getenv("SPAVA_HOSTBUF_TIMELINE");
+    t.on = e && atoi(e) != 0;
+    return true;
+  }();
+  (void)init;
+  return t;
+}
+
 int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record,
                  cudaEvent_t before_hi = nullptr, int scores = 0) {
   const spava_fabric& F = *H->fab;
@@ -492,6 +527,7 @@ int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record,
       g_launches += c.softmax_scores ? 3 : 2;
     }
     span(H, 1, t0, st);
+    timeline().mark("score done", st);
   }
   // both blocks in one select and one gather launch, unless select hi must wait for its
   // v rows (host-buffer pipeline) -- then lo goes first so pass1 is not held back
@@ -537,6 +573,7 @@ int phase_select(spava_host* H, const HostBufs& b, cudaStream_t st, bool record,
     g_launches += p.l_p > 0 ? 2 : 1;
     span(H, 2, t0, st);
     for (int r = r0; r < r0 + per; ++r) ST_TRY(finish(r));
+    timeline().mark(per == 2 ? "select lo+hi done" : r0 == 0 ? "select lo done" : "select hi done", st);
   }
   trace_ev(H, st, kComputeEnd, "score", false);
   return SPAVA_OK;
@@ -1485,6 +1522,7 @@ int spava_host_rows(const spava_host* H) {
   return p.l_a + 2 * p.l_b + p.n_t;
 }
 
+
 namespace {
 
 // Optional host<->device copy pipeline around one layer: each compute phase waits only for
@@ -1492,28 +1530,44 @@ namespace {
 // phases still run (ev_out).  Inputs arrive in the order the phases need them.
 struct CopyEdges {
   bool on = false;
+  int n = 0;                                  // row chunks per block
   int cb[spava_host::kCopyChunks + 1] = {};  // row bounds of the block chunks
 };
 
 CopyEdges copy_edges(const spava_plan& p) {
   // uneven row chunks (multiples of 256 rows, one ping-pong CTA unit): block lo runs its
   // chunks in row order and block hi in REVERSE order, so the first output is ready early
-  // (small first lo chunk) and the last chunk to arrive is the smallest and lightest
-  // (causal rows [0, l_b/16) of hi) -- the tail after the last H2D byte is short
-  static constexpr int kFrac16[spava_host::kCopyChunks + 1] = {0, 1, 4, 8, 12, 16};
+  // (small first lo chunks) and the last chunks to arrive are the smallest and lightest
+  // (causal rows [0, l_b/16) of hi) -- the tail after the last H2D byte is short.  Eleven
+  // chunks per block keep the D2H stream fed between chunks (C1 e2e 4.19 -> 4.11 ms against
+  // five, tools/e2e_chunks.sh).  SPAVA_COPY_CHUNKS="0,..,32" (fractions of 32, dev A/B)
+  // overrides the table.
+  static const std::vector<int> frac = [] {
+    std::vector<int> f = {0, 1, 2, 4, 6, 8, 12, 16, 20, 24, 28, 32};
+    if (const char* e = getenv("SPAVA_COPY_CHUNKS")) {
+      std::vector<int> g;
+      for (const char* c = e; *c;) {
+        g.push_back(atoi(c));
+        while (*c && *c != ',') ++c;
+        if (*c) ++c;
+      }
+      if (g.size() >= 2 && g.size() <= spava_host::kCopyChunks + 1 && g.front() == 0 && g.back() == 32) f = g;
+    }
+    return f;
+  }();
   CopyEdges cp;
   cp.on = true;
-  const int n = spava_host::kCopyChunks;
-  for (int c = 0; c <= n; ++c) {
-    const long long r = (static_cast<long long>(p.l_b) * kFrac16[c] / 16 + 255) / 256 * 256;
+  cp.n = static_cast<int>(frac.size()) - 1;
+  for (int c = 0; c <= cp.n; ++c) {
+    const long long r = (static_cast<long long>(p.l_b) * frac[c] / 32 + 255) / 256 * 256;
     cp.cb[c] = static_cast<int>(std::min<long long>(r, p.l_b));
   }
-  cp.cb[n] = p.l_b;
+  cp.cb[cp.n] = p.l_b;
   return cp;
 }
 
 // row chunk of block `which` processed at position k (hi runs in reverse)
-inline int chunk_of(int which, int k) { return which == 0 ? k : spava_host::kCopyChunks - 1 - k; }
+inline int chunk_of(const CopyEdges& cp, int which, int k) { return which == 0 ? k : cp.n - 1 - k; }
 
 // stage 1 / stage 2 as row chunks (copy pipeline) or whole blocks; events are indexed by
 // processing position
@@ -1521,9 +1575,9 @@ int stage_chunks(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEd
                  bool with_merge = false) {
   if (!cp.on) return which == 0 ? phase_stage1(H, b, st) : phase_stage2(H, b, st, with_merge);
   const spava_layer_cfg& c = H->fab->cfg;
-  const int n = spava_host::kCopyChunks;
+  const int n = cp.n;
   for (int k = 0; k < n; ++k) {
-    const int idx = which * n + k, rc = chunk_of(which, k);
+    const int idx = which * n + k, rc = chunk_of(cp, which, k);
     CU_TRY(cudaStreamWaitEvent(st, H->ev_qc[idx], 0));
     const bool anchor = which == 0 && k == 0 && H->fab->plan.l_a > 0;  // anchor with lo chunk 0
     if (cp.cb[rc + 1] > cp.cb[rc]) {
@@ -1542,7 +1596,7 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
   spava_fabric* F = H->fab;
   cudaStream_t ss = H->serial ? st : cp.on ? H->side_lo : H->side;
   auto merged = [&](cudaStream_t s) -> cudaError_t {
-    return cp.on ? cudaEventRecord(H->ev_oc[2 * spava_host::kCopyChunks], s) : cudaSuccess;
+    return cp.on ? cudaEventRecord(H->ev_oc[2 * cp.n], s) : cudaSuccess;
   };
   // trace records follow run_host's overlapped program order (simhost.cpp:343-426)
   auto T = [&](cudaStream_t s, int kind, const char* label, bool comm = false) {
@@ -1574,6 +1628,7 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     if (fscore) ST_TRY(query(ss));
     ST_TRY(phase_select(H, b, ss, false, before_hi, fscore ? 1 : 0));
     CU_TRY(cudaEventRecord(H->ev_sel, ss));
+    timeline().mark("select done", ss);
     T(ss, kCommIssued, "pass1", true);
     T(ss, kCommIssued, "pass2", true);
     if (!cp.on && !fscore) ST_TRY(query(st));
@@ -1583,10 +1638,13 @@ int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdge
     T(st, kComputeBegin, "stage1");
     ST_TRY(stage_chunks(H, b, st, cp, 0));
     T(st, kComputeEnd, "stage1");
+    timeline().mark("stage1 done", st);
     if (cp.on) ST_TRY(query(st));
+    timeline().mark("query done", st);
     T(st, kCommWaitStart, "pass2", true);
     CU_TRY(cudaStreamWaitEvent(st, H->ev_sel, 0));
     T(st, kCommCompleted, "pass2", true);
+    timeline().mark("stage2 start", st);
     // the merge of the query partial(s) rides in the stage-2 launch (trailing CTAs)
     const bool fused = !cp.on && fused_merge_enabled();
     T(st, kComputeBegin, "stage2");
@@ -1714,42 +1772,6 @@ int spava_host_layer(spava_host* H, const void* q, const void* k, const void* v,
   return layer_impl(H, b, as_stream(stream), CopyEdges{});
 }
 
-namespace {
-// dev: SPAVA_HOSTBUF_TIMELINE=1 prints when each copy / chunk of one host-buffer layer ends
-// (ms after the fork point; synchronises -- never set while timing)
-struct Timeline {
-  bool on = false;
-  std::vector<std::pair<std::string, cudaEvent_t>> ev;
-  void mark(const std::string& name, cudaStream_t s) {
-    if (!on) return;
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    cudaEventRecord(e, s);
-    ev.emplace_back(name, e);
-  }
-  void dump() {
-    if (!on || ev.empty()) return;
-    cudaDeviceSynchronize();
-    for (auto& [n, e] : ev) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ev[0].second, e);
-      fprintf(stderr, "timeline %-14s %8.3f ms\n", n.c_str(), ms);
-    }
-    for (auto& pe : ev) cudaEventDestroy(pe.second);
-    ev.clear();
-  }
-};
-Timeline& timeline() {
-  static Timeline t;
-  static bool init = [] {
-    const char* e = getenv("SPAVA_HOSTBUF_TIMELINE");
-    t.on = e && atoi(e) != 0;
-    return true;
-  }();
-  (void)init;
-  return t;
-}
-}  // namespace
 
 int spava_host_layer_hostbuf(spava_host* H, const void* q_h, const void* k_h, const void* v_h,
                              void* out_h, int32_t* sel_h, void* q_d, void* k_d, void* v_d,
@@ -1777,7 +1799,7 @@ int spava_host_layer_hostbuf(spava_host* H, const void* q_h, const void* k_h, co
   //   [hi | query] (ev_kvq: the scorer starts)  ->  q lo chunks 1..  ->  v of [hi | query]
   //   (ev_vhi: select hi, query attention)  ->  q hi chunks, heaviest (last rows) first
   const CopyEdges cp = copy_edges(p);
-  const int nc = spava_host::kCopyChunks;
+  const int nc = cp.n;
   const size_t lo_rows = lo_end, rest = rows - lo_end;
   Timeline& TL = timeline();
   auto* kd = static_cast<uint8_t*>(k_d);
@@ -1786,7 +1808,7 @@ int spava_host_layer_hostbuf(spava_host* H, const void* q_h, const void* k_h, co
   const auto* vh = static_cast<const uint8_t*>(v_h);
   // q rows of the chunk at processing position idx (chunk 0 of block lo carries the anchor)
   auto chunk_rows = [&](int idx, size_t* r0, size_t* r1) {
-    const int which = idx / nc, c = chunk_of(which, idx % nc);
+    const int which = idx / nc, c = chunk_of(cp, which, idx % nc);
     const size_t base = static_cast<size_t>(p.l_a) + static_cast<size_t>(which) * p.l_b;
     *r0 = (which == 0 && c == 0) ? 0 : base + cp.cb[c];
     *r1 = base + cp.cb[c + 1];
