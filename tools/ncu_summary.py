@@ -24,6 +24,8 @@ want = {
     "fp64_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "issue_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "dram_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "l2_pct": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "l1_pct": "l1tex__throughput.avg.pct_of_peak_sustained_active",
     "regs": "launch__registers_per_thread",
     "grid": "launch__grid_size",
 }
@@ -60,9 +62,10 @@ summary[cfg] = {"dram_bytes_per_launch": attn["dram_bytes_per_launch"] if attn e
 json.dump(summary, open(out + ".json", "w"), indent=1)
 with open(out + ".txt", "w") as f:
     f.write(f"ncu --set full, one bench step ({cfg}); cold-cache serialized replays\n")
-    f.write(f"{'kernel':22s} {'us':>9s} {'DRAM MB':>9s} {'tensor%':>8s} {'xu%':>6s} {'fma%':>6s} {'fp64%':>6s} {'issue%':>7s} {'dram%':>6s} regs grid\n")
+    f.write(f"{'kernel':22s} {'us':>9s} {'DRAM MB':>9s} {'tensor%':>8s} {'xu%':>6s} {'fma%':>6s} {'fp64%':>6s} {'issue%':>7s} {'dram%':>6s} {'l2%':>6s} {'l1%':>6s} regs grid\n")
     for k in kern:
         f.write(f"{k['kernel'][:22]:22s} {k['time_us']:9.1f} {((k['dram_read'] or 0)+(k['dram_write'] or 0))/1e6:9.1f} "
                 f"{k['tensor_pipe_pct'] or 0:8.1f} {k['xu_pct'] or 0:6.1f} {k['fma_pct'] or 0:6.1f} {k['fp64_pct'] or 0:6.1f} "
-                f"{k['issue_pct'] or 0:7.1f} {k['dram_pct'] or 0:6.1f} {int(k['regs'] or 0):4d} {int(k['grid'] or 0)}\n")
+                f"{k['issue_pct'] or 0:7.1f} {k['dram_pct'] or 0:6.1f} {k['l2_pct'] or 0:6.1f} {k['l1_pct'] or 0:6.1f} "
+                f"{int(k['regs'] or 0):4d} {int(k['grid'] or 0)}\n")
 print(open(out + ".txt").read())
