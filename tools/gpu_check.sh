@@ -12,4 +12,4 @@ if [ "$1" = "ncu" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
      python bench.py --steps 2 --warmup 3 --no-cpu --no-extras > gpurun_out/b_ncu.log 2>&1
 fi
-tail -3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; cat gpurun_out/bench.json gpurun_out/bench_ref.json
+tail -n 3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; cat gpurun_out/bench.json gpurun_out/bench_ref.json
