@@ -70,6 +70,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xcompiler", "-fPIC,-O2", "-shared", "-I", inc, "-I", os.path.join(ROOT, "include"),
            *sources(), *objs, "-o", LIB + ".tmp", "-L", libdir, "-l:libnccl.so.2",
            "-Xlinker", f"-rpath,{libdir}"]
+    if os.environ.get("SPAVA_DEV_VARIANTS") == "1":  # A/B kernel variants (dev build only)
+        cmd.insert(1, "-DSPAVA_DEV_VARIANTS")
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -867,8 +867,11 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
   // the ping-pong kernel (2 Q tiles per CTA, 320 threads) with different template switches.
   using KFn = void (*)(AttnParams);
   struct Var { KFn fn; uint32_t smem; int threads = kThreads; };
+  // Only the production kernel ships; the A/B variants are compiled into a
+  // dev build only (SPAVA_DEV_VARIANTS=1 python -m paper_2601_21444_b200.build --force).
   static const Var variants[] = {
       {attn_fwd_kernel<0, 2, false, true, false, 4>, Smem<2>::bytes},  // 0 production: P in 4 key ranges
+#ifdef SPAVA_DEV_VARIANTS
       {attn_fwd_kernel<0, 2, true, true, false, 4>, Smem<2>::bytes},   // 1 0 + cycle counters
       {attn_fwd_kernel<0, 2, false, true, false, 1>, Smem<2>::bytes},  // 2 round-1 kernel (P whole)
       {attn_fwd_kernel<0, 2, false, true, false, 2>, Smem<2>::bytes},  // 3 P in 2 key ranges
@@ -882,7 +885,9 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
       {attn_fwd_kernel<0, 2, false, true, false, 4, 0, true>, Smem<2>::bytes},    // 11 0 + exp phases alternate
       {attn_fwd_kernel<0, 2, false, true, false, 4, 0, false, true>, Smem<2>::bytes},  // 12 0 + split S load
       {attn_fwd_kernel<0, 2, false, true, false, 4, 0, true, true>, Smem<2>::bytes},   // 13 11 + 12
-      {attn_fwd_kernel<4, 2, false, true, false, 4, 224, true, true>, Smem<2>::bytes, 384}};  // 14 13 + setmaxnreg + 25% FMA exp2
+      {attn_fwd_kernel<4, 2, false, true, false, 4, 224, true, true>, Smem<2>::bytes, 384},  // 14 13 + setmaxnreg + 25% FMA exp2
+#endif
+  };
   constexpr int kNumVar = sizeof(variants) / sizeof(variants[0]);
   static_assert(kNumVar <= 32, "attr mask");
   static const int env_sel = [] {
@@ -983,7 +988,12 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
 }
 
 int attn_set_variant(int v) {
-  if (v < -1 || v > 14) return -1;
+#ifdef SPAVA_DEV_VARIANTS
+  constexpr int kBuilt = 15;
+#else
+  constexpr int kBuilt = 1;
+#endif
+  if (v < -1 || v >= kBuilt) return -1;
   g_attn_variant.store(v);
   return 0;
 }

@@ -904,7 +904,7 @@ int spava_debug_fused_merge(int on) {
 }
 
 int spava_debug_attn_variant(int variant) {
-  if (attn_set_variant(variant) != 0) return fail(SPAVA_EINVAL, "attn_variant: -1 or 0..14");
+  if (attn_set_variant(variant) != 0) return fail(SPAVA_EINVAL, "attn_variant: -1, 0, or 1..14 in a dev build (SPAVA_DEV_VARIANTS=1)");
   return SPAVA_OK;
 }
 
