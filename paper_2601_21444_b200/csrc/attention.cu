@@ -500,16 +500,16 @@ __global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
             for (int j = 0; j < 8; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * a);
             tmem_st8(tO + 8 * c, o);
           }
-          return;
-        }
+        } else {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t o[32];
-          tmem_ld32(tO + 32 * c, o);
-          tmem_wait_ld();
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tO + 32 * c, o);
+            tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * a);
-          tmem_st32(tO + 32 * c, o);
+            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * a);
+            tmem_st32(tO + 32 * c, o);
+          }
         }
       };
       float mxp[8];
