@@ -13,9 +13,10 @@
 // fp64 normaliser sum_hi (a tree here) and (b) the fp64 exp (table+polynomial, <=1 ulp,
 // vs glibc); both
 // move p only when it lies within ~1e-15 of an fp32 rounding midpoint.
-// p = float(e/sum) is evaluated as e*(1/sum) with an exact-division fallback whenever
-// the product lands within a few fp64 ulps of an fp32 midpoint (or in fp32 subnormals),
-// so it equals the correctly rounded quotient.
+// p = float(e/sum) is evaluated as e*(1/sum) with a cheaper degree-5 exp and certified:
+// accepted only when the result is provably on the same side of the fp32 rounding midpoint
+// as the true quotient, else recomputed with the accurate exp and a true division
+// (prob_cert), so it equals the correctly rounded quotient.
 //
 // Kernels (both blocks of a host in one launch each):
 //   logits_kernel   : 128x128 CUDA-core SGEMM tile per CTA (8x8 register micro-tiles
@@ -100,6 +101,26 @@ __device__ __forceinline__ double exp_neg(double x, const double* tab) {
   double p = fma(c_expk[4], r, c_expk[5]);
   p = fma(p, r, c_expk[6]);
   p = fma(p, r, c_expk[7]);
+  p = fma(p, r, c_expk[8]);
+  p = fma(p, r, c_expk[9]);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const double y = p * tab[k & 15];
+  return __hiloint2double(__double2hiint(y) + ((k >> 4) << 20), __double2loint(y));
+}
+
+// exp(x) to a relative error below 1.5e-13 for -111 <= x <= 0: exp_neg with the Taylor
+// polynomial cut at degree 5 (truncation (ln2/32)^6/720 = 1.4e-13; two DFMAs fewer).  Used
+// only where the result is certified afterwards (prob_cert): that window is wide enough
+// for this error, so every probability it accepts is the correctly rounded quotient --
+// the same bits the accurate path gives.
+__device__ __forceinline__ double exp_neg5(double x, const double* tab) {
+  const double t = fma(x, c_expk[0], c_expk[1]);
+  const double kd = t - c_expk[1];
+  const int k = __double2loint(t);
+  double r = fma(kd, c_expk[2], x);
+  r = fma(kd, c_expk[3], r);
+  double p = fma(c_expk[6], r, c_expk[7]);  // 1/120 r + 1/24
   p = fma(p, r, c_expk[8]);
   p = fma(p, r, c_expk[9]);
   p = fma(p, r, 1.0);
@@ -419,13 +440,16 @@ __device__ __forceinline__ float lthr_of(const double* st) {
   return __int_as_float(__double2loint(st[3]));
 }
 
-// float(e / sum) evaluated as e*(1/sum): exact unless the product lies within 8 fp64 ulps
-// of an fp32 rounding midpoint or below FLT_MIN (a different rounding grid); those lanes
-// report `redo` and are recomputed with a true division (rare).
-__device__ __forceinline__ float prob_fast(double e, double rinv, bool& redo) {
+// float(e / sum) from an exp_neg5 value, certified: y = e*(1/sum) is within 1.5e-13 relative
+// of the true quotient q = exp(x)/sum, i.e. within ~1.4e3 fp64 ulps of y.  Outside a
+// +-2048-ulp window around the fp32 rounding midpoint (29 bits below the fp32 mantissa)
+// float(y) == float(q); inside it (probability 2^-17) or below FLT_MIN the caller
+// recomputes with the accurate exp and a true division -- exactly what the accurate path
+// does there, so accepted and recomputed probabilities are the bits the accurate path gives.
+__device__ __forceinline__ float prob_cert(double e, double rinv, bool& redo) {
   const double y = __dmul_rn(e, rinv);
   const unsigned low = static_cast<unsigned>(__double2loint(y)) & ((1u << 29) - 1);
-  redo |= (low - ((1u << 28) - 7)) < 15u || y < 1.1754943508222875e-38;
+  redo |= (low - ((1u << 28) - 2048)) < 4096u || y < 1.1754943508222875e-38;
   return __double2float_rn(y);
 }
 
@@ -483,7 +507,7 @@ __global__ void __launch_bounds__(kColWarps * 32) colsum_kernel(const __grid_con
         bool redo = false;
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          p[u] = prob_fast(exp_neg(xrel(l[u], thr_of(i + u), sc, mx_of(i + u)), tab), rinv_of(i + u), redo);
+          p[u] = prob_cert(exp_neg5(xrel(l[u], thr_of(i + u), sc, mx_of(i + u)), tab), rinv_of(i + u), redo);
         if (redo) {
 #pragma unroll 1
           for (int u = 0; u < 8; ++u) {
