@@ -239,6 +239,30 @@ def test_score_closed_form(cuda):
     assert np.allclose(s2, 2 * s, rtol=1e-6)
 
 
+@pytest.mark.parametrize("amp", [3.0, 6.0])
+def test_score_wide_range_fallbacks(cuda, amp):
+    """Large-magnitude logits: probabilities spread over many binades, many below FLT_MIN
+    and many clamped (x - mx < -110), so the column sum's certified fast path hands a large
+    share of elements to its accurate exp + division fallback.  Scores must still match
+    the reference to a few ulp and select identically."""
+    from paper_2601_21444_b200 import spava
+
+    n_t, l_b, hq, hkv = 32, 900, 4, 2
+    rng = np.random.default_rng(int(amp * 10))
+    q = bf16(randn(rng, n_t, hq * 128) * amp)
+    k = bf16(randn(rng, l_b, hkv * 128) * amp)
+    ref = O.score_block(q, k, hq, hkv, 128, None, True)
+    got = host(spava.score_block(dev(q, cuda), dev(k, cuda), hq, hkv, 128))
+    fin = np.isfinite(ref)
+    assert fin.all()
+    assert ulp_diff(got, ref) <= 4
+    assert float(np.mean(got == ref)) > 0.95
+    for l_p in (1, 16, 200):
+        want = O.select_essential(ref, l_p, 0)
+        idx, _, _ = spava.select_essential(spava_t(got, cuda), l_p, 0)
+        assert np.array_equal(idx.cpu().numpy(), want)
+
+
 # ---------------------------------------------------------------- selection
 def test_select_examples(cuda):
     """test_approx.cpp:90-105."""
