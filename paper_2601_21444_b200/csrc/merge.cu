@@ -26,6 +26,7 @@ __global__ void merge_kernel(const __grid_constant__ MergeParams p) {
   const int i = blockIdx.x, h = blockIdx.y, c = threadIdx.x;
   if (threadIdx.x < 32) {
     merge_weights_warp(p, i, h, w, &ok_sh, &lse_sh);
+    __syncwarp();  // lane 0 wrote ok_sh
     if (threadIdx.x == 0 && !ok_sh && p.status) atomicOr(p.status, 4);
   }
   __syncthreads();
