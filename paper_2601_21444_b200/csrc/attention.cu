@@ -31,6 +31,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "fabric_dev.cuh"
 #include "ptx.cuh"
@@ -611,27 +612,37 @@ __global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
             if (qt == 0 ? (k >= 1 && k - 1 < n_min) : (k < n_min)) named_bar_sync(qt == 0 ? 2 : 1, 256);
           }
           const long long te0 = PROF_NOW();
-          chunk_exp_ip(0, negm, mode == kFull);
+          // the exp phase is instantiated twice when some exps go to the FMA pipe (kEmu):
+          // fully visible tiles take the mixed MUFU / polynomial body, partial tiles the
+          // MUFU-only one -- one uniform branch per tile, none inside the unrolled body
+          auto exp_phase = [&](auto emu_tag) {
+            constexpr bool kE = decltype(emu_tag)::value;
+            chunk_exp_ip(0, negm, kE);
 #pragma unroll
-          for (int c = 1; c < 4; ++c) {
-            chunk_exp_ip(c, negm, mode == kFull);
-            if (kSeq && c == 3) {  // exps done: hand the MUFUs to the other warpgroup
-              // warpgroup 0's turn k is awaited by warpgroup 1 iff k < n_min; warpgroup 1's
-              // turn k by warpgroup 0 iff k < n_min and warpgroup 0 has a turn k + 1
-              if (qt == 0 ? (k < n_min) : (k < n_min && k + 1 < n_ot)) named_bar_arrive(qt == 0 ? 1 : 2, 256);
+            for (int c = 1; c < 4; ++c) {
+              chunk_exp_ip(c, negm, kE);
+              if (kSeq && c == 3) {  // exps done: hand the MUFUs to the other warpgroup
+                // warpgroup 0's turn k is awaited by warpgroup 1 iff k < n_min; warpgroup 1's
+                // turn k by warpgroup 0 iff k < n_min and warpgroup 0 has a turn k + 1
+                if (qt == 0 ? (k < n_min) : (k < n_min && k + 1 < n_ot)) named_bar_arrive(qt == 0 ? 1 : 2, 256);
+              }
+              chunk_pack(c - 1, sacc);
+              tmem_st16(tS + 16 * (c - 1), pk[c - 1]);
+              if (c % kCpp == 0) {
+                const long long ts0 = PROF_NOW();
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(p_full + 4 * qt + c / kCpp - 1);
+                if (kProf) pr[11] += PROF_NOW() - ts0;
+              }
             }
-            chunk_pack(c - 1, sacc);
-            tmem_st16(tS + 16 * (c - 1), pk[c - 1]);
-            if (c % kCpp == 0) {
-              const long long ts0 = PROF_NOW();
-              tmem_wait_st();
-              tc_fence_before();
-              mbar_arrive(p_full + 4 * qt + c / kCpp - 1);
-              if (kProf) pr[11] += PROF_NOW() - ts0;
-            }
-          }
-          chunk_pack(3, sacc);
-          tmem_st16(tS + 48, pk[3]);
+            chunk_pack(3, sacc);
+            tmem_st16(tS + 48, pk[3]);
+          };
+          if (kEmu > 0 && mode == kFull)
+            exp_phase(std::true_type{});
+          else
+            exp_phase(std::false_type{});
           if (kProf) pr[10] += PROF_NOW() - te0;
         } else if constexpr (kPipe) {
           chunk_exp_ip(0, negm, mode == kFull);
