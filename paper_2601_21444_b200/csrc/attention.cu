@@ -808,6 +808,768 @@ __global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
 #undef TILE_HEAD
 }
 
+#ifdef SPAVA_DEV_VARIANTS
+// ---------------------------------------------------------------------------------------
+// CTA-pair form (2-SM tcgen05.mma.cta_group::2): a cluster of two CTAs computes two q-heads
+// of one KV group over the same 256 rows, so both see the same segment / causal tile
+// sequence.  The rank-0 CTA issues every MMA for the pair (M = 256: each CTA's own Q tile
+// rows, D in each CTA's TMEM); the B operand is split along N -- each CTA loads and holds
+// half of every K tile (64 keys) and half of every V tile (64 of the 128 dh columns) -- so
+// K/V TMA traffic, smem footprint and the MMA's smem operand reads per SM are halved.
+// Commits multicast to both CTAs; P readiness is counted on the rank-0 CTA's barriers by
+// the softmax threads of both.  The softmax / epilogue code is the production kernel's.
+constexpr uint32_t kHalfTile = kTileBytes / 2;  // 64 keys x 128 dh (K half) or 128 keys x 64 dh (V half)
+template <int KS>
+struct SmemP {
+  static constexpr uint32_t q = 0;
+  static constexpr uint32_t k = q + kTilesPerCta * kTileBytes;
+  static constexpr uint32_t v = k + KS * kHalfTile;
+  static constexpr uint32_t bar = v + KS * kHalfTile;
+  static constexpr uint32_t total = bar + 256;
+  static constexpr uint32_t bytes = total + 1024;
+};
+
+constexpr int kPairStages = 4;  // K / V half-tile ring depth of the pair kernel
+template <int KS>
+__global__ void __launch_bounds__(kThreads, 1) attn_pair_kernel(const __grid_constant__ AttnParams P) {
+  constexpr int kPParts = 4;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  using SL = SmemP<KS>;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SL::bar);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;        // [KS]   counted on rank 0
+  uint64_t* k_empty = k_full + KS;    // [KS]   both CTAs (multicast commit)
+  uint64_t* v_full = k_empty + KS;    // [KS]   rank 0
+  uint64_t* v_empty = v_full + KS;    // [KS]   both
+  uint64_t* s_full = v_empty + KS;    // [2]    both
+  uint64_t* p_full = s_full + 2;      // [2][4] rank 0, 256 arrivals (both CTAs' softmax)
+  uint64_t* o_full = p_full + 8;      // [2]    both
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+  static_assert((1 + 4 * KS + 12) * 8 + 4 <= 256, "barrier area");
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int warp = warp_id();
+  const int lane = lane_id();
+
+  // ---- decode the pair's work item: problem, 256-row unit (heaviest first), head group, split
+  const int w = static_cast<int>(blockIdx.x >> 1);
+  int pi = 0;
+  while (pi + 1 < P.nprob && w >= P.prob[pi + 1].work_begin) ++pi;
+  const AttnProb& prob = P.prob[pi];
+  int local = w - prob.work_begin;
+  const int split = local % prob.splits;
+  local /= prob.splits;
+  const int pair = prob.head_pair;  // nq <= 128: a CTA's two Q tiles are heads h, h+1
+  const int ngroups = pair ? P.hq / 4 : P.hq / 2;
+  const int g = local % ngroups;
+  local /= ngroups;
+  const int head = pair ? 4 * g + 2 * static_cast<int>(rank) : 2 * g + static_cast<int>(rank);
+  const int unit = prob.units - 1 - local;
+  const int i0 = pair ? 0 : unit * (kTilesPerCta * kBlockM);
+  const int nq = prob.nq;
+  const int imax = min(i0 + (pair ? kBlockM : kTilesPerCta * kBlockM), nq);
+  const int hk = head / (P.hq / P.hkv);
+#define TILE_R0(t) (pair ? 0 : i0 + (t) * kBlockM)
+#define TILE_HEAD(t) (head + pair * (t))
+  int T = 0;
+  for (int s = 0; s < prob.nseg; ++s) T += seg_tiles(prob.seg[s], imax);
+  const int t_begin = static_cast<int>(static_cast<long long>(T) * split / prob.splits);
+  const int t_end = static_cast<int>(static_cast<long long>(T) * (split + 1) / prob.splits);
+  const int ntiles = t_end - t_begin;
+  const CUtensorMap* tm = P.tmap[pi];  // [0] Q, [1+2s] K (64-key boxes), [2+2s] V
+
+  if (warp == kProducerWarp && elect_one()) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < KS; ++s) {
+      mbar_init(k_full + s, 1);
+      mbar_init(k_empty + s, 1);
+      mbar_init(v_full + s, 1);
+      mbar_init(v_empty + s, 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(s_full + t, 1);
+      for (int pp = 0; pp < kPParts; ++pp) mbar_init(p_full + 4 * t + pp, 256);
+      mbar_init(o_full + t, 1);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tm[0]);
+    for (int s = 0; s < prob.nseg; ++s) {
+      tma_prefetch_desc(&tm[1 + 2 * s]);
+      tma_prefetch_desc(&tm[2 + 2 * s]);
+    }
+  }
+  if (warp == kMmaWarp) tmem_alloc2(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // both CTAs' barriers exist before any remote arrive / TMA signal
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kProducerWarp) {
+    // ======================================================== TMA producer (both CTAs)
+    if (elect_one()) {
+      const bool has1 = TILE_R0(1) < nq;
+      if (leader) mbar_expect_tx(q_full, 2u * (has1 ? 2u : 1u) * kTileBytes);
+      for (int qt = 0; qt < (has1 ? 2 : 1); ++qt)
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d_pair(smem + SL::q + qt * kTileBytes + c * kBoxBytes, &tm[0], q_full,
+                           TILE_HEAD(qt) * kHeadDim + c * 64, TILE_R0(qt));
+      Cursor cur = cursor_at(prob, imax, t_begin);
+      for (int it = 0; it < ntiles; ++it) {
+        const CUtensorMap* km = &tm[1 + 2 * cur.seg];
+        const CUtensorMap* vm = &tm[2 + 2 * cur.seg];
+        const int st = it % KS;
+        if (it >= KS) mbar_wait(k_empty + st, ((it / KS) - 1) & 1);
+        if (leader) mbar_expect_tx(k_full + st, kTileBytes);  // both halves
+        for (int c = 0; c < 2; ++c)  // keys [kt*128 + rank*64, +64), dh half c
+          tma_load_2d_pair(smem + SL::k + st * kHalfTile + c * (kBoxBytes / 2), km, k_full + st,
+                           hk * kHeadDim + c * 64, cur.kt * kBlockN + static_cast<int>(rank) * 64);
+        if (it >= KS) mbar_wait(v_empty + st, ((it / KS) - 1) & 1);
+        if (leader) mbar_expect_tx(v_full + st, kTileBytes);
+        tma_load_2d_pair(smem + SL::v + st * kHalfTile, vm, v_full + st,
+                         hk * kHeadDim + static_cast<int>(rank) * 64, cur.kt * kBlockN);  // dh half `rank`
+        cursor_next(prob, imax, cur);
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ======================================================== MMA issuer (rank 0 for the pair)
+    if (leader && elect_one()) {
+      const uint32_t idesc_qk = idesc_bf16_f32(256, 128, 0, 0);
+      const uint32_t idesc_pv = idesc_bf16_f32(256, 128, 0, 1);
+      const uint32_t sq = smem_u32(smem + SL::q);
+      const uint32_t sk = smem_u32(smem + SL::k);
+      const uint32_t sv = smem_u32(smem + SL::v);
+      auto issue_qk = [&](int qt, int stage) {
+        const uint32_t d = tmem + qt * 128;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t a = sdesc_sw128(sq + qt * kTileBytes + (kk >> 2) * kBoxBytes + (kk & 3) * 32, 16, 1024);
+          const uint64_t b = sdesc_sw128(sk + stage * kHalfTile + (kk >> 2) * (kBoxBytes / 2) + (kk & 3) * 32, 16, 1024);
+          mma_ss2(d, a, b, idesc_qk, kk > 0 ? 1u : 0u);
+        }
+      };
+      auto issue_pv = [&](int qt, int stage, bool acc, int kk0, int n) {
+        const uint32_t d = tmem + 256 + qt * 128;
+        const uint32_t a = tmem + qt * 128;
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+          const int kk = kk0 + k;
+          const uint64_t b = sdesc_sw128(sv + stage * kHalfTile + kk * 2048, kHalfTile, 1024);
+          mma_ts2(d, a + kk * 8, b, idesc_pv, (acc || kk > 0) ? 1u : 0u);
+        }
+      };
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      Cursor cur = cursor_at(prob, imax, t_begin);
+      int mode[2] = {kSkip, kSkip};
+      uint32_t p_cnt[2] = {0, 0};
+      bool o_acc[2] = {false, false};
+      if (ntiles > 0) {
+        for (int qt = 0; qt < 2; ++qt) mode[qt] = tile_mode(prob.seg[cur.seg], cur.kt, TILE_R0(qt), nq);
+        mbar_wait(k_full + 0, 0);
+        tc_fence_after();
+        for (int qt = 0; qt < 2; ++qt)
+          if (mode[qt] != kSkip) {
+            issue_qk(qt, 0);
+            tc_commit_pair(s_full + qt);
+          }
+        tc_commit_pair(k_empty + 0);
+      }
+      for (int it = 0; it < ntiles; ++it) {
+        const int st = it % KS;
+        const bool has_next = it + 1 < ntiles;
+        Cursor nxt = cur;
+        int nmode[2] = {kSkip, kSkip};
+        const int kn = (it + 1) % KS;
+        if (has_next) {
+          cursor_next(prob, imax, nxt);
+          for (int qt = 0; qt < 2; ++qt) nmode[qt] = tile_mode(prob.seg[nxt.seg], nxt.kt, TILE_R0(qt), nq);
+          mbar_wait(k_full + kn, ((it + 1) / KS) & 1);
+        }
+        mbar_wait(v_full + st, (it / KS) & 1);
+        tc_fence_after();
+        for (int qt = 0; qt < 2; ++qt) {
+          if (mode[qt] != kSkip) {
+#pragma unroll
+            for (int pp = 0; pp < kPParts; ++pp) {
+              mbar_wait(p_full + 4 * qt + pp, p_cnt[qt] & 1);
+              tc_fence_after();
+              issue_pv(qt, st, o_acc[qt], pp * (8 / kPParts), 8 / kPParts);
+            }
+            o_acc[qt] = true;
+            ++p_cnt[qt];
+            tc_commit_pair(o_full + qt);
+          }
+          if (qt == 1) tc_commit_pair(v_empty + st);
+          if (nmode[qt] != kSkip) {
+            issue_qk(qt, kn);
+            tc_commit_pair(s_full + qt);
+          }
+        }
+        if (has_next) tc_commit_pair(k_empty + kn);
+        cur = nxt;
+        mode[0] = nmode[0];
+        mode[1] = nmode[1];
+      }
+    }
+  } else {
+    // ======================================================== softmax warpgroups (both CTAs)
+    const int qt = warp >> 2;
+    const int quad = warp & 3;
+    const int row = TILE_R0(qt) + quad * 32 + lane;
+    const int qhead = TILE_HEAD(qt);
+    const uint32_t t_lane = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t tS = tmem + t_lane + qt * 128;
+    const uint32_t tO = tmem + t_lane + 256 + qt * 128;
+    const float sl2 = P.scale_log2;
+    const float2 sl2v = make_float2(sl2, sl2);
+    float m_ref = -INFINITY, l = 0.f;
+    uint32_t cnt = 0;
+    Cursor cur = cursor_at(prob, imax, t_begin);
+    for (int it = 0; it < ntiles; ++it, cursor_next(prob, imax, cur)) {
+      const AttnSeg sg = prob.seg[cur.seg];
+      const int mode = tile_mode(sg, cur.kt, TILE_R0(qt), nq);
+      if (mode == kSkip) continue;
+      mbar_wait(s_full + qt, cnt & 1);
+      tc_fence_after();
+      uint32_t sr[4][32];
+      uint32_t pk[4][16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tS + 32 * c, sr[c]);
+      tmem_wait_ld();
+      if (mode == kPart) {
+        const int k0 = cur.kt * kBlockN;
+        int lim = sg.len - k0;
+        if (sg.causal) lim = min(lim, row - k0 + 1);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c * 32 + j >= lim) sr[c][j] = __float_as_uint(-INFINITY);
+      }
+      float mxp[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const int t = (j / 2) & 7;
+          mxp[t] = fmaxf(mxp[t], fmaxf(__uint_as_float(sr[c][j]), __uint_as_float(sr[c][j + 1])));
+        }
+      const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                             fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+      float alpha = 1.f;
+      bool rescale = false;
+      const float m_new = fmaxf(m_ref, mx * sl2);
+      if (m_new > m_ref + 8.f) {
+        alpha = exp2f(m_ref - m_new);
+        m_ref = m_new;
+        rescale = true;
+      }
+      const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+      const float2 negm = make_float2(-m_use, -m_use);
+      if (rescale && cnt > 0) {
+        mbar_wait(o_full + qt, (cnt - 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 16; ++c) {
+          uint32_t o[8];
+          tmem_ld8(tO + 8 * c, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
+          tmem_st8(tO + 8 * c, o);
+        }
+      }
+      float2 sacc[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
+      auto chunk_exp = [&](int c) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 x2 = __ffma2_rn(
+              make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1])), sl2v, negm);
+          sr[c][2 * j] = __float_as_uint(fast_exp2(x2.x));
+          sr[c][2 * j + 1] = __float_as_uint(fast_exp2(x2.y));
+        }
+      };
+      auto chunk_pack = [&](int c) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 p2 = make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1]));
+          sacc[j & 3] = __fadd2_rn(sacc[j & 3], p2);
+          __nv_bfloat162 b = __floats2bfloat162_rn(p2.x, p2.y);
+          pk[c][j] = *reinterpret_cast<uint32_t*>(&b);
+        }
+      };
+      chunk_exp(0);
+#pragma unroll
+      for (int c = 1; c < 4; ++c) {
+        chunk_exp(c);
+        chunk_pack(c - 1);
+        tmem_st16(tS + 16 * (c - 1), pk[c - 1]);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive_leader(p_full + 4 * qt + c - 1);
+      }
+      chunk_pack(3);
+      tmem_st16(tS + 48, pk[3]);
+      const float2 sum2 = __fadd2_rn(__fadd2_rn(sacc[0], sacc[1]), __fadd2_rn(sacc[2], sacc[3]));
+      l = l * alpha + (sum2.x + sum2.y);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive_leader(p_full + 4 * qt + 3);
+      ++cnt;
+    }
+    // ---- epilogue: O / l, lse
+    if (cnt > 0) {
+      mbar_wait(o_full + qt, (cnt - 1) & 1);
+      tc_fence_after();
+    }
+    const bool valid_row = row < nq;
+    const float inv = (l > 0.f) ? 1.f / l : 0.f;
+    const long long obase = static_cast<long long>(split) * prob.split_stride_out +
+                            static_cast<long long>(row) * prob.ldo + qhead * kHeadDim;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t o[32];
+      if (cnt > 0) {
+        tmem_ld32(tO + 32 * c, o);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o[j] = 0u;
+      }
+      if (valid_row) {
+        if (prob.out_f32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(prob.out) + obase + 32 * c);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(__uint_as_float(o[4 * j]) * inv, __uint_as_float(o[4 * j + 1]) * inv,
+                                 __uint_as_float(o[4 * j + 2]) * inv, __uint_as_float(o[4 * j + 3]) * inv);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(prob.out) + obase + 32 * c);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t wv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(o[8 * j + 2 * e]) * inv,
+                                                       __uint_as_float(o[8 * j + 2 * e + 1]) * inv);
+              wv[e] = *reinterpret_cast<uint32_t*>(&b);
+            }
+            dst[j] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+          }
+        }
+      }
+    }
+    if (valid_row && prob.lse) {
+      const float lse = (l > 0.f) ? (m_ref + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+      prob.lse[static_cast<long long>(split) * prob.split_stride_lse + static_cast<long long>(row) * prob.ld_lse +
+               qhead] = lse;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the pair's last MMAs (issued by rank 0) are done with both TMEMs
+  tc_fence_after();
+  if (warp == kMmaWarp) tmem_dealloc2(tmem, kTmemCols);
+#undef TILE_R0
+#undef TILE_HEAD
+}
+
+template <int KS>
+struct SmemPS {
+  static constexpr uint32_t q = 0;
+  static constexpr uint32_t k = q + kTilesPerCta * kTileBytes;
+  static constexpr uint32_t v = k + KS * kHalfTile;
+  static constexpr uint32_t p = v + KS * kHalfTile;  // P_0 | P_1, 32 KB each
+  static constexpr uint32_t bar = p + kTilesPerCta * kTileBytes;
+  static constexpr uint32_t total = bar + 256;
+  static constexpr uint32_t bytes = total + 1024;
+};
+
+// Pair kernel with P in shared memory (SS PV): S_t is free as soon as the softmax has read
+// it, so QK_t(j+1) no longer waits for PV_t(j) -- the softmax -> PV -> QK chain of the
+// TMEM-aliased form is cut; the halved B operands leave the smem bandwidth for P.
+template <int KS>
+__global__ void __launch_bounds__(kThreads, 1) attn_pair_ps_kernel(const __grid_constant__ AttnParams P) {
+  constexpr int kPParts = 4;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  using SL = SmemPS<KS>;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SL::bar);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;        // [KS]   counted on rank 0
+  uint64_t* k_empty = k_full + KS;    // [KS]   both CTAs (multicast commit)
+  uint64_t* v_full = k_empty + KS;    // [KS]   rank 0
+  uint64_t* v_empty = v_full + KS;    // [KS]   both
+  uint64_t* s_full = v_empty + KS;    // [2]    both
+  uint64_t* p_full = s_full + 2;      // [2][4] rank 0, 256 arrivals (both CTAs' softmax)
+  uint64_t* o_full = p_full + 8;      // [2]    both: PV done (O landed, P buffer free)
+  uint64_t* s_free = o_full + 2;      // [2]    rank 0, 256 arrivals: S loaded by both CTAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + 2);
+  static_assert((1 + 4 * KS + 14) * 8 + 4 <= 256, "barrier area");
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int warp = warp_id();
+  const int lane = lane_id();
+
+  // ---- decode the pair's work item: problem, 256-row unit (heaviest first), head group, split
+  const int w = static_cast<int>(blockIdx.x >> 1);
+  int pi = 0;
+  while (pi + 1 < P.nprob && w >= P.prob[pi + 1].work_begin) ++pi;
+  const AttnProb& prob = P.prob[pi];
+  int local = w - prob.work_begin;
+  const int split = local % prob.splits;
+  local /= prob.splits;
+  const int pair = prob.head_pair;  // nq <= 128: a CTA's two Q tiles are heads h, h+1
+  const int ngroups = pair ? P.hq / 4 : P.hq / 2;
+  const int g = local % ngroups;
+  local /= ngroups;
+  const int head = pair ? 4 * g + 2 * static_cast<int>(rank) : 2 * g + static_cast<int>(rank);
+  const int unit = prob.units - 1 - local;
+  const int i0 = pair ? 0 : unit * (kTilesPerCta * kBlockM);
+  const int nq = prob.nq;
+  const int imax = min(i0 + (pair ? kBlockM : kTilesPerCta * kBlockM), nq);
+  const int hk = head / (P.hq / P.hkv);
+#define TILE_R0(t) (pair ? 0 : i0 + (t) * kBlockM)
+#define TILE_HEAD(t) (head + pair * (t))
+  int T = 0;
+  for (int s = 0; s < prob.nseg; ++s) T += seg_tiles(prob.seg[s], imax);
+  const int t_begin = static_cast<int>(static_cast<long long>(T) * split / prob.splits);
+  const int t_end = static_cast<int>(static_cast<long long>(T) * (split + 1) / prob.splits);
+  const int ntiles = t_end - t_begin;
+  const CUtensorMap* tm = P.tmap[pi];  // [0] Q, [1+2s] K (64-key boxes), [2+2s] V
+
+  if (warp == kProducerWarp && elect_one()) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < KS; ++s) {
+      mbar_init(k_full + s, 1);
+      mbar_init(k_empty + s, 1);
+      mbar_init(v_full + s, 1);
+      mbar_init(v_empty + s, 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(s_full + t, 1);
+      for (int pp = 0; pp < kPParts; ++pp) mbar_init(p_full + 4 * t + pp, 256);
+      mbar_init(o_full + t, 1);
+      mbar_init(s_free + t, 256);
+    }
+    fence_barrier_init();
+    tma_prefetch_desc(&tm[0]);
+    for (int s = 0; s < prob.nseg; ++s) {
+      tma_prefetch_desc(&tm[1 + 2 * s]);
+      tma_prefetch_desc(&tm[2 + 2 * s]);
+    }
+  }
+  if (warp == kMmaWarp) tmem_alloc2(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // both CTAs' barriers exist before any remote arrive / TMA signal
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kProducerWarp) {
+    // ======================================================== TMA producer (both CTAs)
+    if (elect_one()) {
+      const bool has1 = TILE_R0(1) < nq;
+      if (leader) mbar_expect_tx(q_full, 2u * (has1 ? 2u : 1u) * kTileBytes);
+      for (int qt = 0; qt < (has1 ? 2 : 1); ++qt)
+        for (int c = 0; c < 2; ++c)
+          tma_load_2d_pair(smem + SL::q + qt * kTileBytes + c * kBoxBytes, &tm[0], q_full,
+                           TILE_HEAD(qt) * kHeadDim + c * 64, TILE_R0(qt));
+      Cursor cur = cursor_at(prob, imax, t_begin);
+      for (int it = 0; it < ntiles; ++it) {
+        const CUtensorMap* km = &tm[1 + 2 * cur.seg];
+        const CUtensorMap* vm = &tm[2 + 2 * cur.seg];
+        const int st = it % KS;
+        if (it >= KS) mbar_wait(k_empty + st, ((it / KS) - 1) & 1);
+        if (leader) mbar_expect_tx(k_full + st, kTileBytes);  // both halves
+        for (int c = 0; c < 2; ++c)  // keys [kt*128 + rank*64, +64), dh half c
+          tma_load_2d_pair(smem + SL::k + st * kHalfTile + c * (kBoxBytes / 2), km, k_full + st,
+                           hk * kHeadDim + c * 64, cur.kt * kBlockN + static_cast<int>(rank) * 64);
+        if (it >= KS) mbar_wait(v_empty + st, ((it / KS) - 1) & 1);
+        if (leader) mbar_expect_tx(v_full + st, kTileBytes);
+        tma_load_2d_pair(smem + SL::v + st * kHalfTile, vm, v_full + st,
+                         hk * kHeadDim + static_cast<int>(rank) * 64, cur.kt * kBlockN);  // dh half `rank`
+        cursor_next(prob, imax, cur);
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ======================================================== MMA issuer (rank 0 for the pair)
+    if (leader && elect_one()) {
+      const uint32_t idesc_qk = idesc_bf16_f32(256, 128, 0, 0);
+      const uint32_t idesc_pv = idesc_bf16_f32(256, 128, 0, 1);
+      const uint32_t sq = smem_u32(smem + SL::q);
+      const uint32_t sk = smem_u32(smem + SL::k);
+      const uint32_t sv = smem_u32(smem + SL::v);
+      auto issue_qk = [&](int qt, int stage) {
+        const uint32_t d = tmem + qt * 128;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t a = sdesc_sw128(sq + qt * kTileBytes + (kk >> 2) * kBoxBytes + (kk & 3) * 32, 16, 1024);
+          const uint64_t b = sdesc_sw128(sk + stage * kHalfTile + (kk >> 2) * (kBoxBytes / 2) + (kk & 3) * 32, 16, 1024);
+          mma_ss2(d, a, b, idesc_qk, kk > 0 ? 1u : 0u);
+        }
+      };
+      auto issue_pv = [&](int qt, int stage, bool acc, int kk0, int n) {
+        const uint32_t d = tmem + 256 + qt * 128;
+        const uint32_t a = tmem + qt * 128;
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+          const int kk = kk0 + k;
+          const uint64_t b = sdesc_sw128(sv + stage * kHalfTile + kk * 2048, kHalfTile, 1024);
+          mma_ts2(d, a + kk * 8, b, idesc_pv, (acc || kk > 0) ? 1u : 0u);
+        }
+      };
+      const uint32_t sp = smem_u32(smem + SL::p);
+      // PV with P from shared memory (SS): A = P_t, laid out like a Q tile
+      auto issue_pv_s = [&](int qt, int stage, bool acc, int kk0, int n) {
+        const uint32_t d = tmem + 256 + qt * 128;
+#pragma unroll
+        for (int k = 0; k < n; ++k) {
+          const int kk = kk0 + k;
+          const uint64_t a = sdesc_sw128(sp + qt * kTileBytes + (kk >> 2) * kBoxBytes + (kk & 3) * 32, 16, 1024);
+          const uint64_t b = sdesc_sw128(sv + stage * kHalfTile + kk * 2048, kHalfTile, 1024);
+          mma_ss2(d, a, b, idesc_pv, (acc || kk > 0) ? 1u : 0u);
+        }
+      };
+      (void)issue_pv;
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      // step j: QK(j) of both Q tiles as soon as K(j) is in and the softmax has LOADED S(j-1)
+      // (P lives in shared memory, so S is free right after its tcgen05.ld), then PV(j-1)
+      Cursor cur = cursor_at(prob, imax, t_begin);
+      int mode_prev[2] = {kSkip, kSkip};
+      uint32_t n_qk[2] = {0, 0}, p_cnt[2] = {0, 0};
+      bool o_acc[2] = {false, false};
+      auto pv_step = [&](int jj) {  // PV of tile jj (ring slot jj % KS)
+        const int st = jj % KS;
+        mbar_wait(v_full + st, (jj / KS) & 1);
+        tc_fence_after();
+        for (int qt = 0; qt < 2; ++qt)
+          if (mode_prev[qt] != kSkip) {
+#pragma unroll
+            for (int pp = 0; pp < kPParts; ++pp) {
+              mbar_wait(p_full + 4 * qt + pp, p_cnt[qt] & 1);
+              tc_fence_after();
+              issue_pv_s(qt, st, o_acc[qt], pp * (8 / kPParts), 8 / kPParts);
+            }
+            o_acc[qt] = true;
+            ++p_cnt[qt];
+            tc_commit_pair(o_full + qt);
+          }
+        tc_commit_pair(v_empty + st);
+      };
+      for (int it = 0; it < ntiles; ++it, cursor_next(prob, imax, cur)) {
+        const int st = it % KS;
+        int mode[2];
+        for (int qt = 0; qt < 2; ++qt) mode[qt] = tile_mode(prob.seg[cur.seg], cur.kt, TILE_R0(qt), nq);
+        mbar_wait(k_full + st, (it / KS) & 1);
+        tc_fence_after();
+        for (int qt = 0; qt < 2; ++qt)
+          if (mode[qt] != kSkip) {
+            if (n_qk[qt] > 0) {
+              mbar_wait(s_free + qt, (n_qk[qt] - 1) & 1);
+              tc_fence_after();
+            }
+            issue_qk(qt, st);
+            tc_commit_pair(s_full + qt);
+            ++n_qk[qt];
+          }
+        tc_commit_pair(k_empty + st);
+        if (it > 0) pv_step(it - 1);
+        mode_prev[0] = mode[0];
+        mode_prev[1] = mode[1];
+      }
+      if (ntiles > 0) pv_step(ntiles - 1);
+    }
+  } else {
+    // ======================================================== softmax warpgroups (both CTAs)
+    const int qt = warp >> 2;
+    const int quad = warp & 3;
+    const int row = TILE_R0(qt) + quad * 32 + lane;
+    const int qhead = TILE_HEAD(qt);
+    const uint32_t t_lane = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t tS = tmem + t_lane + qt * 128;
+    const uint32_t tO = tmem + t_lane + 256 + qt * 128;
+    const float sl2 = P.scale_log2;
+    const float2 sl2v = make_float2(sl2, sl2);
+    float m_ref = -INFINITY, l = 0.f;
+    uint32_t cnt = 0;
+    Cursor cur = cursor_at(prob, imax, t_begin);
+    for (int it = 0; it < ntiles; ++it, cursor_next(prob, imax, cur)) {
+      const AttnSeg sg = prob.seg[cur.seg];
+      const int mode = tile_mode(sg, cur.kt, TILE_R0(qt), nq);
+      if (mode == kSkip) continue;
+      mbar_wait(s_full + qt, cnt & 1);
+      tc_fence_after();
+      uint32_t sr[4][32];
+      uint32_t pk[4][16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(tS + 32 * c, sr[c]);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive_leader(s_free + qt);  // S is in registers: QK(next) may overwrite it
+      if (mode == kPart) {
+        const int k0 = cur.kt * kBlockN;
+        int lim = sg.len - k0;
+        if (sg.causal) lim = min(lim, row - k0 + 1);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c * 32 + j >= lim) sr[c][j] = __float_as_uint(-INFINITY);
+      }
+      float mxp[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const int t = (j / 2) & 7;
+          mxp[t] = fmaxf(mxp[t], fmaxf(__uint_as_float(sr[c][j]), __uint_as_float(sr[c][j + 1])));
+        }
+      const float mx = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                             fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+      float alpha = 1.f;
+      bool rescale = false;
+      const float m_new = fmaxf(m_ref, mx * sl2);
+      if (m_new > m_ref + 8.f) {
+        alpha = exp2f(m_ref - m_new);
+        m_ref = m_new;
+        rescale = true;
+      }
+      const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+      const float2 negm = make_float2(-m_use, -m_use);
+      if (rescale && cnt > 0) {
+        mbar_wait(o_full + qt, (cnt - 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 16; ++c) {
+          uint32_t o[8];
+          tmem_ld8(tO + 8 * c, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
+          tmem_st8(tO + 8 * c, o);
+        }
+      }
+      float2 sacc[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
+      auto chunk_exp = [&](int c) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 x2 = __ffma2_rn(
+              make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1])), sl2v, negm);
+          sr[c][2 * j] = __float_as_uint(fast_exp2(x2.x));
+          sr[c][2 * j + 1] = __float_as_uint(fast_exp2(x2.y));
+        }
+      };
+      auto chunk_pack = [&](int c) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 p2 = make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1]));
+          sacc[j & 3] = __fadd2_rn(sacc[j & 3], p2);
+          __nv_bfloat162 b = __floats2bfloat162_rn(p2.x, p2.y);
+          pk[c][j] = *reinterpret_cast<uint32_t*>(&b);
+        }
+      };
+      // P_t in shared memory, laid out like a TMA-loaded Q tile (two 64-key SW128 boxes; row
+      // r's 16-byte chunk j at ((j ^ (r & 7)) << 4)) -- the A operand of the SS PV
+      const uint32_t prow = smem_u32(smem + SL::p) + qt * kTileBytes + ((quad * 32 + lane) >> 3) * 1024 +
+                            ((lane & 7) << 7);
+      auto store_p = [&](int c) {  // keys 32c .. 32c+31
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t a = prow + (c >> 1) * kBoxBytes + (((((c & 1) << 2) + q) ^ (lane & 7)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pk[c][4 * q]),
+                       "r"(pk[c][4 * q + 1]), "r"(pk[c][4 * q + 2]), "r"(pk[c][4 * q + 3])
+                       : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_leader(p_full + 4 * qt + c);
+      };
+      chunk_exp(0);
+#pragma unroll
+      for (int c = 1; c < 4; ++c) {
+        chunk_exp(c);
+        chunk_pack(c - 1);
+        if (c == 1 && cnt > 0 && !rescale) mbar_wait(o_full + qt, (cnt - 1) & 1);  // P buffer free
+        store_p(c - 1);
+      }
+      chunk_pack(3);
+      store_p(3);
+      const float2 sum2 = __fadd2_rn(__fadd2_rn(sacc[0], sacc[1]), __fadd2_rn(sacc[2], sacc[3]));
+      l = l * alpha + (sum2.x + sum2.y);
+      ++cnt;
+    }
+    // ---- epilogue: O / l, lse
+    if (cnt > 0) {
+      mbar_wait(o_full + qt, (cnt - 1) & 1);
+      tc_fence_after();
+    }
+    const bool valid_row = row < nq;
+    const float inv = (l > 0.f) ? 1.f / l : 0.f;
+    const long long obase = static_cast<long long>(split) * prob.split_stride_out +
+                            static_cast<long long>(row) * prob.ldo + qhead * kHeadDim;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t o[32];
+      if (cnt > 0) {
+        tmem_ld32(tO + 32 * c, o);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o[j] = 0u;
+      }
+      if (valid_row) {
+        if (prob.out_f32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(prob.out) + obase + 32 * c);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(__uint_as_float(o[4 * j]) * inv, __uint_as_float(o[4 * j + 1]) * inv,
+                                 __uint_as_float(o[4 * j + 2]) * inv, __uint_as_float(o[4 * j + 3]) * inv);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(prob.out) + obase + 32 * c);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t wv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(o[8 * j + 2 * e]) * inv,
+                                                       __uint_as_float(o[8 * j + 2 * e + 1]) * inv);
+              wv[e] = *reinterpret_cast<uint32_t*>(&b);
+            }
+            dst[j] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+          }
+        }
+      }
+    }
+    if (valid_row && prob.lse) {
+      const float lse = (l > 0.f) ? (m_ref + __log2f(l)) * 0.69314718055994530942f : -INFINITY;
+      prob.lse[static_cast<long long>(split) * prob.split_stride_lse + static_cast<long long>(row) * prob.ld_lse +
+               qhead] = lse;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the pair's last MMAs (issued by rank 0) are done with both TMEMs
+  tc_fence_after();
+  if (warp == kMmaWarp) tmem_dealloc2(tmem, kTmemCols);
+#undef TILE_R0
+#undef TILE_HEAD
+}
+
+#endif  // SPAVA_DEV_VARIANTS
+
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -912,6 +1674,7 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
   constexpr int rows_per_cta = kTilesPerCta * kBlockM;
   int work = 0;
   int np = 0;
+  int src_of[kMaxProbs] = {};
   for (int i = 0; i < nprob; ++i) {
     const ProbView& v = probs[i];
     if (v.nq <= 0) continue;
@@ -952,6 +1715,7 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
         return cudaErrorInvalidValue;
     }
     work += p.units * (p.head_pair ? hq / 2 : hq) * p.splits;
+    src_of[np] = i;
     ++np;
   }
   P.nprob = np;
@@ -977,6 +1741,55 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
   }
   const int grid = work + P.job.ctas + P.sj.ctas;
   if (grid == 0) return cudaSuccess;
+#ifdef SPAVA_DEV_VARIANTS
+  // CTA-pair kernels (dev build, SPAVA_ATTN_PAIR=1: P in TMEM, =2: P in shared memory): two
+  // q-heads of one KV group per 2-CTA cluster
+  static const int pair_env = [] {
+    const char* e = getenv("SPAVA_ATTN_PAIR");
+    return e ? atoi(e) : 0;
+  }();
+  if (pair_env && vsel == 0 && P.job.ctas == 0 && P.sj.ctas == 0) {
+    bool ok = true;
+    for (int q = 0; q < np; ++q)
+      ok = ok && P.prob[q].seg_lse2 == nullptr && ((hq / hkv) % (P.prob[q].head_pair ? 4 : 2)) == 0;
+    if (ok) {
+      AttnParams P2 = P;
+      int pw = 0;
+      for (int q = 0; q < np; ++q) {
+        AttnProb& p2 = P2.prob[q];
+        p2.work_begin = pw;
+        pw += p2.units * (p2.head_pair ? hq / 4 : hq / 2) * p2.splits;
+        const ProbView& v = probs[src_of[q]];
+        for (int sg = 0; sg < v.nseg; ++sg)  // K tiles of a pair: 64-key halves
+          if (!make_tmap(&P2.tmap[q][1 + 2 * sg], v.seg[sg].k, v.seg[sg].len, static_cast<long long>(hkv) * dh,
+                         v.seg[sg].ld, err, 64))
+            return cudaErrorInvalidValue;
+      }
+      P2.total_work = pw;
+      const KFn pf = pair_env == 2 ? attn_pair_ps_kernel<2> : attn_pair_kernel<kPairStages>;
+      const uint32_t pbytes = pair_env == 2 ? SmemPS<2>::bytes : SmemP<kPairStages>::bytes;
+      static std::atomic<uint32_t> attr_p[kMaxDevices] = {};
+      if (cudaError_t e = smem_optin(reinterpret_cast<const void*>(pf), static_cast<int>(pbytes), attr_p, pair_env);
+          e != cudaSuccess)
+        return e;
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(2 * pw);
+      lc.blockDim = dim3(kThreads);
+      lc.dynamicSmemBytes = pbytes;
+      lc.stream = stream;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      cudaError_t e = cudaLaunchKernelEx(&lc, pf, P2);
+      if (e != cudaSuccess && err) *err = std::string("attention launch (pair): ") + cudaGetErrorString(e);
+      return e;
+    }
+  }
+#endif
   static std::atomic<uint32_t> attr_set[kMaxDevices] = {};
   const KFn fn = var.fn;
   const uint32_t smem_bytes = smem_need;
