@@ -102,7 +102,10 @@ struct SelJobs {
   int32_t* status;
 };
 
-template <int kSelThreads>
+// kOne: the whole block fits one chunk (l_b <= kSelThreads * kItems, every C1..C4 shape):
+// each thread loads its 16 scores once and keeps them in registers for all five passes
+// (count, three radix digits, emission) instead of re-reading them from L2 every pass.
+template <int kSelThreads, bool kOne>
 __global__ void __launch_bounds__(kSelThreads) select_kernel(const __grid_constant__ SelJobs J) {
   constexpr int kChunk = kSelThreads * kItems;
   constexpr int kWarps = kSelThreads / 32;
@@ -117,11 +120,21 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const __grid_consta
   __shared__ uint32_t sh_prefix;
   __shared__ int sh_need;
   const int tid = threadIdx.x;
+  float vk[kItems];  // kOne: this thread's scores for every pass
+  if (kOne) load_items(scores, l_b, 0, vk);
+  auto items = [&](int base, float (&v)[kItems]) {
+    if (kOne) {
+#pragma unroll
+      for (int t = 0; t < kItems; ++t) v[t] = vk[t];
+    } else {
+      load_items(scores, l_b, base, v);
+    }
+  };
   // ---- 1. counts
   int fin = 0, bad = 0;
   for (int base = 0; base < l_b; base += kChunk) {
     float v[kItems];
-    load_items(scores, l_b, base, v);
+    items(base, v);
 #pragma unroll
     for (int t = 0; t < kItems; ++t) {
       fin += isfinite(v[t]) ? 1 : 0;
@@ -158,7 +171,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const __grid_consta
     __syncthreads();
     for (int base = 0; base < l_b; base += kChunk) {
       float v[kItems];
-      load_items(scores, l_b, base, v);
+      items(base, v);
 #pragma unroll
       for (int t = 0; t < kItems; ++t) {
         const uint32_t key = order_key(v[t]);
@@ -200,7 +213,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const __grid_consta
   int eq_base = 0, out_base = 0;
   for (int base = 0; base < l_b; base += kChunk) {
     float v[kItems];
-    load_items(scores, l_b, base, v);
+    items(base, v);
     int n_eq = 0;
 #pragma unroll
     for (int t = 0; t < kItems; ++t) n_eq += (isfinite(v[t]) && order_key(v[t]) == T) ? 1 : 0;
@@ -308,9 +321,11 @@ cudaError_t launch_select_pack_n(const SelectPackJob* jobs, int n, int l_b, int 
     if (j.fr.n < 0 || j.fr.n > kMaxPeers || (j.fr.n > 0 && !j.fr.counter)) return cudaErrorInvalidValue;
   }
   if (l_b <= kSelSmall * kItems)
-    select_kernel<kSelSmall><<<n, kSelSmall, 0, stream>>>(J);
+    select_kernel<kSelSmall, true><<<n, kSelSmall, 0, stream>>>(J);
+  else if (l_b <= kSelBig * kItems)
+    select_kernel<kSelBig, true><<<n, kSelBig, 0, stream>>>(J);
   else
-    select_kernel<kSelBig><<<n, kSelBig, 0, stream>>>(J);
+    select_kernel<kSelBig, false><<<n, kSelBig, 0, stream>>>(J);
   if (gather) gather_kernel<<<dim3((l_p + 7) / 8, n), 256, 0, stream>>>(J);
   return cudaGetLastError();
 }
