@@ -19,7 +19,11 @@ namespace spava {
 
 namespace {
 
-__global__ void merge_kernel(const __grid_constant__ MergeParams p) {
+// kMinB: blocks per SM the register budget must allow.  The dh = 128 instance asks for 16
+// so a (128 rows x 16 heads) query merge -- 2048 CTAs -- runs in one wave (at the default
+// 38 registers only 12 CTAs fit per SM: 1.15 waves, the second one nearly empty).
+template <int kMaxT, int kMinB>
+__global__ void __launch_bounds__(kMaxT, kMinB) merge_kernel(const __grid_constant__ MergeParams p) {
   __shared__ float w[kMaxMergeParts];
   __shared__ int ok_sh;
   __shared__ float lse_sh;
@@ -54,7 +58,10 @@ cudaError_t launch_merge(const MergeParams& p, cudaStream_t stream) {
   if (p.fr.n < 0 || p.fr.n > kMaxPeers || (p.fr.n > 0 && (!p.fr.counter || p.rows == 0)))
     return cudaErrorInvalidValue;
   if (p.rows == 0) return cudaSuccess;
-  merge_kernel<<<dim3(p.rows, p.hq), p.dh, 0, stream>>>(p);
+  if (p.dh == 128)
+    merge_kernel<128, 16><<<dim3(p.rows, p.hq), p.dh, 0, stream>>>(p);
+  else
+    merge_kernel<1024, 1><<<dim3(p.rows, p.hq), p.dh, 0, stream>>>(p);
   return cudaGetLastError();
 }
 
