@@ -13,8 +13,9 @@ score_block / select_essential / mha_lse / mha_merge (oracle/layer_ref.py):
 * the scorer's own report: non-identical scores vs the reference and the smallest
   relative top-k boundary gap (how close the selection came to a flip).
 
-C3 (131072 tokens, l_p=1024) on 8 simulated hosts does the same for all 16 virtual
-blocks (zigzag pairing, passing sets of up to 15 sources).  The report of every test is
+C2 (64K, 4 simulated hosts), C3 (131072 tokens, l_p=1024, 8 simulated hosts) and C4
+(Qwen2.5-VL-7B heads 28q/4kv, 256K tokens, H=1 and 8 simulated hosts) do the same for
+every virtual block (zigzag pairing, passing sets of up to 15 sources).  The report of every test is
 printed (pytest -s) and written to gpurun_out/parity_report.json when that dir exists.
 """
 import json
@@ -89,7 +90,7 @@ def _run_host_layer(cuda, g, hq, hkv, Q, K, V, score_mode=0):
 
 
 def _check_layer(name, cuda, g, hq, hkv, n_anchor, n_block, seed, score_mode=0, impl="ref",
-                 gpu_scores=True):
+                 gpu_scores=True, min_rows=1024):
     from paper_2601_21444_b200 import spava
 
     Q, K, V = LR.layer_inputs(g, hq, hkv, seed=seed)
@@ -157,7 +158,7 @@ def _check_layer(name, cuda, g, hq, hkv, n_anchor, n_block, seed, score_mode=0, 
     rep["tolerance"] = dict(max_abs=ATOL_BF16_OUT, rel_l2=RTOL_L2_BF16)
     _report(name, rep)
     assert sel_ok, rep["blocks"]
-    assert n_rows >= 1024
+    assert n_rows >= min_rows
     assert ok, rep
 
 
@@ -181,3 +182,28 @@ def test_c3_sim8_layer_vs_reference(cuda):
     g = LR.geometry(131072 - 128, 128, 8, 2048, 1024)
     assert g["l_b"] == 8056
     _check_layer("c3_h8_exact", cuda, g, 16, 2, n_anchor=64, n_block=64, seed=77)
+
+
+def test_c2_sim4_layer_vs_reference(cuda):
+    """C2 (BASELINE configs[2]: 64K tokens, 16q/2kv, one layer) on 4 simulated hosts:
+    all 8 blocks' passing indices and sampled rows against the reference."""
+    g = LR.geometry(65536 - 128, 128, 4, 1024, 512)
+    assert (g["l_b"], g["pad"]) == (8048, 0)
+    _check_layer("c2_h4_exact", cuda, g, 16, 2, n_anchor=64, n_block=112, seed=21)
+
+
+def test_c4_7b_h1_layer_vs_reference(cuda):
+    """C4 (BASELINE configs[4]: Qwen2.5-VL-7B heads 28q/4kv, 256K tokens) at H=1 -- the
+    bench's sweep_h1 C4 line: both blocks' passing indices and >= 512 sampled rows (the
+    reference row-slice problems here average ~70K keys x 28 heads: 1024 rows took 150 s)."""
+    g = LR.geometry(262144 - 128, 128, 1, 4096, 2048)
+    assert g["l_b"] == 128960
+    _check_layer("c4_7b_h1_exact", cuda, g, 28, 4, n_anchor=64, n_block=160, seed=4242, min_rows=512)
+
+
+def test_c4_7b_sim8_layer_vs_reference(cuda):
+    """C4 at the top of its 1/2/4/8 sweep: 8 simulated hosts, 16 blocks of 16120 keys,
+    passing sets of up to 15 x 2048 keys."""
+    g = LR.geometry(262144 - 128, 128, 8, 4096, 2048)
+    assert g["l_b"] == 16120
+    _check_layer("c4_7b_h8_exact", cuda, g, 28, 4, n_anchor=64, n_block=56, seed=808)
