@@ -309,7 +309,11 @@ int spava_sim_layer(spava_fabric* fab, spava_host* const* hosts, const void* con
 /* spava_sim_layer with every host's phases bracketed by events and run alone on the GPU:
  * ms_per_host[h] = host h's device time for one layer (excluding any exchange cost).  The
  * max over hosts is the per-GPU layer time an H-GPU run would see before communication --
- * used to measure load balance (zigzag vs naive pairing) on real kernels.  Synchronises. */
+ * used to measure load balance (zigzag vs naive pairing) on real kernels.  hosts may list
+ * the fabric's H hosts in any order (q..sel and ms_per_host follow that order): phase 1 of
+ * every host runs first, then phase 2 host by host in the given order -- rotating the order
+ * lets each host be timed early in a run, before a sustained-load power cap lowers the
+ * clocks.  Synchronises. */
 int spava_sim_layer_timed(spava_fabric* fab, spava_host* const* hosts, const void* const* q,
                           const void* const* k, const void* const* v, void* const* out,
                           int32_t* const* sel, void* stream, float* ms_per_host);

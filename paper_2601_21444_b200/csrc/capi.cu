@@ -1947,9 +1947,10 @@ int spava_sim_layer_timed(spava_fabric* F, spava_host* const* hosts, const void*
   cudaStream_t st = as_stream(stream);
   const int H = F->plan.hosts;
   std::vector<HostBufs> b(H);
+  std::vector<char> seen(H, 0);
   for (int h = 0; h < H; ++h) {
-    if (!hosts[h] || hosts[h]->fab != F || hosts[h]->h != h)
-      return fail(SPAVA_EINVAL, "sim_layer_timed: hosts[h] must be host h of this fabric");
+    if (!hosts[h] || hosts[h]->fab != F || hosts[h]->h < 0 || hosts[h]->h >= H || seen[hosts[h]->h]++)
+      return fail(SPAVA_EINVAL, "sim_layer_timed: hosts must be the fabric's H hosts, each once");
     b[h] = HostBufs{static_cast<const uint8_t*>(q[h]), static_cast<const uint8_t*>(k[h]),
                     static_cast<const uint8_t*>(v[h]), static_cast<uint8_t*>(out[h]),
                     sel ? sel[h] : nullptr};

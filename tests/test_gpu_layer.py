@@ -15,8 +15,9 @@ pytestmark = pytest.mark.gpu
 
 
 def run_layer(cuda, Q, K, V, n_v, n_t, hosts, l_a, l_p, hq, hkv, zigzag=True, softmax=True,
-              query_splits=0):
-    """Drive the local fabric (H simulated hosts on one GPU) over the global padded inputs."""
+              query_splits=0, timed_order=None):
+    """Drive the local fabric (H simulated hosts on one GPU) over the global padded inputs
+    (timed_order: through sim_layer_timed with the hosts in that order)."""
     import torch
 
     from paper_2601_21444_b200 import spava
@@ -36,7 +37,11 @@ def run_layer(cuda, Q, K, V, n_v, n_t, hosts, l_a, l_p, hq, hkv, zigzag=True, so
                        .to(torch.bfloat16).contiguous())
         outs.append(torch.zeros((H.rows, hq * 128), dtype=torch.bfloat16, device=cuda))
         sels.append(torch.full((2, max(l_p, 1)), -1, dtype=torch.int32, device=cuda))
-    fab.sim_layer(hs, qs, ks, vs, outs, sels)
+    if timed_order is None:
+        fab.sim_layer(hs, qs, ks, vs, outs, sels)
+    else:
+        ms = fab.sim_layer_timed(*[[x[i] for i in timed_order] for x in (hs, qs, ks, vs, outs, sels)])
+        assert len(ms) == hosts and all(t > 0 for t in ms)
     torch.cuda.synchronize()
     status = [H.status() for H in hs]
     res = dict(plan=plan, status=status, out=[o.float().cpu().numpy() for o in outs],
@@ -100,6 +105,39 @@ def test_layer_c0_shape(cuda, hosts, zigzag, splits):
     want = O.spava_layer(Q, K, V, n_v, n_t, hosts, l_a, l_p, hq, hkv, 128, zigzag=zigzag)
     res = run_layer(cuda, Q, K, V, n_v, n_t, hosts, l_a, l_p, hq, hkv, zigzag, True, splits)
     check_layer(res, want, n_t, hosts, l_a, zigzag)
+
+
+def test_sim_layer_timed_any_host_order(cuda):
+    """sim_layer_timed accepts the fabric's hosts in any order (tools/sim_scaling.py rotates
+    it so every host is timed before a power cap sets in): outputs and passing indices are
+    bit-identical to sim_layer's; a host listed twice is rejected."""
+    import torch
+
+    from paper_2601_21444_b200 import spava
+
+    n, n_t, hq, hkv, hosts = 8192, 64, 16, 2, 4
+    n_v, l_a, l_p = n - n_t, n // 64, n // 128
+    plan = spava.make_plan(n_v, n_t, hosts, l_a, l_p, True)
+    n_pad = l_a + 2 * hosts * plan.l_b + n_t
+    rng = np.random.default_rng(31)
+    Q, K, V = randn(rng, n_pad, hq * 128), randn(rng, n_pad, hkv * 128), randn(rng, n_pad, hkv * 128)
+    base = run_layer(cuda, Q, K, V, n_v, n_t, hosts, l_a, l_p, hq, hkv)
+    for order in ([2, 3, 0, 1], [3, 1, 2, 0]):
+        got = run_layer(cuda, Q, K, V, n_v, n_t, hosts, l_a, l_p, hq, hkv, timed_order=order)
+        assert got["status"] == [0] * hosts
+        for h in range(hosts):
+            assert np.array_equal(got["sel"][h], base["sel"][h]), (order, h)
+            assert np.array_equal(got["out"][h], base["out"][h]), (order, h)
+    cfg = spava.LayerConfig.make(n_v, n_t, hosts, l_a, l_p, hq, hkv, 128)
+    fab = spava.Fabric(cfg, 0)
+    hs = [fab.host(h) for h in range(hosts)]
+    bufs = [[torch.zeros((hs[0].rows, w * 128), dtype=torch.bfloat16, device=cuda) for _ in range(hosts)]
+            for w in (hq, hkv, hkv, hq)]
+    with pytest.raises(RuntimeError, match="each once"):
+        fab.sim_layer_timed([hs[0], hs[0], hs[2], hs[3]], *bufs)
+    for H in hs:
+        H.close()
+    fab.close()
 
 
 def test_nccl_fabric_world1_matches_local(cuda):

@@ -4,7 +4,7 @@ before NCCL exchange cost.  Compares zigzag (load-balanced) vs naive pairing.
 
     python tools/sim_scaling.py [C3] [hosts ...]      -> JSON lines (projection, not a bench value)
 """
-import json, sys, torch
+import json, sys, time, torch
 sys.path.insert(0, '.')
 import bench
 from paper_2601_21444_b200 import spava
@@ -51,8 +51,19 @@ for H in host_list:
         outs = [torch.empty(rows, hq * 128, dtype=torch.bfloat16, device=dev) for _ in range(H)]
         for _ in range(2):
             fab.sim_layer_timed(hosts, qs, ks, vs, outs)
-        runs = [fab.sim_layer_timed(hosts, qs, ks, vs, outs) for _ in range(5)]
-        ms = [min(r[h] for r in runs) for h in range(H)]
+        # each host is timed early in some run (order rotated, 1 s idle before each run): a
+        # sustained-load power cap (~70 ms at C4, SM clock 1965 -> 1590 MHz) would otherwise
+        # bill the hosts that happen to run last (tools/sim_clocks.py)
+        ms = [float("inf")] * H
+        for rep in range(2):
+            for rot in range(0, H, max(1, H // 4)):
+                order = [(i + rot) % H for i in range(H)]
+                torch.cuda.synchronize()
+                time.sleep(1.0)
+                r = fab.sim_layer_timed([hosts[i] for i in order], [qs[i] for i in order], [ks[i] for i in order],
+                                        [vs[i] for i in order], [outs[i] for i in order])
+                for pos, i in enumerate(order):
+                    ms[i] = min(ms[i], r[pos])
         fl = [bench.attn_flops_host(g, hq, h, zz) for h in range(H)]
         mx = max(ms)
         print(json.dumps({"config": cfg_name, "n": g["n"], "hosts": H, "pairing": "zigzag" if zz else "naive",
