@@ -103,6 +103,16 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&pk)[1
       "r"(pk[14]), "r"(pk[15]));
 }
 
+// the first 16 words of a 32-word register row (P packed in place over S)
+__device__ __forceinline__ void tmem_st16_lo(uint32_t taddr, const uint32_t (&pk)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]), "r"(pk[4]), "r"(pk[5]), "r"(pk[6]),
+      "r"(pk[7]), "r"(pk[8]), "r"(pk[9]), "r"(pk[10]), "r"(pk[11]), "r"(pk[12]), "r"(pk[13]),
+      "r"(pk[14]), "r"(pk[15]));
+}
+
 __device__ __forceinline__ int seg_tiles(const AttnSeg& s, int imax) {
   const int klen = s.causal ? min(s.len, imax) : s.len;
   return klen > 0 ? (klen + kBlockN - 1) / kBlockN : 0;
@@ -152,12 +162,20 @@ __device__ __forceinline__ void cursor_next(const AttnProb& p, int imax, Cursor&
 // kSeq: the exp phases of the two softmax warpgroups strictly alternate (named barriers 1/2),
 // so each runs with the SM's MUFU to itself and the two stay in anti-phase with the MMAs.
 // kLd2: S is read from TMEM in two halves, the max of the first overlapping the second load.
+// kWG = 2: FOUR softmax warpgroups (576 threads), two per Q tile, each taking 64 of the 128
+// key columns of every S tile: per-tile softmax latency halves (64 exps per thread), the two
+// halves exchange their row maxima through shared memory (named barrier per Q tile) and
+// keep partial row sums that are added in the epilogue; each half commits its two P ranges.
 template <int kEmu, int KS, bool kProf = false, bool kPipe = false, bool kSpec = true, int kPParts = 1,
-          int kRegs = 0, bool kSeq = false, bool kLd2 = false>
-__global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
+          int kRegs = 0, bool kSeq = false, bool kLd2 = false, int kWG = 1>
+__global__ void __launch_bounds__(kWG == 2 ? 576 : kRegs > 0 ? 384 : kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ AttnParams P) {
   static_assert(kPParts == 1 || (kPipe && !kSpec && (kPParts == 2 || kPParts == 4)),
                 "split P needs the max-first pipelined softmax");
+  static_assert(kWG == 1 || (kPipe && !kSpec && kPParts == 4 && kRegs == 0 && !kSeq && !kLd2),
+                "column-split softmax: max-first pipelined body with P in 4 ranges only");
+  constexpr int kProdW = kWG == 2 ? 16 : kProducerWarp;
+  constexpr int kMmaW = kProdW + 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -174,6 +192,7 @@ __global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
 
   // trailing CTAs of a stage launch (peer fabric): the receive-side query merge
+  if constexpr (kWG == 1) {
   if (P.job.ctas > 0 && static_cast<int>(blockIdx.x) >= P.total_work &&
       static_cast<int>(blockIdx.x) < P.total_work + P.job.ctas) {
     merge_job(P.job, static_cast<int>(blockIdx.x) - P.total_work, reinterpret_cast<float*>(smem));
@@ -187,6 +206,7 @@ __global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
     score_fast_cta<1>(P.sj.fa, t % P.sj.fa.ntiles, t / P.sj.fa.ntiles, smem);
     return;
   }
+  }  // kWG == 1 (the launcher keeps trailing jobs on the production kernel)
   const int warp = warp_id();
   const int lane = lane_id();
   long long pr[14] = {};
@@ -220,7 +240,7 @@ __global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
   const int ntiles = t_end - t_begin;
   const CUtensorMap* tm = P.tmap[pi];
 
-  if (warp == kProducerWarp && elect_one()) {
+  if (warp == kProdW && elect_one()) {
     mbar_init(q_full, 1);
     for (int s = 0; s < KS; ++s) {
       mbar_init(k_full + s, 1);
@@ -242,16 +262,16 @@ __global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
       tma_prefetch_desc(&tm[2 + 2 * s]);
     }
   }
-  if (warp == kMmaWarp) tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == kMmaW) tmem_alloc(tmem_slot, kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // Role branches: the register budget changes at the top of each warpgroup's branch and the
   // branches only rejoin at the teardown, so ptxas allocates each role within its budget.
-  if (warp >= kProducerWarp) {
+  if (warp >= kProdW) {
   if constexpr (kRegs > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
-  if (warp == kProducerWarp) {
+  if (warp == kProdW) {
     // ======================================================== TMA producer
     if (elect_one()) {
       const bool has1 = TILE_R0(1) < nq;
@@ -278,7 +298,7 @@ __global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
         cursor_next(prob, imax, cur);
       }
     }
-  } else if (warp == kMmaWarp) {
+  } else if (warp == kMmaW) {
     // ======================================================== MMA issuer
     if (elect_one()) {
       const uint32_t idesc_qk = idesc_bf16_f32(128, 128, 0, 0);  // Q, K both K-major
@@ -380,6 +400,201 @@ __global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
   } else {
     if constexpr (kRegs > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegs));
     // ======================================================== softmax warpgroups
+    if constexpr (kWG == 2) {
+    // ---- column-split softmax: warpgroup g takes Q tile g & 1, key columns [64 h, 64 h + 64)
+    // of every S tile (h = g >> 1); TMEM lanes are per warp-in-warpgroup, so both halves of a
+    // Q tile address the same 128 lanes.
+    const int g = warp >> 2;
+    const int qt = g & 1;
+    const int half = g >> 1;
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int row = TILE_R0(qt) + r;
+    const int qhead = TILE_HEAD(qt);
+    const uint32_t t_lane = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t tS = tmem + t_lane + qt * 128;
+    const uint32_t tO = tmem + t_lane + 256 + qt * 128 + 64 * half;
+    float* xmax = reinterpret_cast<float*>(smem + SL::total);  // [2 parity][2 qt][2 half][128]
+    float* xl = xmax + 1024;  // [2 qt][2 half][3][128]  (10 KB in all, Smem<2>::bytes + 10240)
+    const float sl2 = P.scale_log2;
+    const float2 sl2v = make_float2(sl2, sl2);
+    float m_ref = -INFINITY;
+    const bool seg_stats = prob.seg_lse2 != nullptr;
+    float l_seg[2] = {0.f, 0.f};
+    float l = 0.f;
+    uint32_t cnt = 0;
+    Cursor cur = cursor_at(prob, imax, t_begin);
+    for (int it = 0; it < ntiles; ++it, cursor_next(prob, imax, cur)) {
+      const AttnSeg sg = prob.seg[cur.seg];
+      const int mode = tile_mode(sg, cur.kt, TILE_R0(qt), nq);
+      if (mode == kSkip) continue;  // same decision in both halves (it depends on rows only)
+      mbar_wait(s_full + qt, cnt & 1);
+      tc_fence_after();
+      uint32_t sr[2][32];
+      tmem_ld32(tS + 64 * half, sr[0]);
+      tmem_ld32(tS + 64 * half + 32, sr[1]);
+      tmem_wait_ld();
+      if (mode == kPart) {
+        const int k0 = cur.kt * kBlockN + 64 * half;
+        int lim = sg.len - k0;
+        if (sg.causal) lim = min(lim, row - k0 + 1);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c * 32 + j >= lim) sr[c][j] = __float_as_uint(-INFINITY);
+      }
+      float mxp[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) mxp[t] = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int j = 0; j < 32; j += 2)
+          mxp[(j / 2) & 7] = fmaxf(mxp[(j / 2) & 7], fmaxf(__uint_as_float(sr[c][j]), __uint_as_float(sr[c][j + 1])));
+      const float mxl = fmaxf(fmaxf(fmaxf(mxp[0], mxp[1]), fmaxf(mxp[2], mxp[3])),
+                              fmaxf(fmaxf(mxp[4], mxp[5]), fmaxf(mxp[6], mxp[7])));
+      // row max of the whole tile: exchange with the other half (slot by tile parity: the
+      // partner reads slot j before either half can reach tile j + 2's write of it).  The
+      // barrier also orders this half's S loads before the other half's P stores, which
+      // land in S columns [32 h', 32 h' + 32) -- half 0's S columns 32..63 for h' = 1.
+      float* xm = xmax + ((cnt & 1) * 2 + qt) * 2 * 128;
+      xm[half * 128 + r] = mxl;
+      named_bar_sync(1 + qt, 256);
+      const float mx = fmaxf(mxl, xm[(half ^ 1) * 128 + r]);
+      const float m_new = fmaxf(m_ref, mx * sl2);
+      float alpha = 1.f;
+      const bool rescale = m_new > m_ref + 8.f;  // identical in both halves
+      if (rescale) {
+        alpha = exp2f(m_ref - m_new);
+        m_ref = m_new;
+      }
+      if (rescale && cnt > 0) {
+        // each half corrects its 64 O columns; both are done before either releases a P
+        // range (the PV K-steps write all 128 columns)
+        mbar_wait(o_full + qt, (cnt - 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 8; ++c) {
+          uint32_t o[8];
+          tmem_ld8(tO + 8 * c, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
+          tmem_st8(tO + 8 * c, o);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        named_bar_sync(1 + qt, 256);
+      }
+      const float m_use = (m_ref == -INFINITY) ? 0.f : m_ref;
+      const float2 negm = make_float2(-m_use, -m_use);
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 x2 = __ffma2_rn(
+              make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1])), sl2v, negm);
+          float2 p2;
+          if (kEmu > 0 && mode == kFull && emu_slot(j, kEmu))
+            p2 = exp2_poly2(x2);
+          else
+            p2 = make_float2(fast_exp2(x2.x), fast_exp2(x2.y));  // -inf -> 0
+          sr[c][2 * j] = __float_as_uint(p2.x);
+          sr[c][2 * j + 1] = __float_as_uint(p2.y);
+        }
+      float2 sacc[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) sacc[t] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        // pack in place (word j <- keys 2j, 2j+1; reads never hit an already packed word)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 p2 = make_float2(__uint_as_float(sr[c][2 * j]), __uint_as_float(sr[c][2 * j + 1]));
+          sacc[j & 3] = __fadd2_rn(sacc[j & 3], p2);
+          __nv_bfloat162 b = __floats2bfloat162_rn(p2.x, p2.y);
+          sr[c][j] = *reinterpret_cast<uint32_t*>(&b);
+        }
+        tmem_st16_lo(tS + 32 * half + 16 * c, sr[c]);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(p_full + 4 * qt + 2 * half + c);
+      }
+      const float2 sum2 = __fadd2_rn(__fadd2_rn(sacc[0], sacc[1]), __fadd2_rn(sacc[2], sacc[3]));
+      l = l * alpha + (sum2.x + sum2.y);
+      if (seg_stats) {
+        l_seg[0] *= alpha;
+        l_seg[1] *= alpha;
+        if (cur.seg == prob.stat_seg[0]) l_seg[0] += sum2.x + sum2.y;
+        if (cur.seg == prob.stat_seg[1]) l_seg[1] += sum2.x + sum2.y;
+      }
+      ++cnt;
+    }
+    // ---- epilogue: row sums of both halves (half 0 + half 1), O / l of this half's columns
+    if (cnt > 0) {
+      mbar_wait(o_full + qt, (cnt - 1) & 1);
+      tc_fence_after();
+    }
+    float* xq = xl + qt * 2 * 3 * 128;
+    xq[(half * 3 + 0) * 128 + r] = l;
+    xq[(half * 3 + 1) * 128 + r] = l_seg[0];
+    xq[(half * 3 + 2) * 128 + r] = l_seg[1];
+    named_bar_sync(1 + qt, 256);
+    const float lt = xq[0 * 128 + r] + xq[3 * 128 + r];
+    const float ls0 = xq[1 * 128 + r] + xq[4 * 128 + r];
+    const float ls1 = xq[2 * 128 + r] + xq[5 * 128 + r];
+    const bool valid_row = row < nq;
+    const float inv = (lt > 0.f) ? 1.f / lt : 0.f;
+    const long long obase = static_cast<long long>(split) * prob.split_stride_out +
+                            static_cast<long long>(row) * prob.ldo + qhead * kHeadDim + 64 * half;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uint32_t o[32];
+      if (cnt > 0) {
+        tmem_ld32(tO + 32 * c, o);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o[j] = 0u;
+      }
+      if (valid_row) {
+        if (prob.out_f32) {
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(prob.out) + obase + 32 * c);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(__uint_as_float(o[4 * j]) * inv, __uint_as_float(o[4 * j + 1]) * inv,
+                                 __uint_as_float(o[4 * j + 2]) * inv, __uint_as_float(o[4 * j + 3]) * inv);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(prob.out) + obase + 32 * c);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(o[8 * j + 2 * e]) * inv,
+                                                       __uint_as_float(o[8 * j + 2 * e + 1]) * inv);
+              w[e] = *reinterpret_cast<uint32_t*>(&b);
+            }
+            dst[j] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+    }
+    if (valid_row && half == 0 && prob.lse) {
+      const float lse = (lt > 0.f) ? (m_ref + __log2f(lt)) * 0.69314718055994530942f : -INFINITY;
+      prob.lse[static_cast<long long>(split) * prob.split_stride_lse +
+               static_cast<long long>(row) * prob.ld_lse + qhead] = lse;
+    }
+    if (valid_row && half == 0 && seg_stats) {
+      const float lsv[2] = {ls0, ls1};
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2)
+        if (prob.stat_seg[s2] >= 0)
+          prob.seg_lse2[((static_cast<long long>(s2) * prob.splits + split) * nq + row) * P.hq + qhead] =
+              lsv[s2] > 0.f ? m_ref + __log2f(lsv[s2]) : -INFINITY;
+    }
+    } else {
     const int qt = warp >> 2;
     const int quad = warp & 3;
     const int row = TILE_R0(qt) + quad * 32 + lane;  // problem-local query row
@@ -737,6 +952,7 @@ __global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
           prob.seg_lse2[((static_cast<long long>(s2) * prob.splits + split) * nq + row) * P.hq + qhead] =
               l_seg[s2] > 0.f ? m_ref + __log2f(l_seg[s2]) : -INFINITY;
     }
+    }  // kWG
   }
 
   if (P.sj.ctas > 0) __threadfence();  // seg_lse2 stores, before this CTA is counted
@@ -800,10 +1016,10 @@ __global__ void __launch_bounds__(kRegs > 0 ? 384 : kThreads, 1)
       }
     }
   }
-  if (kProf && (warp == kMmaWarp || (warp < kProducerWarp && lane == 0)))
+  if (kProf && (warp == kMmaW || (warp < kProdW && lane == 0)))
     for (int i = 0; i < 14; ++i)
       if (pr[i]) atomicAdd(&g_attn_prof[i], static_cast<unsigned long long>(pr[i]));
-  if (warp == kMmaWarp) tmem_dealloc(tmem, kTmemCols);
+  if (warp == kMmaW) tmem_dealloc(tmem, kTmemCols);
 #undef TILE_R0
 #undef TILE_HEAD
 }
@@ -1659,6 +1875,9 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
       {attn_fwd_kernel<0, 2, false, true, false, 4, 0, false, true>, Smem<2>::bytes},  // 12 0 + split S load
       {attn_fwd_kernel<0, 2, false, true, false, 4, 0, true, true>, Smem<2>::bytes},   // 13 11 + 12
       {attn_fwd_kernel<4, 2, false, true, false, 4, 224, true, true>, Smem<2>::bytes, 384},  // 14 13 + setmaxnreg + 25% FMA exp2
+      {attn_fwd_kernel<0, 2, false, true, false, 4, 0, false, false, 2>, Smem<2>::bytes + 10240, 576},  // 15 column-split softmax (4 warpgroups)
+      {attn_fwd_kernel<4, 2, false, true, false, 4, 0, false, false, 2>, Smem<2>::bytes + 10240, 576},  // 16 15 + 25% FMA exp2
+      {attn_fwd_kernel<2, 2, false, true, false, 4, 0, false, false, 2>, Smem<2>::bytes + 10240, 576},  // 17 15 + 12.5% FMA exp2
 #endif
   };
   constexpr int kNumVar = sizeof(variants) / sizeof(variants[0]);
@@ -1669,7 +1888,10 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
     return (v >= 0 && v < kNumVar) ? v : 0;
   }();
   const int forced = g_attn_variant.load();
-  const int vsel = (forced >= 0 && forced < kNumVar) ? forced : env_sel;
+  const int vsel0 = (forced >= 0 && forced < kNumVar) ? forced : env_sel;
+  // trailing merge / column-sum CTAs run with the production block shape
+  const bool trailing = (job && job->ctas > 0) || (sj && sj->ctas > 0);
+  const int vsel = (trailing && variants[vsel0].threads != kThreads) ? 0 : vsel0;
   const Var& var = variants[vsel];
   constexpr int rows_per_cta = kTilesPerCta * kBlockM;
   int work = 0;
@@ -1813,7 +2035,7 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
 
 int attn_set_variant(int v) {
 #ifdef SPAVA_DEV_VARIANTS
-  constexpr int kBuilt = 15;
+  constexpr int kBuilt = 18;
 #else
   constexpr int kBuilt = 1;
 #endif
