@@ -167,7 +167,7 @@ __device__ __forceinline__ void cursor_next(const AttnProb& p, int imax, Cursor&
 // halves exchange their row maxima through shared memory (named barrier per Q tile) and
 // keep partial row sums that are added in the epilogue; each half commits its two P ranges.
 template <int kEmu, int KS, bool kProf = false, bool kPipe = false, bool kSpec = true, int kPParts = 1,
-          int kRegs = 0, bool kSeq = false, bool kLd2 = false, int kWG = 1>
+          int kRegs = 0, bool kSeq = false, bool kLd2 = false, int kWG = 1, bool kStats = true>
 __global__ void __launch_bounds__(kWG == 2 ? 576 : kRegs > 0 ? 384 : kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ AttnParams P) {
   static_assert(kPParts == 1 || (kPipe && !kSpec && (kPParts == 2 || kPParts == 4)),
@@ -606,7 +606,9 @@ __global__ void __launch_bounds__(kWG == 2 ? 576 : kRegs > 0 ? 384 : kThreads, 1
     float m_ref = -INFINITY;
     // fused fast scorer: sum of 2^(x - m_ref) over the keys of block lo / hi alone (same
     // reference max and lazy rescale as l), i.e. the scorer's per-row softmax statistics
-    const bool seg_stats = prob.seg_lse2 != nullptr;
+    // (kStats = false: an instance without them -- two fewer live registers in the softmax
+    // loop, which runs at the 168-register cap of 320 threads)
+    const bool seg_stats = kStats && prob.seg_lse2 != nullptr;
     float l_seg[2] = {0.f, 0.f};
     float l = 0.f;
     uint32_t cnt = 0;
@@ -1859,7 +1861,7 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
   // Only the production kernel ships; the A/B variants are compiled into a
   // dev build only (SPAVA_DEV_VARIANTS=1 python -m paper_2601_21444_b200.build --force).
   static const Var variants[] = {
-      {attn_fwd_kernel<0, 2, false, true, false, 4>, Smem<2>::bytes},  // 0 production: P in 4 key ranges
+      {attn_fwd_kernel<0, 2, false, true, false, 4, 0, false, false, 1, false>, Smem<2>::bytes},  // 0 production: P in 4 key ranges
 #ifdef SPAVA_DEV_VARIANTS
       {attn_fwd_kernel<0, 2, true, true, false, 4>, Smem<2>::bytes},   // 1 0 + cycle counters
       {attn_fwd_kernel<0, 2, false, true, false, 1>, Smem<2>::bytes},  // 2 round-1 kernel (P whole)
@@ -1891,8 +1893,16 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
   const int vsel0 = (forced >= 0 && forced < kNumVar) ? forced : env_sel;
   // trailing merge / column-sum CTAs run with the production block shape
   const bool trailing = (job && job->ctas > 0) || (sj && sj->ctas > 0);
-  const int vsel = (trailing && variants[vsel0].threads != kThreads) ? 0 : vsel0;
-  const Var& var = variants[vsel];
+  const int vsel1 = (trailing && variants[vsel0].threads != kThreads) ? 0 : vsel0;
+  // the fused-scorer query launch (per-block row statistics) takes the production kernel's
+  // instance with the statistics compiled in
+  static const Var stats_var = {attn_fwd_kernel<0, 2, false, true, false, 4, 0, false, false, 1, true>,
+                                Smem<2>::bytes};
+  bool stats = false;
+  for (int i = 0; i < nprob; ++i) stats = stats || (probs[i].nq > 0 && probs[i].seg_lse2 != nullptr);
+  const bool use_stats = stats && vsel1 == 0;
+  const int vsel = use_stats ? 31 : vsel1;  // attr cache slot
+  const Var& var = use_stats ? stats_var : variants[vsel1];
   constexpr int rows_per_cta = kTilesPerCta * kBlockM;
   int work = 0;
   int np = 0;
