@@ -1863,16 +1863,16 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
   static const Var variants[] = {
       {attn_fwd_kernel<0, 2, false, true, false, 4, 0, false, false, 1, false>, Smem<2>::bytes},  // 0 production: P in 4 key ranges
 #ifdef SPAVA_DEV_VARIANTS
-      {attn_fwd_kernel<0, 2, true, true, false, 4>, Smem<2>::bytes},   // 1 0 + cycle counters
+      {attn_fwd_kernel<0, 2, true, true, false, 4, 0, false, false, 1, false>, Smem<2>::bytes},   // 1 0 + cycle counters
       {attn_fwd_kernel<0, 2, false, true, false, 1>, Smem<2>::bytes},  // 2 round-1 kernel (P whole)
       {attn_fwd_kernel<0, 2, false, true, false, 2>, Smem<2>::bytes},  // 3 P in 2 key ranges
-      {attn_fwd_kernel<4, 2, false, true, false, 4>, Smem<2>::bytes},  // 4 0 + 25% FMA exp2
-      {attn_fwd_kernel<2, 2, false, true, false, 4>, Smem<2>::bytes},  // 5 0 + 12.5% FMA exp2
+      {attn_fwd_kernel<4, 2, false, true, false, 4, 0, false, false, 1, false>, Smem<2>::bytes},  // 4 0 + 25% FMA exp2
+      {attn_fwd_kernel<2, 2, false, true, false, 4, 0, false, false, 1, false>, Smem<2>::bytes},  // 5 0 + 12.5% FMA exp2
       {attn_fwd_kernel<0, 3, false, true, false, 4>, Smem<3>::bytes},  // 6 0 + 3-deep K ring
       {attn_fwd_kernel<0, 2, false, true, true, 1>, Smem<2>::bytes},   // 7 speculative stale max
-      {attn_fwd_kernel<0, 2, false, true, false, 4, 224>, Smem<2>::bytes, 384},  // 8 0 + setmaxnreg
-      {attn_fwd_kernel<4, 2, false, true, false, 4, 224>, Smem<2>::bytes, 384},  // 9 8 + 25% FMA exp2
-      {attn_fwd_kernel<2, 2, false, true, false, 4, 224>, Smem<2>::bytes, 384},  // 10 8 + 12.5% FMA exp2
+      {attn_fwd_kernel<0, 2, false, true, false, 4, 224, false, false, 1, false>, Smem<2>::bytes, 384},  // 8 0 + setmaxnreg
+      {attn_fwd_kernel<4, 2, false, true, false, 4, 224, false, false, 1, false>, Smem<2>::bytes, 384},  // 9 8 + 25% FMA exp2
+      {attn_fwd_kernel<2, 2, false, true, false, 4, 224, false, false, 1, false>, Smem<2>::bytes, 384},  // 10 8 + 12.5% FMA exp2
       {attn_fwd_kernel<0, 2, false, true, false, 4, 0, true>, Smem<2>::bytes},    // 11 0 + exp phases alternate
       {attn_fwd_kernel<0, 2, false, true, false, 4, 0, false, true>, Smem<2>::bytes},  // 12 0 + split S load
       {attn_fwd_kernel<0, 2, false, true, false, 4, 0, true, true>, Smem<2>::bytes},   // 13 11 + 12
