@@ -167,9 +167,12 @@ __device__ __forceinline__ void cursor_next(const AttnProb& p, int imax, Cursor&
 // halves exchange their row maxima through shared memory (named barrier per Q tile) and
 // keep partial row sums that are added in the epilogue; each half commits its two P ranges.
 template <int kEmu, int KS, bool kProf = false, bool kPipe = false, bool kSpec = true, int kPParts = 1,
-          int kRegs = 0, bool kSeq = false, bool kLd2 = false, int kWG = 1, bool kStats = true>
+          int kRegs = 0, bool kSeq = false, bool kLd2 = false, int kWG = 1, bool kStats = true,
+          bool kHalfQK = false>
 __global__ void __launch_bounds__(kWG == 2 ? 576 : kRegs > 0 ? 384 : kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ AttnParams P) {
+  static_assert(!kHalfQK || (kWG == 1 && !kSpec && !kLd2 && kPParts == 4),
+                "split QK: production softmax path only");
   static_assert(kPParts == 1 || (kPipe && !kSpec && (kPParts == 2 || kPParts == 4)),
                 "split P needs the max-first pipelined softmax");
   static_assert(kWG == 1 || (kPipe && !kSpec && kPParts == 4 && kRegs == 0 && !kSeq && !kLd2),
@@ -189,7 +192,8 @@ __global__ void __launch_bounds__(kWG == 2 ? 576 : kRegs > 0 ? 384 : kThreads, 1
   uint64_t* s_full = v_empty + kVStages;      // [2] S_t ready in TMEM
   uint64_t* p_full = s_full + 2;              // [2][4] P_t key range written (O_t corrected)
   uint64_t* o_full = p_full + 8;              // [2] PV_t complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+  uint64_t* s_loaded = o_full + 2;            // [2] kHalfQK: S_t(j) is in the softmax registers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_loaded + 2);
 
   // trailing CTAs of a stage launch (peer fabric): the receive-side query merge
   if constexpr (kWG == 1) {
@@ -254,6 +258,7 @@ __global__ void __launch_bounds__(kWG == 2 ? 576 : kRegs > 0 ? 384 : kThreads, 1
       mbar_init(s_full + t, 1);
       for (int pp = 0; pp < kPParts; ++pp) mbar_init(p_full + 4 * t + pp, 128);
       mbar_init(o_full + t, 1);
+      mbar_init(s_loaded + t, 128);
     }
     fence_barrier_init();
     tma_prefetch_desc(&tm[0]);
@@ -316,6 +321,22 @@ __global__ void __launch_bounds__(kWG == 2 ? 576 : kRegs > 0 ? 384 : kThreads, 1
           mma_ss(d, a, b, idesc_qk, kk > 0 ? 1u : 0u);
         }
       };
+      // kHalfQK: S_t(j+1) as two N = 64 halves.  Keys 64..127 land in S columns 64..127,
+      // which hold no P, so that half is issued as soon as the softmax has S_t(j) in
+      // registers (s_loaded) and runs under its exps; only keys 0..63 (columns 0..63, where
+      // P_t(j) sits) still follow PV_t(j) -- the chain after the last P range shrinks from
+      // 1.25 to 0.75 MMA times.
+      const uint32_t idesc_qk64 = idesc_bf16_f32(128, 64, 0, 0);
+      auto issue_qk_half = [&](int qt, int stage, int h) {
+        const uint32_t d = tmem + qt * 128 + 64 * h;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t koff = (kk >> 2) * kBoxBytes + (kk & 3) * 32;
+          const uint64_t a = sdesc_sw128(sq + qt * kTileBytes + koff, 16, 1024);
+          const uint64_t b = sdesc_sw128(sk + stage * kTileBytes + koff + h * 8192u, 16, 1024);
+          mma_ss(d, a, b, idesc_qk64, kk > 0 ? 1u : 0u);
+        }
+      };
       // PV K-steps [kk0, kk0 + n) (16 keys each; P of K-step kk at S columns 8kk..8kk+7)
       auto issue_pv = [&](int qt, int stage, bool acc, int kk0, int n) {
         const uint32_t d = tmem + 256 + qt * 128;
@@ -370,6 +391,15 @@ __global__ void __launch_bounds__(kWG == 2 ? 576 : kRegs > 0 ? 384 : kThreads, 1
         }
         tc_fence_after();
         for (int qt = 0; qt < 2; ++qt) {
+          if constexpr (kHalfQK) {
+            if (nmode[qt] != kSkip) {
+              if (mode[qt] != kSkip) {  // S_qt(it) exists: wait until the softmax holds it
+                mbar_wait(s_loaded + qt, p_cnt[qt] & 1);
+                tc_fence_after();
+              }
+              issue_qk_half(qt, kn, 1);
+            }
+          }
           if (mode[qt] != kSkip) {
 #pragma unroll
             for (int pp = 0; pp < kPParts; ++pp) {
@@ -385,7 +415,10 @@ __global__ void __launch_bounds__(kWG == 2 ? 576 : kRegs > 0 ? 384 : kThreads, 1
           }
           if (qt == 1) tc_commit(v_empty + vs);
           if (nmode[qt] != kSkip) {
-            issue_qk(qt, kn);
+            if constexpr (kHalfQK)
+              issue_qk_half(qt, kn, 0);
+            else
+              issue_qk(qt, kn);
             tc_commit(s_full + qt);
           }
         }
@@ -761,6 +794,10 @@ __global__ void __launch_bounds__(kWG == 2 ? 576 : kRegs > 0 ? 384 : kThreads, 1
         chunk_max(3, mxp);
       } else {
         load_s();
+        if constexpr (kHalfQK) {  // S columns 64..127 may now take the next tile's keys 64..127
+          tc_fence_before();
+          mbar_arrive(s_loaded + qt);
+        }
       }
       if (kProf) pr[9] += PROF_NOW() - tw1;
       if (kSpec && mode == kFull && m_ref != -INFINITY) {
@@ -1877,9 +1914,11 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
       {attn_fwd_kernel<0, 2, false, true, false, 4, 0, false, true>, Smem<2>::bytes},  // 12 0 + split S load
       {attn_fwd_kernel<0, 2, false, true, false, 4, 0, true, true>, Smem<2>::bytes},   // 13 11 + 12
       {attn_fwd_kernel<4, 2, false, true, false, 4, 224, true, true>, Smem<2>::bytes, 384},  // 14 13 + setmaxnreg + 25% FMA exp2
-      {attn_fwd_kernel<0, 2, false, true, false, 4, 0, false, false, 2>, Smem<2>::bytes + 10240, 576},  // 15 column-split softmax (4 warpgroups)
-      {attn_fwd_kernel<4, 2, false, true, false, 4, 0, false, false, 2>, Smem<2>::bytes + 10240, 576},  // 16 15 + 25% FMA exp2
-      {attn_fwd_kernel<2, 2, false, true, false, 4, 0, false, false, 2>, Smem<2>::bytes + 10240, 576},  // 17 15 + 12.5% FMA exp2
+      {attn_fwd_kernel<0, 2, false, true, false, 4, 0, false, false, 1, false, true>, Smem<2>::bytes},  // 15 split QK (keys 64..127 under the softmax)
+      {attn_fwd_kernel<0, 2, true, true, false, 4, 0, false, false, 1, false, true>, Smem<2>::bytes},   // 16 15 + cycle counters
+      {attn_fwd_kernel<0, 2, false, true, false, 4, 0, false, false, 2>, Smem<2>::bytes + 10240, 576},  // 17 column-split softmax (4 warpgroups)
+      {attn_fwd_kernel<4, 2, false, true, false, 4, 0, false, false, 2>, Smem<2>::bytes + 10240, 576},  // 18 17 + 25% FMA exp2
+      {attn_fwd_kernel<2, 2, false, true, false, 4, 0, false, false, 2>, Smem<2>::bytes + 10240, 576},  // 19 17 + 12.5% FMA exp2
 #endif
   };
   constexpr int kNumVar = sizeof(variants) / sizeof(variants[0]);
@@ -2045,7 +2084,7 @@ cudaError_t launch_attention(const ProbView* probs, int nprob, int hq, int hkv, 
 
 int attn_set_variant(int v) {
 #ifdef SPAVA_DEV_VARIANTS
-  constexpr int kBuilt = 18;
+  constexpr int kBuilt = 20;
 #else
   constexpr int kBuilt = 1;
 #endif

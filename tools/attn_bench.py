@@ -30,7 +30,7 @@ fl2 = 2.0*n*n*hq*128
 ms3 = t(lambda: spava.attention(q, [dict(k=k, v=v)], hq, hkv), 5)
 fl3 = 4.0*lb*lb*hq*128
 print(f"variant {os.environ.get('SPAVA_ATTN_VARIANT','0')}: block {ms:.3f} ms {fl/ms/1e9:.0f} TF/s | dense causal {ms2:.3f} ms {fl2/ms2/1e9:.0f} TF/s | full {ms3:.3f} ms {fl3/ms3/1e9:.0f} TF/s")
-if os.environ.get('SPAVA_ATTN_VARIANT') == '1':
+if os.environ.get('SPAVA_ATTN_VARIANT') in ('1', '16'):
     import ctypes as C
     L = spava.lib()
     buf = (C.c_uint64 * 16)()
