@@ -354,7 +354,7 @@ def time_layer(torch, host, q, k, v, out, sel, stream, flush, steps, warmup):
     return [a.elapsed_time(b) for a, b in ev]
 
 
-def sweep_line(torch, spava, name, local, stream, flush, steps, pk):
+def sweep_line(torch, spava, name, local, stream, flush, steps, pk, full=True):
     """One more single-GPU configuration on the N=1 line (BASELINE's 1/2/4/8 sweep config
     C4 at H=1, and C3 at H=1 for the 128K scaling curve): tokens/s, attention roofline and
     e2e through the host-buffer C-ABI call.  Inputs are drawn on the device (not compared)."""
@@ -387,6 +387,12 @@ def sweep_line(torch, spava, name, local, stream, flush, steps, pk):
                         "frac": round(ach / pk["bf16_burst"], 4),
                         "flops_per_step": tim["attention_flops"] / n_layers,
                         "kernel_ms_per_step": round(tim["attention_ms"] / n_layers, 3)}}
+    if not full:  # device path only (N > 1: the same workload at H = 1, for the curve)
+        host.close()
+        fab.close()
+        del q, k, v, out
+        torch.cuda.empty_cache()
+        return res
     try:  # e2e through the host-buffer entry point
         qh, kh, vh = q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory()
         oh = torch.empty(out.shape, dtype=out.dtype).pin_memory()
@@ -681,6 +687,14 @@ def run_spava_arm(args):
 
     extra = {}
     cpu = None
+    if world > 1 and not args.no_extras:
+        # the same workload on ONE GPU (H = 1, local fabric), measured here on rank 0 while
+        # the other ranks wait: the N = 1 point of this config's strong-scaling curve (the
+        # driver's N = 1 run is BASELINE's C1 line, a different workload than C3)
+        try:
+            extra["same_workload_n1"] = sweep_line(torch, spava, name, local, stream, flush, 3, pk, full=False)
+        except Exception as e:  # pragma: no cover
+            extra["same_workload_n1"] = {"error": str(e)[:200]}
     if world == 1 and not args.no_extras:
         n = g["n"]
         gen = torch.Generator(device=dev).manual_seed(4321)

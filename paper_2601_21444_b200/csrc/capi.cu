@@ -1592,9 +1592,19 @@ int stage_chunks(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEd
   return SPAVA_OK;
 }
 
+// dev A/B: SPAVA_SERIAL_SCORE=1 runs the scorer on the caller's stream (no overlap) in the
+// device-resident layer
+bool serial_score_env() {
+  static const bool v = [] {
+    const char* e = getenv("SPAVA_SERIAL_SCORE");
+    return e && atoi(e) != 0;
+  }();
+  return v;
+}
+
 int layer_impl(spava_host* H, const HostBufs& b, cudaStream_t st, const CopyEdges& cp) {
   spava_fabric* F = H->fab;
-  cudaStream_t ss = H->serial ? st : cp.on ? H->side_lo : H->side;
+  cudaStream_t ss = (H->serial || (!cp.on && serial_score_env())) ? st : cp.on ? H->side_lo : H->side;
   auto merged = [&](cudaStream_t s) -> cudaError_t {
     return cp.on ? cudaEventRecord(H->ev_oc[2 * cp.n], s) : cudaSuccess;
   };
