@@ -9,36 +9,66 @@ CUDA_DEVICE_MAX_CONNECTIONS and the process layout are under the test's control.
 
 Every rank runs LAYERS consecutive layers (different inputs each, so the epoch flags and
 the slot-release protocol are exercised) and checks its outputs and passing indices
-bit-identical against the local fabric (spava_sim_layer) on the same inputs.
+bit-identical against the local fabric (spava_sim_layer) on the same inputs, and layer 0
+against the C oracle (indices exact, outputs within the bf16 bar).
 Prints one line "PEER_OK <rank|all> <layers>" on success.
 """
 import os
 import sys
 
+import numpy as np
 import torch
 
+from oracle import oracle as O
 from paper_2601_21444_b200 import spava
+from tests.util import ATOL_BF16_OUT, RTOL_L2_BF16, host_local, max_abs, randn, rel_l2
 
 N_V, N_T, L_A, L_P, HQ, HKV = 5000, 64, 64, 160, 8, 2
 ZIGZAG = os.environ.get("PEER_ZIGZAG", "1") == "1"
 
 
-def inputs(world, layer):
-    """Per-host [anchor | lo | hi | query] buffers of one layer (same on every rank)."""
-    cfg = spava.LayerConfig.make(N_V, N_T, world, L_A, L_P, HQ, HKV, zigzag=ZIGZAG)
+def global_inputs(world, layer):
+    """One layer's global padded Q/K/V (bf16-valued fp32, the same on every rank)."""
     plan = spava.make_plan(N_V, N_T, world, L_A, L_P, ZIGZAG)
+    n_pad = L_A + 2 * world * plan.l_b + N_T
+    rng = np.random.default_rng(1000 + layer)
+    return plan, randn(rng, n_pad, HQ * 128), randn(rng, n_pad, HKV * 128), randn(rng, n_pad, HKV * 128)
+
+
+def inputs(world, layer):
+    """Per-host [anchor | lo | hi | query] rows of one consistent global sequence (the
+    reference's split_context of the same Q/K/V), on cuda:0."""
+    cfg = spava.LayerConfig.make(N_V, N_T, world, L_A, L_P, HQ, HKV, zigzag=ZIGZAG)
+    plan, Q, K, V = global_inputs(world, layer)
     rows = L_A + 2 * plan.l_b + N_T
-    g = torch.Generator(device="cuda:0").manual_seed(1000 + layer)
+    qoff = spava.query_offset(plan)
     qs, ks, vs = [], [], []
-    for _ in range(world):
-        qs.append(torch.randn(rows, HQ * 128, device="cuda:0", generator=g).to(torch.bfloat16))
-        ks.append(torch.randn(rows, HKV * 128, device="cuda:0", generator=g).to(torch.bfloat16))
-        vs.append(torch.randn(rows, HKV * 128, device="cuda:0", generator=g).to(torch.bfloat16))
+    for h in range(world):
+        lo, hi = spava.virtual_pair(plan, h)
+        for X, lst in ((Q, qs), (K, ks), (V, vs)):
+            lst.append(torch.from_numpy(host_local(X, L_A, plan.l_b, lo, hi, qoff, N_T)).to("cuda:0")
+                       .to(torch.bfloat16))
     return cfg, rows, qs, ks, vs
 
 
+def oracle_layer(world, layer):
+    """C oracle (oracle/spava_oracle.c, the reference's run_host restated) of one layer:
+    per host the passing indices of (lo, hi) and the expected [anchor | lo | hi | query]
+    output rows.  Test infrastructure only (the checker)."""
+    plan, Q, K, V = global_inputs(world, layer)
+    want = O.spava_layer(Q, K, V, N_V, N_T, world, L_A, L_P, HQ, HKV, 128, zigzag=ZIGZAG)
+    res = []
+    for h in range(world):
+        lo, hi = spava.virtual_pair(plan, h)
+        out = np.concatenate([want["anchor"], want["blocks"][lo], want["blocks"][hi], want["query"]])
+        res.append((np.stack([want["sel"][lo], want["sel"][hi]]), out))
+    return res
+
+
 def reference(world, layers):
-    """Local fabric (the in-process GatherFabric) outputs, per layer and host."""
+    """Local fabric (the in-process GatherFabric) outputs, per layer and host; layer 0 of
+    the local fabric is also checked against the C oracle (indices exact, outputs within
+    the bf16 bar), so the peer ranks' bit-identity to it is parity with the reference."""
     res = []
     for layer in range(layers):
         cfg, rows, qs, ks, vs = inputs(world, layer)
@@ -53,7 +83,11 @@ def reference(world, layers):
         for h in hs:
             h.close()
         fab.close()
+    ORACLE.extend(oracle_layer(world, 0))
     return res
+
+
+ORACLE = []  # layer 0 per host: (indices [2, l_p], output rows) from the C oracle
 
 
 def check(ref, layer, rank, out, sel):
@@ -63,6 +97,14 @@ def check(ref, layer, rank, out, sel):
     if not torch.equal(out, want_out):
         d = (out.float() - want_out.float()).abs().max().item()
         raise AssertionError(f"layer {layer} rank {rank}: output differs (max {d})")
+    if layer == 0 and ORACLE:  # the peer rank against the reference algorithm directly
+        o_sel, o_out = ORACLE[rank]
+        if not np.array_equal(sel.cpu().numpy(), o_sel):
+            raise AssertionError(f"rank {rank}: passing indices differ from the oracle")
+        got = out.float().cpu().numpy()
+        if max_abs(got, o_out) >= ATOL_BF16_OUT or rel_l2(got, o_out) >= RTOL_L2_BF16:
+            raise AssertionError(f"rank {rank}: output vs oracle max {max_abs(got, o_out)} "
+                                 f"rel-L2 {rel_l2(got, o_out)}")
 
 
 def inproc(world, layers):

@@ -4,7 +4,9 @@ The pass rounds are stored by the select gather kernel and the qpartial round by
 query split-merge kernel straight into every peer's exchange slot; epoch flags (stream
 memory operations) order them.  Parity bar: every rank's layer output and passing
 indices bit-identical to the local fabric (the reference's in-process GatherFabric
-order, simhost.cpp:61-166) over several consecutive layers.
+order, simhost.cpp:61-166) over several consecutive layers, and the first layer's against
+the C oracle of the whole layer on the same global inputs (indices exact, outputs within
+the bf16 bar) -- every rank checked against the reference algorithm directly.
 
 Only one GPU is available, so the ranks share cuda:0: either WORLD fabrics in one
 process on WORLD streams, or WORLD real processes that map each other's exchange
