@@ -170,3 +170,32 @@ def h2d_two(fine_d2h=True):
 
 
 print(f"27 H2D copies over 2 streams + fine D2H: {h2d_two(True):.3f} ms; + 1 D2H copy: {h2d_two(False):.3f} ms")
+
+
+
+def d2h_pieces(piece):
+    with torch.cuda.stream(s2):
+        for a, e in chunks(o_b):
+            for x in range(a, e, piece):
+                y = min(e, x + piece)
+                ho[x:y].copy_(do[x:y], non_blocking=True)
+            torch.cuda.current_stream().record_event()
+
+
+def h2d_pieces(piece):
+    with torch.cuda.stream(s1):
+        half = kv_b // 2
+        for a, e in ((0, half), (kv_b, kv_b + half), (half, kv_b), (kv_b + half, 2 * kv_b)):
+            dk[a:e].copy_(hk[a:e], non_blocking=True)
+            torch.cuda.current_stream().record_event()
+        for a, e in chunks(q_b):
+            for x in range(a, e, piece):
+                y = min(e, x + piece)
+                dq[x:y].copy_(hq[x:y], non_blocking=True)
+            torch.cuda.current_stream().record_event()
+
+
+for piece in (1 << 20, 2 << 20, 4 << 20):
+    print(f"pipeline H2D + D2H chunks split in {piece >> 20} MB pieces: "
+          f"{timed(lambda: (h2d(True), d2h_pieces(piece))):.3f} ms; both split: "
+          f"{timed(lambda: (h2d_pieces(piece), d2h_pieces(piece))):.3f} ms")
