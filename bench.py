@@ -478,8 +478,9 @@ def run_spava_arm(args):
     from paper_2601_21444_b200 import spava
 
     rank, world, local = dist_env()
-    if world != args.gpus and world > 1:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world} (N > 1 runs one process per GPU "
+                         "under torch.distributed.run)")
     torch.cuda.set_device(local)
     all_cpus = os.sched_getaffinity(0)
     numa_cpus = bind_gpu_numa(local)
