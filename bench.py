@@ -218,9 +218,12 @@ def dist_env():
 
 
 def job_config(args, world):
-    """(config name, cfg, geometry) of the job: C1 on one GPU (BASELINE configs[1]); the
-    128K-token C3 (north_star's scaling target) at N > 1 unless --config says otherwise."""
-    name = args.config or ("C1" if max(world, args.gpus) == 1 else "C3")
+    """(config name, cfg, geometry) of the job, unless --config says otherwise: the BASELINE
+    config quoted at that GPU count -- C1 at N = 1 and 2 (configs[1]: "32K tokens, 1 B200 vs
+    2 GPUs"), C2 at N = 3..4 (configs[2]: 64K tokens, "4 and 8 B200"), the 128K-token C3 at
+    N > 4 (configs[3], north_star's 1 -> 8 scaling target)."""
+    n = max(world, args.gpus)
+    name = args.config or ("C1" if n <= 2 else "C2" if n <= 4 else "C3")
     cfg = CONFIGS[name]
     return name, cfg, geometry(cfg, max(world, args.gpus))
 
@@ -691,7 +694,7 @@ def run_spava_arm(args):
     if world > 1 and not args.no_extras:
         # the same workload on ONE GPU (H = 1, local fabric), measured here on rank 0 while
         # the other ranks wait: the N = 1 point of this config's strong-scaling curve (the
-        # driver's N = 1 run is BASELINE's C1 line, a different workload than C3)
+        # driver's N = 1 run is BASELINE's C1 line; at N > 2 the job is C2 / C3)
         try:
             extra["same_workload_n1"] = sweep_line(torch, spava, name, local, stream, flush, 3, pk, full=False)
         except Exception as e:  # pragma: no cover
@@ -866,7 +869,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
-                    help="default: C1 on one GPU, C3 (128K tokens) at N > 1")
+                    help="default: C1 at N <= 2, C2 at N <= 4, C3 (128K tokens) above")
     ap.add_argument("--impl", default="spava", choices=["spava", "reference"])
     ap.add_argument("--fabric", default="peer", choices=["peer", "nccl"],
                     help="N>1 exchange: NVLink peer stores + flags (default) or NCCL allgathers")
