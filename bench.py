@@ -806,12 +806,13 @@ def run_spava_arm(args):
             del xw, w_qkv, w_o, w_1, w_2, wsd
         except Exception as e:  # pragma: no cover
             extra["decoder_layer"] = {"error": str(e)[:200]}
-        # BASELINE's sweep config (C4, 7B 256K) and the 128K scaling config (C3) at H = 1
+        # BASELINE's sweep config (C4, 7B 256K) and the N = 4 / N = 8 configs (C2 64K, C3 128K)
+        # at H = 1: the N = 1 points of the multi-GPU lines' workloads
         if not args.no_sweep:
             del q, k, v, out, out_timed
             torch.cuda.empty_cache()
             extra["sweep_h1"] = {}
-            for sname in ("C3", "C4"):
+            for sname in ("C2", "C3", "C4"):
                 try:
                     extra["sweep_h1"][sname] = sweep_line(torch, spava, sname, local, stream, flush, 3, pk)
                 except Exception as e:  # pragma: no cover
@@ -876,7 +877,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds for the CPU baseline sample")
     ap.add_argument("--ref-max-s", type=float, default=150.0,
                     help="reference arm: run the whole layer when it fits this estimate, else a sample")
-    ap.add_argument("--no-sweep", action="store_true", help="skip the C3/C4 H=1 lines (N=1)")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the C2/C3/C4 H=1 lines (N=1)")
     ap.add_argument("--no-self-check", action="store_true", help="N>1: skip the one-GPU comparison")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
