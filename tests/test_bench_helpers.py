@@ -42,3 +42,15 @@ def test_zigzag_balanced_naive_not(name, hosts):
                  (2 * g["n_t"] ** 2 if h == hosts - 1 else 0)) * d
         assert zz[h] - extra == ref_attn_flops_per_host(g["l_a"], g["l_b"], g["l_p"], hosts, d)
     assert max(nv) / min(nv) > 1.05 and max(zz) / min(zz) < 1.01
+
+
+@pytest.mark.parametrize("n,want", [(1, "C1"), (2, "C1"), (4, "C2"), (8, "C3")])
+def test_default_workload_per_gpu_count(n, want):
+    """bench.py's default job at N GPUs is the BASELINE config quoted at that count
+    (configs[1] C1 at 1 / 2, configs[2] C2 at 4, configs[3] C3 at 8), split over N hosts."""
+    import argparse
+
+    args = argparse.Namespace(config=None, gpus=n)
+    name, cfg, g = bench.job_config(args, n)
+    assert name == want and cfg is bench.CONFIGS[want] and g["hosts"] == n
+    assert bench.job_config(argparse.Namespace(config="C4", gpus=n), n)[0] == "C4"
